@@ -1,0 +1,196 @@
+/* fs_b200.h — C-ABI of the B200 flow+blend path (the drop-in boundary).
+ *
+ * One extern "C" entry point per function of the reference's hot-path API
+ * (namespace flowstitch, /root/reference/proj/include/flowstitch/*.hpp), each
+ * citing the declaration it replaces.  Plain pointers and sizes only; the
+ * data layouts are the reference's value types:
+ *   image : float[w*h*ch] interleaved, ch = 1 or 3, plus uint8 valid[w*h]
+ *           (image.hpp:32-64, ImageBuf)
+ *   mask  : uint8[w*h] (image.hpp:17-28, Mask)
+ *   label : uint8[w*h] in {0 Outside, 1 Area1, 2 Area2, 3 Area3} and
+ *           int64 counts[4] (image.hpp:66-77, Region/RegionPartition)
+ *   flow  : float[w*h*2] interleaved (dx, dy), uint8 valid[w*h] (flow.hpp:15-34)
+ *   field : double[w*h] (blend_field.hpp:12-28, DistanceField / BlendField)
+ * Buffers may live in host or device memory (CUDA unified addressing tells the
+ * two apart); host buffers are staged through the device inside the call.
+ * `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls with
+ * host outputs return after the result is in place; calls whose outputs are
+ * all device pointers are asynchronous on `stream`.
+ *
+ * Errors: the reference throws (errors.hpp:10-37); here every call returns a
+ * status and fs_last_error() gives the thread-local message, with the same
+ * wording as the reference's exception where the reference tests match on it.
+ * There is no CPU fallback: without a usable sm_100 GPU every compute entry
+ * point returns FS_ERR_CUDA.
+ */
+#ifndef FS_B200_H
+#define FS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FS_OK = 0,
+    FS_ERR_CONTRACT = 1,     /* ContractError  (errors.hpp:10-14) */
+    FS_ERR_EMPTY_REGION = 2, /* EmptyRegionError (errors.hpp:34-38) */
+    FS_ERR_LAYOUT = 3,       /* LayoutError (errors.hpp:28-32) */
+    FS_ERR_CUDA = 4,         /* device missing / CUDA failure */
+    FS_ERR_OOM = 5,          /* device allocation failed */
+    FS_ERR_UNSUPPORTED = 6,  /* parameter outside what the kernels implement */
+    FS_ERR_IO = 7,           /* IoError (errors.hpp:16-20) */
+    FS_ERR_FORMAT = 8        /* FormatError (errors.hpp:22-26) */
+} fs_status;
+
+/* FlowParams (flow.hpp:36-44); defaults 4 / 8 / 3 / 1e-4 / 2. */
+typedef struct {
+    int levels;
+    int window_radius;
+    int iterations_per_level;
+    double min_eigen_eps;
+    int smoothing_passes;
+} fs_flow_params;
+
+/* BlendParams (blender.hpp:12-17); defaults 10 / 0.05. */
+typedef struct {
+    double k_softmax_sharpness;
+    double k_flow_mag_coef;
+} fs_blend_params;
+
+/* PairStats subset (pipeline.hpp:30-38) filled by the fold. */
+typedef struct {
+    int64_t overlap_pixels;
+    double mean_flow_mag_ltor;
+    double mean_flow_mag_rtol;
+    double flow_seconds;  /* device time of the pair's flow stage */
+    double blend_seconds; /* device time of blend field + blend + compose */
+    int32_t crop_box[4];  /* x0, y0, w, h of the Area3 bounding box */
+} fs_pair_stats;
+
+const char* fs_last_error(void);
+int fs_abi_version(void);
+/* 1 if a usable sm_100 device is present (does not initialise the others). */
+int fs_device_available(void);
+void fs_default_flow_params(fs_flow_params* p);
+void fs_default_blend_params(fs_blend_params* p);
+
+/* ---- imagecore (image.hpp:94-108) ---- */
+/* to_gray (image.hpp:94): out is w*h floats. */
+fs_status fs_to_gray(const float* img, int w, int h, int ch, float* out, void* stream);
+/* bilinear_sample (image.hpp:98), batched: xy = n (x, y) pairs, out = n*ch. */
+fs_status fs_bilinear_sample(const float* img, const uint8_t* valid, int w, int h, int ch,
+                             const double* xy, int n, float* out, void* stream);
+/* compute_partition (image.hpp:100). */
+fs_status fs_compute_partition(const uint8_t* mask_l, const uint8_t* mask_r, int w, int h,
+                               uint8_t* label, int64_t* counts, void* stream);
+/* crop_overlap (image.hpp:103): box = {offset_x, offset_y, w, h}; pass out =
+ * NULL to query the box, then call again with buffers of box[2]*box[3]. */
+fs_status fs_crop_overlap(const float* img, const uint8_t* valid, int w, int h, int ch,
+                          const uint8_t* label, const int64_t* counts, float* out,
+                          uint8_t* out_valid, int* box, void* stream);
+/* place_on_canvas (image.hpp:107-108); valid may be NULL (all valid). */
+fs_status fs_place_on_canvas(const float* img, const uint8_t* valid, int w, int h, int ch,
+                             int offset_x, int offset_y, int canvas_w, int canvas_h, float* out,
+                             uint8_t* out_valid, void* stream);
+
+/* ---- optflow (flow.hpp:46-66) ---- */
+/* pyramid depth for a w x h level 0 (flow.hpp:46-48) */
+int fs_pyramid_depth(int w, int h, int levels);
+/* build_pyramid (flow.hpp:48): levels concatenated, level 0 first. */
+fs_status fs_build_pyramid(const float* gray, int w, int h, int levels, float* out, int* depth,
+                           void* stream);
+/* dense_pyr_lk (flow.hpp:52) */
+fs_status fs_dense_pyr_lk(const float* from, const float* to, int w, int h,
+                          const fs_flow_params* params, float* vec, uint8_t* valid,
+                          void* stream);
+/* bidirectional_flow (flow.hpp:56-58): returns {LtoR, RtoL}. */
+fs_status fs_bidirectional_flow(const float* overlapped_l, const float* overlapped_r, int w,
+                                int h, int ch, const fs_flow_params* params, float* vec_ltor,
+                                uint8_t* valid_ltor, float* vec_rtol, uint8_t* valid_rtol,
+                                void* stream);
+/* flow_magnitude (flow.hpp:61) */
+fs_status fs_flow_magnitude(const float* vec, int w, int h, float* out, void* stream);
+/* embed_flow (flow.hpp:65-66) */
+fs_status fs_embed_flow(const float* vec, const uint8_t* valid, int w, int h, int offset_x,
+                        int offset_y, int canvas_w, int canvas_h, float* out_vec,
+                        uint8_t* out_valid, void* stream);
+
+/* ---- blendfield (blend_field.hpp:30-34) ---- */
+/* distance_transform (blend_field.hpp:32) */
+fs_status fs_distance_transform(const uint8_t* mask, int w, int h, double* out, void* stream);
+/* compute_blend (blend_field.hpp:34) */
+fs_status fs_compute_blend(const uint8_t* label, const int64_t* counts, int w, int h, double* b,
+                           void* stream);
+
+/* ---- blender (blender.hpp:19-46) ---- */
+/* softmax_weights (blender.hpp:21-23): scalar, evaluated with the kernels'
+ * own per-pixel routine (host copy of the same source). */
+void fs_softmax_weights(double blend_l, double blend_r, double mag_rtol, double mag_ltor,
+                        const fs_blend_params* params, double* sl, double* sr);
+/* blend_pair (blender.hpp:30-33): all inputs canvas-sized. */
+fs_status fs_blend_pair(const float* l, const uint8_t* valid_l, const float* r,
+                        const uint8_t* valid_r, int w, int h, int ch, const float* flow_ltor,
+                        const float* flow_rtol, const double* blend, const uint8_t* label,
+                        const fs_blend_params* params, float* out, uint8_t* out_valid,
+                        void* stream);
+/* feather_blend (blender.hpp:36-37) */
+fs_status fs_feather_blend(const float* l, const uint8_t* valid_l, const float* r,
+                           const uint8_t* valid_r, int w, int h, int ch, const double* blend,
+                           const uint8_t* label, float* out, uint8_t* out_valid, void* stream);
+/* warp_constituents (blender.hpp:42-46) */
+fs_status fs_warp_constituents(const float* l, const uint8_t* valid_l, const float* r,
+                               const uint8_t* valid_r, int w, int h, int ch,
+                               const float* flow_ltor, const float* flow_rtol,
+                               const double* blend, const uint8_t* label, float* out_l,
+                               uint8_t* out_valid_l, float* out_r, uint8_t* out_valid_r,
+                               void* stream);
+
+/* ---- pipeline fold (pipeline.hpp:63-67) ---- */
+/* stitch_placed: images[i] is dims[2i] x dims[2i+1] x ch at offsets[2i],
+ * offsets[2i+1]; valids may be NULL or hold NULL entries (all valid).  The
+ * whole fold runs device-resident; stats (optional) gets n-1 entries. */
+fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* const* valids,
+                           const int* dims, const int* offsets, int ch, int canvas_w,
+                           int canvas_h, const fs_flow_params* flow, const fs_blend_params* blend,
+                           float* out, uint8_t* out_valid, fs_pair_stats* stats, void* stream);
+
+/* ---- production path: planned, graph-captured fold over 8-bit views ----
+ * A plan fixes the layout (view sizes, offsets, fold order, canvas) and owns
+ * all device memory.  Executions recompute everything per call (partition,
+ * crop, pyramid, flow, distance transform, blend, compose, quantise) and
+ * verify on the device that the views' masks still produce the planned Area3
+ * boxes; fs_plan_check() reports a mismatch.  Views are RGBA8 (alpha >= 128
+ * valid, image.hpp:86-88) and the output canvas is RGBA8 (alpha = valid). */
+typedef struct fs_plan_s* fs_plan;
+fs_status fs_plan_create(fs_plan* plan, int device, int n, const int* dims, const int* offsets,
+                         int canvas_w, int canvas_h, const fs_flow_params* flow,
+                         const fs_blend_params* blend, const uint8_t* const* views_rgba);
+/* device pointer of view k's RGBA8 buffer (dims[2k]*dims[2k+1]*4 bytes) */
+void* fs_plan_view_buffer(fs_plan plan, int k);
+/* device pointer of the RGBA8 output canvas (canvas_w*canvas_h*4 bytes) */
+void* fs_plan_output_buffer(fs_plan plan);
+/* run the fold on the views already in the plan's device buffers (async) */
+fs_status fs_plan_execute(fs_plan plan, void* stream);
+/* end-to-end: copy host (or device) views in, fold, copy the canvas out */
+fs_status fs_plan_execute_host(fs_plan plan, const uint8_t* const* views_rgba, uint8_t* out_rgba,
+                               void* stream);
+/* after the stream is synchronised: FS_OK or the first device-side error */
+fs_status fs_plan_check(fs_plan plan);
+/* number of kernel launches of one execution (for accounting) */
+int fs_plan_launch_count(fs_plan plan);
+/* fold geometry: for fold k (1..n-1) the Area3 box {x0,y0,w,h} and depth */
+fs_status fs_plan_fold_info(fs_plan plan, int k, int* box, int* depth);
+void fs_plan_destroy(fs_plan plan);
+
+/* ---- runtime (parallel.hpp:9-18): kept for drop-in completeness; the GPU
+ * path has no host worker pool, so these only record the value. ---- */
+void fs_set_thread_count(int n);
+int fs_thread_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FS_B200_H */

@@ -1,0 +1,182 @@
+// Device-side data types and kernel declarations of the B200 flow+blend path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "fs_math.cuh"
+
+namespace fs {
+
+constexpr int kInfSq = 0x3fffffff;  // "no seed" squared distance (exceeds any canvas d^2)
+
+struct Rect {
+    int x0 = 0, y0 = 0, w = 0, h = 0;
+    __host__ __device__ int x1() const { return x0 + w; }
+    __host__ __device__ int y1() const { return y0 + h; }
+    __host__ __device__ bool contains(int x, int y) const {
+        return x >= x0 && y >= y0 && x < x0 + w && y < y0 + h;
+    }
+    __host__ __device__ long long area() const { return (long long)w * h; }
+};
+
+// The running panorama: RGB in float4 (w unused), validity in its own plane.
+// Pixel values of invalid pixels are undefined; every reader masks by valid.
+struct Canvas {
+    float4* rgb;
+    uint8_t* valid;
+    int w, h, ch;
+};
+
+// A placed view in 8-bit RGBA (alpha >= 128 is valid, src/image.cpp:38-39),
+// value = byte * (1/255) exactly as load_image (src/image.cpp:31-37).
+struct ViewU8 {
+    const uchar4* px;
+    Rect rect;  // canvas placement
+    __device__ __forceinline__ bool valid_at(int x, int y) const {
+        if (!rect.contains(x, y)) return false;
+        return px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)].w >= 128;
+    }
+    __device__ __forceinline__ float4 value_at(int x, int y) const {
+        uchar4 p = px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)];
+        const float s = 1.0f / 255.0f;
+        return make_float4(p.x * s, p.y * s, p.z * s, 0.f);
+    }
+};
+
+// A placed view in float (ImageBuf semantics): float4 rgb + u8 valid.
+struct ViewF4 {
+    const float4* px;
+    const uint8_t* valid;
+    Rect rect;
+    __device__ __forceinline__ bool valid_at(int x, int y) const {
+        if (!rect.contains(x, y)) return false;
+        return valid[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)] != 0;
+    }
+    __device__ __forceinline__ float4 value_at(int x, int y) const {
+        return px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)];
+    }
+};
+
+// Per-fold device bookkeeping (written by the partition kernel).
+struct FoldStats {
+    unsigned long long cnt2;  // Area2 pixels
+    unsigned long long cnt3;  // Area3 pixels
+    int bx0, by0, bx1, by1;   // Area3 bbox (inclusive max), init (INT_MAX, INT_MAX, -1, -1)
+    unsigned int edt_fail;    // bounded-domain EDT certificate failed (bit per mask)
+    unsigned int box_mismatch;
+};
+
+struct CanvasCount {
+    unsigned long long valid_count;  // |pano valid|
+};
+
+// ---- flow (per level) ----
+struct LkDir {
+    const float* F;        // from-level
+    const float* T;        // to-level
+    const float2* fin;     // level flow in (mode 1) or coarse flow (mode 2)
+    const uint8_t* okin;   // level ok in (mode 1) or coarse ok (mode 2)
+    float2* fout;
+    uint8_t* okout;
+};
+struct LkArgs {
+    LkDir d[2];
+    int ndir;
+    int w, h;    // level dims
+    int cw, ch;  // coarse dims (mode 2)
+    double sx, sy;
+    int mode;    // 0 zero, 1 flow-in, 2 upsample-from-coarse
+    int r;
+    int tw, th;  // output tile
+    double eig_thresh;
+    float flow_cap;
+};
+
+struct SmoothArgs {
+    const float2* fin[2];
+    float2* fout[2];
+    const uint8_t* ok[2];
+    uint8_t* valid_out[2];  // written when final_cap > 0 (finalisation)
+    int ndir, w, h, passes;  // passes: 1 or 2
+    float final_cap;         // > 0: level-0 finalisation (cap + valid)
+};
+
+// ---- distance transform ----
+// Seed masks of the fold: Area1 = pano valid && !view valid, Area2 = view
+// valid && !pano valid (src/blend_field.cpp:100-104 on src/image.cpp:115-132).
+template <class V>
+struct FoldMask {
+    const uint8_t* pvalid;
+    int cw;
+    V view;
+    int which;  // 1 or 2
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        bool pv = pvalid[(size_t)y * cw + x] != 0;
+        bool rv = view.valid_at(x, y);
+        return which == 1 ? (pv && !rv) : (rv && !pv);
+    }
+};
+// A plain u8 mask plane (standalone distance_transform).
+struct PlaneMask {
+    const uint8_t* m;
+    int w;
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        return m[(size_t)y * w + x] != 0;
+    }
+};
+
+// Region-label plane compared against one label (compute_blend's m1/m2).
+struct LabelMask {
+    const uint8_t* label;
+    int w;
+    uint8_t value;
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        return label[(size_t)y * w + x] == value;
+    }
+};
+
+template <class M>
+struct EdtJob {
+    M mask;
+    int which = 0;   // 0 plain, 1 Area1, 2 Area2 (selects the "have" test)
+    int active = 0;
+    Rect W, C;       // seed domain, output box (C inside W)
+    int vfirst = 1;  // 1: columns 1-D first, envelope along rows
+    int* g = nullptr;           // pass-1 output, laid out line-contiguous for pass 2
+    int* summ_first = nullptr;  // [nseg][nlines]
+    int* summ_last = nullptr;
+    int* stack = nullptr;       // [pass-2 lines][sites]
+    int* out = nullptr;         // squared distance on C, row-major C.w
+    int e_left = 1, e_right = 1, e_top = 1, e_bottom = 1;  // W side == seed-bbox side
+    int check = 0;
+};
+
+namespace launch {
+void init();  // one-time kernel attributes (call before any graph capture)
+template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
+template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
+template <class V> void partition(const Canvas&, const V&, FoldStats*, cudaStream_t);
+void check_box(FoldStats*, const Rect&, cudaStream_t);
+template <class V>
+void crop_gray(const Canvas&, const V&, const Rect&, float*, float*, cudaStream_t);
+void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
+                int nimg, cudaStream_t);
+cudaError_t lk_iter(const LkArgs&, cudaStream_t);
+int lk_max_radius();
+void smooth(const SmoothArgs&, cudaStream_t);
+void finalize_flow(const SmoothArgs&, cudaStream_t);
+template <class M>
+void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, const CanvasCount*, cudaStream_t);
+template <class V>
+void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
+                 const int*, const FoldStats*, const CanvasCount*, double, double, float4*,
+                 cudaStream_t);
+template <class V>
+void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
+             cudaStream_t);
+void quantize(const Canvas&, uchar4*, cudaStream_t);
+void export_float(const Canvas&, float*, uint8_t*, cudaStream_t);
+}  // namespace launch
+
+}  // namespace fs

@@ -1,0 +1,344 @@
+// Host orchestration of the B200 flow+blend path (see fs_engine.cuh).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "fs_engine.cuh"
+
+namespace fs {
+
+void raise(fs_status code, const std::string& msg) { throw Error{code, msg}; }
+
+std::string& last_error_slot() {
+    thread_local std::string msg;
+    return msg;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) raise(FS_ERR_OOM, std::string("device allocation failed: ") + what);
+    if (e != cudaSuccess) raise(FS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ensure_device() {
+    static int ok = -1;
+    if (ok < 0) {
+        int n = 0;
+        ok = 0;
+        if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) {
+            int dev = 0, major = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+            ok = major == 10 ? 1 : 0;
+        }
+        cudaGetLastError();
+    }
+    if (!ok) raise(FS_ERR_CUDA, "no sm_100 (B200) CUDA device available; the flow+blend path has no CPU fallback");
+    launch::init();
+}
+
+// src/flow.cpp:15-21 (same messages)
+void validate_flow_params(const fs_flow_params& p) {
+    if (p.levels < 1) raise(FS_ERR_CONTRACT, "FlowParams: levels must be >= 1");
+    if (p.window_radius < 1) raise(FS_ERR_CONTRACT, "FlowParams: window_radius must be >= 1");
+    if (p.iterations_per_level < 1)
+        raise(FS_ERR_CONTRACT, "FlowParams: iterations_per_level must be >= 1");
+    if (!(p.min_eigen_eps > 0.0)) raise(FS_ERR_CONTRACT, "FlowParams: min_eigen_eps must be > 0");
+    if (p.smoothing_passes < 0) raise(FS_ERR_CONTRACT, "FlowParams: smoothing_passes must be >= 0");
+    if (p.window_radius > launch::lk_max_radius())
+        raise(FS_ERR_UNSUPPORTED, "FlowParams: window_radius above the kernel's maximum (48)");
+}
+
+// src/blender.cpp:11-16
+void validate_blend_params(const fs_blend_params& p) {
+    if (!(p.k_softmax_sharpness > 0.0) || !std::isfinite(p.k_softmax_sharpness))
+        raise(FS_ERR_CONTRACT, "BlendParams: k_softmax_sharpness must be finite and > 0");
+    if (p.k_flow_mag_coef < 0.0 || !std::isfinite(p.k_flow_mag_coef))
+        raise(FS_ERR_CONTRACT, "BlendParams: k_flow_mag_coef must be finite and >= 0");
+}
+
+int pyramid_depth(int w, int h, int levels) {
+    int usable = 1;
+    while (usable < levels && w / 2 >= 8 && h / 2 >= 8) {
+        w /= 2;
+        h /= 2;
+        ++usable;
+    }
+    return usable;
+}
+
+// ---------------------------------------------------------------------------
+void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
+    w = w_;
+    h = h_;
+    ndir = ndir_;
+    depth = pyramid_depth(w, h, levels);
+    lv.clear();
+    int pw = w, ph = h;
+    for (int l = 0; l < depth; ++l) {
+        lv.push_back({pw, ph});
+        pw = std::max(1, pw / 2);
+        ph = std::max(1, ph / 2);
+    }
+    for (int i = 0; i < 2; ++i) {
+        pyr[i].assign(depth, nullptr);
+        for (int l = 1; l < depth; ++l) pyr[i][l] = a.take<float>((size_t)lv[l].w * lv[l].h);
+    }
+    size_t n = (size_t)w * h;
+    for (int d = 0; d < ndir; ++d)
+        for (int q = 0; q < 2; ++q) {
+            fb[d][q] = a.take<float2>(n);
+            ok[d][q] = a.take<uint8_t>(n);
+        }
+}
+
+int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_params& p,
+                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s) {
+    int launches = 0;
+    ws.pyr[0][0] = const_cast<float*>(g0);
+    ws.pyr[1][0] = const_cast<float*>(g1);
+    for (int l = 1; l < ws.depth; ++l) {
+        launch::downsample(ws.pyr[0][l - 1], ws.pyr[1][l - 1], ws.pyr[0][l], ws.pyr[1][l],
+                           ws.lv[l - 1].w, ws.lv[l - 1].h, 2, s);
+        ++launches;
+    }
+    const int r = p.window_radius;
+    const double win_area = static_cast<double>(2 * r + 1) * (2 * r + 1);
+    const double eig_thresh = p.min_eigen_eps * win_area;  // src/flow.cpp:205-206
+    int fcur = 0, okcur = 0;
+    for (int l = ws.depth - 1; l >= 0; --l) {
+        const Level L = ws.lv[l];
+        for (int it = 0; it < p.iterations_per_level; ++it) {
+            LkArgs a{};
+            a.ndir = ws.ndir;
+            a.w = L.w;
+            a.h = L.h;
+            a.mode = it > 0 ? 1 : (l == ws.depth - 1 ? 0 : 2);
+            if (a.mode == 2) {
+                a.cw = ws.lv[l + 1].w;
+                a.ch = ws.lv[l + 1].h;
+                a.sx = static_cast<double>(a.cw) / L.w;  // src/flow.cpp:145-146
+                a.sy = static_cast<double>(a.ch) / L.h;
+            }
+            a.r = r;
+            a.th = 64;
+            a.eig_thresh = eig_thresh;
+            a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
+            for (int d = 0; d < ws.ndir; ++d) {
+                int src = ws.ndir == 1 ? 0 : d;
+                a.d[d].F = ws.pyr[src][l];
+                a.d[d].T = ws.pyr[1 - src][l];
+                a.d[d].fin = ws.fb[d][fcur];
+                a.d[d].okin = ws.ok[d][okcur];
+                a.d[d].fout = ws.fb[d][fcur ^ 1];
+                a.d[d].okout = ws.ok[d][okcur ^ 1];
+            }
+            FS_CK(launch::lk_iter(a, s));
+            ++launches;
+            fcur ^= 1;
+            okcur ^= 1;
+        }
+        int P = p.smoothing_passes;
+        while (P > 0) {
+            int passes = std::min(2, P);
+            P -= passes;
+            bool fin = (l == 0 && P == 0);
+            SmoothArgs a{};
+            a.ndir = ws.ndir;
+            a.w = L.w;
+            a.h = L.h;
+            a.passes = passes;
+            a.final_cap = fin ? static_cast<float>(std::max(ws.w, ws.h)) : 0.f;
+            for (int d = 0; d < ws.ndir; ++d) {
+                a.fin[d] = ws.fb[d][fcur];
+                a.fout[d] = fin ? out_vec[d] : ws.fb[d][fcur ^ 1];
+                a.ok[d] = ws.ok[d][okcur];
+                a.valid_out[d] = out_valid[d];
+            }
+            launch::smooth(a, s);
+            ++launches;
+            if (!fin) fcur ^= 1;
+        }
+        if (l == 0 && p.smoothing_passes == 0) {
+            SmoothArgs a{};
+            a.ndir = ws.ndir;
+            a.w = L.w;
+            a.h = L.h;
+            a.final_cap = static_cast<float>(std::max(ws.w, ws.h));
+            for (int d = 0; d < ws.ndir; ++d) {
+                a.fin[d] = ws.fb[d][fcur];
+                a.fout[d] = out_vec[d];
+                a.ok[d] = ws.ok[d][okcur];
+                a.valid_out[d] = out_valid[d];
+            }
+            launch::finalize_flow(a, s);
+            ++launches;
+        }
+    }
+    FS_CK(cudaGetLastError());
+    return launches;
+}
+
+// ---------------------------------------------------------------------------
+static Rect intersect(const Rect& a, const Rect& b) {
+    int x0 = std::max(a.x0, b.x0), y0 = std::max(a.y0, b.y0);
+    int x1 = std::min(a.x1(), b.x1()), y1 = std::min(a.y1(), b.y1());
+    Rect r;
+    r.x0 = x0;
+    r.y0 = y0;
+    r.w = std::max(0, x1 - x0);
+    r.h = std::max(0, y1 - y0);
+    return r;
+}
+
+EdtPlan edt_plan(const Rect& C, const Rect& E, bool full_domain) {
+    EdtPlan p;
+    p.C = C;
+    p.E = E;
+    p.vfirst = C.h >= C.w ? 1 : 0;
+    if (full_domain) {
+        p.W = E;
+        return p;
+    }
+    int M = std::min(C.w, C.h) + 8;
+    Rect grown;
+    grown.x0 = C.x0 - M;
+    grown.y0 = C.y0 - M;
+    grown.w = C.w + 2 * M;
+    grown.h = C.h + 2 * M;
+    p.W = intersect(grown, E);
+    p.e_left = p.W.x0 == E.x0;
+    p.e_right = p.W.x1() == E.x1();
+    p.e_top = p.W.y0 == E.y0;
+    p.e_bottom = p.W.y1() == E.y1();
+    p.check = !(p.e_left && p.e_right && p.e_top && p.e_bottom);
+    return p;
+}
+
+void EdtWS::layout(Arena& a, const Rect& C, const Rect& E) {
+    bool vfirst = C.h >= C.w;
+    size_t gsz = vfirst ? (size_t)C.h * E.w : (size_t)C.w * E.h;
+    size_t nlines = vfirst ? E.w : E.h;
+    size_t nseg = ((vfirst ? E.h : E.w) + 63) / 64;
+    g = a.take<int>(gsz);
+    stack = a.take<int>(gsz);
+    summ_first = a.take<int>(nlines * nseg);
+    summ_last = a.take<int>(nlines * nseg);
+    out = a.take<int>((size_t)C.w * C.h);
+}
+
+template <class V>
+void FoldWS<V>::layout(Arena& a, const Rect& box_, const Rect& pano_bbox, const Rect& view_rect,
+                       const fs_flow_params& fp) {
+    box = box_;
+    E1 = pano_bbox;
+    E2 = view_rect;
+    size_t n = (size_t)box.w * box.h;
+    gray[0] = a.take<float>(n);
+    gray[1] = a.take<float>(n);
+    flow.layout(a, box.w, box.h, fp.levels, 2);
+    depth = flow.depth;
+    for (int d = 0; d < 2; ++d) {
+        fvec[d] = a.take<float2>(n);
+        fvalid[d] = a.take<uint8_t>(n);
+    }
+    edt[0].layout(a, box, E1);
+    edt[1].layout(a, box, E2);
+    blended = a.take<float4>(n);
+    st = a.take<FoldStats>(1);
+    replan_edt();
+}
+
+template <class V>
+void FoldWS<V>::replan_edt() {
+    ep[0] = edt_plan(box, E1, full_domain);
+    ep[1] = edt_plan(box, E2, full_domain);
+}
+
+__global__ void k_init_stats(FoldStats* st) {
+    st->cnt2 = 0;
+    st->cnt3 = 0;
+    st->bx0 = INT_MAX;
+    st->by0 = INT_MAX;
+    st->bx1 = -1;
+    st->by1 = -1;
+    st->edt_fail = 0;
+    st->box_mismatch = 0;
+}
+__global__ void k_init_count(CanvasCount* cc) { cc->valid_count = 0; }
+
+void init_stats(FoldStats* st, cudaStream_t s) { k_init_stats<<<1, 1, 0, s>>>(st); }
+void init_count(CanvasCount* cc, cudaStream_t s) { k_init_count<<<1, 1, 0, s>>>(cc); }
+
+template <class V>
+int fold_enqueue_pre(FoldWS<V>& f, const Canvas& cv, const V& view, cudaStream_t s) {
+    init_stats(f.st, s);
+    launch::partition(cv, view, f.st, s);
+    return 2;
+}
+
+template <class V>
+int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+                          const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
+                          cudaEvent_t ev_flow1) {
+    int launches = 0;
+    launch::check_box(f.st, f.box, s);
+    launch::crop_gray(cv, view, f.box, f.gray[0], f.gray[1], s);
+    launches += 2;
+    if (ev_flow0) FS_CK(cudaEventRecord(ev_flow0, s));
+    launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s);
+    if (ev_flow1) FS_CK(cudaEventRecord(ev_flow1, s));
+    EdtJob<FoldMask<V>> j[2];
+    for (int m = 0; m < 2; ++m) {
+        const EdtPlan& P = f.ep[m];
+        j[m].mask = FoldMask<V>{cv.valid, cv.w, view, m + 1};
+        j[m].which = m + 1;
+        j[m].active = 1;
+        j[m].W = P.W;
+        j[m].C = P.C;
+        j[m].vfirst = P.vfirst;
+        j[m].g = f.edt[m].g;
+        j[m].summ_first = f.edt[m].summ_first;
+        j[m].summ_last = f.edt[m].summ_last;
+        j[m].stack = f.edt[m].stack;
+        j[m].out = f.edt[m].out;
+        j[m].e_left = P.e_left;
+        j[m].e_right = P.e_right;
+        j[m].e_top = P.e_top;
+        j[m].e_bottom = P.e_bottom;
+        j[m].check = P.check;
+    }
+    launch::edt(j[0], j[1], f.st, cc, s);
+    launches += 3;
+    FS_CK(cudaGetLastError());
+    return launches;
+}
+
+template <class V>
+int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+                       const fs_blend_params& bp, cudaStream_t s) {
+    int launches = 0;
+    launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out, f.st,
+                        cc, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
+    launch::compose(cv, view, f.box, f.blended, cc, f.st, s);
+    launches += 3;
+    FS_CK(cudaGetLastError());
+    return launches;
+}
+
+template struct FoldWS<ViewU8>;
+template struct FoldWS<ViewF4>;
+template int fold_enqueue_pre<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&, cudaStream_t);
+template int fold_enqueue_pre<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&, cudaStream_t);
+template int fold_enqueue_flow_edt<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
+                                           CanvasCount*, const fs_flow_params&, cudaStream_t,
+                                           cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_flow_edt<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
+                                           CanvasCount*, const fs_flow_params&, cudaStream_t,
+                                           cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
+                                        CanvasCount*, const fs_blend_params&, cudaStream_t);
+template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
+                                        CanvasCount*, const fs_blend_params&, cudaStream_t);
+
+}  // namespace fs

@@ -1,0 +1,111 @@
+// Host-side orchestration of the B200 flow+blend path: the pyramidal flow
+// driver (src/flow.cpp:194-314), the fold step (src/pipeline.cpp:153-207) and
+// the planned, graph-captured fold.  Internal C++ API; the boundary is the
+// C-ABI in include/fs_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fs_b200.h"
+#include "fs_device.cuh"
+
+namespace fs {
+
+struct Error {
+    fs_status code;
+    std::string msg;
+};
+[[noreturn]] void raise(fs_status code, const std::string& msg);
+std::string& last_error_slot();  // thread-local message behind fs_last_error()
+void cuda_check(cudaError_t e, const char* what);
+#define FS_CK(x) ::fs::cuda_check((x), #x)
+
+void validate_flow_params(const fs_flow_params& p);    // src/flow.cpp:15-21
+void validate_blend_params(const fs_blend_params& p);  // src/blender.cpp:11-16
+int pyramid_depth(int w, int h, int levels);           // src/flow.cpp:178-185
+void ensure_device();                                  // throws FS_ERR_CUDA without sm_100
+
+// Bump allocator: run the layout once with base == nullptr to size it, then
+// again over one device allocation.
+struct Arena {
+    char* base = nullptr;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+struct Level {
+    int w, h;
+};
+
+// Workspace of one (bi)directional pyramidal LK problem on a w x h crop.
+struct FlowWS {
+    int w = 0, h = 0, depth = 0, ndir = 0;
+    std::vector<Level> lv;
+    std::vector<float*> pyr[2];  // level pointers (level 0 = caller's gray buffers)
+    float2* fb[2][2] = {};       // [dir][pingpong] level flow
+    uint8_t* ok[2][2] = {};
+    void layout(Arena& a, int w, int h, int levels, int ndir);
+};
+// Enqueue the whole coarse-to-fine flow on stream s.  ndir = 1: from=g0,
+// to=g1.  ndir = 2: dir 0 is L->R (from g0), dir 1 is R->L (from g1).
+// Outputs are the reference FlowField layouts (interleaved dx,dy + valid).
+int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_params& p,
+                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s);
+
+// Distance-transform job layout for one seed mask of a fold.
+struct EdtPlan {
+    Rect W, C, E;
+    int vfirst = 1;
+    int e_left = 1, e_right = 1, e_top = 1, e_bottom = 1;
+    int check = 0;
+};
+EdtPlan edt_plan(const Rect& C, const Rect& E, bool full_domain);
+struct EdtWS {
+    int *g = nullptr, *summ_first = nullptr, *summ_last = nullptr, *stack = nullptr,
+        *out = nullptr;
+    void layout(Arena& a, const Rect& C, const Rect& E);  // sized for the full domain E
+};
+
+// One fold (pano = L, view k = R) on a planned Area3 box.
+template <class V>
+struct FoldWS {
+    Rect box, E1, E2;
+    EdtPlan ep[2];
+    bool full_domain = false;
+    int depth = 0;
+    float* gray[2] = {};
+    FlowWS flow;
+    float2* fvec[2] = {};
+    uint8_t* fvalid[2] = {};
+    EdtWS edt[2];
+    float4* blended = nullptr;
+    FoldStats* st = nullptr;
+    void layout(Arena& a, const Rect& box, const Rect& pano_bbox, const Rect& view_rect,
+                const fs_flow_params& fp);
+    void replan_edt();
+};
+template <class V>
+int fold_enqueue_pre(FoldWS<V>& f, const Canvas& cv, const V& view, cudaStream_t s);
+// check box, crop+gray, pyramid, flow (both directions), distance transforms
+template <class V>
+int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+                          const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
+                          cudaEvent_t ev_flow1);
+// Code 1 blend on Area3 + composition of the view onto the canvas
+template <class V>
+int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+                       const fs_blend_params& bp, cudaStream_t s);
+
+void init_stats(FoldStats* st, cudaStream_t s);
+void init_count(CanvasCount* cc, cudaStream_t s);
+
+}  // namespace fs

@@ -1,0 +1,839 @@
+// sm_100a kernels of the flow+blend hot path (K0-K8 of SURVEY.md §2.2).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false ...
+// -fmad=false keeps every float/double expression that mirrors the reference
+// un-contracted, which is what makes the outputs bit-comparable with the
+// reference's Release build (no -march, hence no FMA).
+#include <climits>
+
+#include "fs_device.cuh"
+
+namespace fs {
+
+// ============================================================================
+// K0 — placement, partition statistics, crop + gray
+// ============================================================================
+
+// src/image.cpp:164-177 (place_on_canvas) for the first view of a fold: the
+// canvas valid plane was cleared; the view's pixels and validity are written
+// at its offset and its valid pixels counted.
+template <class V>
+__global__ void k_place_view(Canvas cv, V view, CanvasCount* count) {
+    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    int y = view.rect.y0 + blockIdx.y;
+    int n = 0;
+    if (x < view.rect.x1()) {
+        size_t p = (size_t)y * cv.w + x;
+        bool v = view.valid_at(x, y);
+        cv.rgb[p] = view.value_at(x, y);
+        cv.valid[p] = v ? 1 : 0;
+        n = v;
+    }
+    n = __reduce_add_sync(0xffffffffu, n);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(&count->valid_count, (unsigned long long)n);
+}
+
+// src/image.cpp:115-132 + :140-148, restricted to the view rectangle (Area2 and
+// Area3 live there): Area2/Area3 counts and the Area3 bounding box.
+template <class V>
+__global__ void k_partition(const uint8_t* __restrict__ pvalid, int cw, V view, FoldStats* st) {
+    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    int y = view.rect.y0 + blockIdx.y;
+    bool a2 = false, a3 = false;
+    if (x < view.rect.x1() && view.valid_at(x, y)) {
+        bool l = pvalid[(size_t)y * cw + x] != 0;
+        a3 = l;
+        a2 = !l;
+    }
+    unsigned m3 = __ballot_sync(0xffffffffu, a3);
+    unsigned m2 = __ballot_sync(0xffffffffu, a2);
+    int lane = threadIdx.x & 31;
+    int minx = a3 ? x : INT_MAX, maxx = a3 ? x : -1;
+    minx = __reduce_min_sync(0xffffffffu, minx);
+    maxx = __reduce_max_sync(0xffffffffu, maxx);
+    if (lane == 0) {
+        if (m2) atomicAdd(&st->cnt2, (unsigned long long)__popc(m2));
+        if (m3) {
+            atomicAdd(&st->cnt3, (unsigned long long)__popc(m3));
+            atomicMin(&st->bx0, minx);
+            atomicMax(&st->bx1, maxx);
+            atomicMin(&st->by0, y);
+            atomicMax(&st->by1, y);
+        }
+    }
+}
+
+// Checks the device-measured Area3 box against the planned one.
+__global__ void k_check_box(FoldStats* st, Rect planned) {
+    bool ok = st->cnt3 > 0 && st->bx0 == planned.x0 && st->by0 == planned.y0 &&
+              st->bx1 == planned.x1() - 1 && st->by1 == planned.y1() - 1;
+    if (!ok) st->box_mismatch = 1;
+}
+
+// src/image.cpp:134-162 then src/image.cpp:70-83: crop of both sides over the
+// Area3 box (invalid pixels zeroed) and their gray levels.
+template <class V>
+__global__ void k_crop_gray(Canvas cv, V view, Rect box, float* __restrict__ gl,
+                            float* __restrict__ gr) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int j = blockIdx.y;
+    if (i >= box.w) return;
+    int x = box.x0 + i, y = box.y0 + j;
+    size_t p = (size_t)y * cv.w + x;
+    float4 l = cv.valid[p] ? cv.rgb[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 r = view.valid_at(x, y) ? view.value_at(x, y) : make_float4(0.f, 0.f, 0.f, 0.f);
+    size_t o = (size_t)j * box.w + i;
+    gl[o] = cv.ch == 3 ? gray3(l.x, l.y, l.z) : l.x;
+    gr[o] = cv.ch == 3 ? gray3(r.x, r.y, r.z) : r.x;
+}
+
+// ============================================================================
+// K1 — Gaussian pyramid (src/flow.cpp:29-56): one level of both images.
+// out(i,j) = sum_t k[t] * tmp(2i, clamp(2j+t)),  tmp(x,y) = sum_s k[s] in(clamp(x+s), y)
+// with float accumulation in tap order, exactly as the reference's two passes.
+// ============================================================================
+__global__ void k_downsample(const float* __restrict__ in0, const float* __restrict__ in1,
+                             float* __restrict__ out0, float* __restrict__ out1, int w, int h,
+                             int ow, int oh) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= ow || j >= oh) return;
+    const float* in = blockIdx.z == 0 ? in0 : in1;
+    float* out = blockIdx.z == 0 ? out0 : out1;
+    int xs[5];
+#pragma unroll
+    for (int s = -2; s <= 2; ++s) xs[s + 2] = clampi(2 * i + s, 0, w - 1);
+    float acc = 0.f;
+#pragma unroll
+    for (int t = -2; t <= 2; ++t) {
+        const float* row = in + (size_t)clampi(2 * j + t, 0, h - 1) * w;
+        float tmp = 0.f;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) tmp += binom_tap(s - 2) * __ldg(row + xs[s]);
+        acc += binom_tap(t) * tmp;
+    }
+    out[(size_t)j * ow + i] = acc;
+}
+
+// ============================================================================
+// K2+K3 — one fused LK iteration (src/flow.cpp:225-291), both directions.
+//
+// A CTA owns an output tile of tw columns x th rows and sweeps its input rows
+// top to bottom.  Thread c owns input column x0-r+c and keeps the five
+// vertical running window sums (double) of its column in registers; the
+// per-pixel inputs (gx, gy, dt) of the last 2r+1 rows live in a shared-memory
+// ring so the row leaving the window is subtracted exactly.  Every LK_NB rows
+// the column sums are staged in shared memory and turned into horizontal
+// (2r+1)-tap sums by sliding runs of LK_S outputs, then solved.  Products are
+// exact in double (float x float); the window sums are double, so they agree
+// with the reference's double prefix tables to ~1e-12 relative.  Upsampling of
+// the coarser level's flow (src/flow.cpp:138-170) is fused into the first
+// iteration of each level (MODE 2).
+// ============================================================================
+constexpr int LK_NB = 8;
+constexpr int LK_S = 8;
+
+__host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
+__host__ inline size_t lk_smem_bytes(int iw, int r) {
+    size_t ring = (size_t)(2 * r + 1) * iw * 3 * sizeof(float);
+    ring = (ring + 15) & ~size_t(15);
+    return ring + (size_t)LK_NB * 5 * lk_iwp(iw) * sizeof(double);
+}
+
+template <int MODE>
+__device__ __forceinline__ float2 lk_flow_at(const LkArgs& a, const LkDir& D, int x, int y) {
+    if (MODE == 0) return make_float2(0.f, 0.f);
+    if (MODE == 1) return D.fin[(size_t)y * a.w + x];
+    UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
+    float2 f00 = D.fin[(size_t)t.y0 * a.cw + t.x0], f10 = D.fin[(size_t)t.y0 * a.cw + t.x1];
+    float2 f01 = D.fin[(size_t)t.y1 * a.cw + t.x0], f11 = D.fin[(size_t)t.y1 * a.cw + t.x1];
+    return make_float2(up_combine(t, f00.x, f10.x, f01.x, f11.x),
+                       up_combine(t, f00.y, f10.y, f01.y, f11.y));
+}
+
+template <int MODE>
+__device__ __forceinline__ uint8_t lk_ok_at(const LkArgs& a, const LkDir& D, int x, int y) {
+    if (MODE == 0) return 0;
+    if (MODE == 1) return D.okin[(size_t)y * a.w + x];
+    UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
+    return D.okin[(size_t)t.yn * a.cw + t.xn];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_lk_iter(LkArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int IW = blockDim.x;
+    const int r = a.r, K = 2 * r + 1;
+    const int IWP = lk_iwp(IW);
+    size_t ring_bytes = ((size_t)K * IW * 3 * sizeof(float) + 15) & ~size_t(15);
+    float* ring = reinterpret_cast<float*>(smem);
+    double* vbuf = reinterpret_cast<double*>(smem + ring_bytes);
+    const LkDir& D = a.d[blockIdx.z];
+    const int w = a.w, h = a.h;
+    const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
+    const int c = threadIdx.x;
+    const int x = x0 - r + c;
+    const bool xin = x >= 0 && x < w;
+    const int xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
+
+    for (int k = 0; k < K; ++k) {
+        float* rs = ring + ((size_t)k * IW + c) * 3;
+        rs[0] = 0.f;
+        rs[1] = 0.f;
+        rs[2] = 0.f;
+    }
+    double V0 = 0.0, V1 = 0.0, V2 = 0.0, V3 = 0.0, V4 = 0.0;
+    const int yo_end = min(y0 + a.th, h);
+    const int ystart = y0 - r;
+    const int yend = yo_end + r;
+    const int nruns = (a.tw + LK_S - 1) / LK_S;
+
+    for (int ybase = ystart; ybase < yend; ybase += LK_NB) {
+        // ---- phase 1: per-column products and vertical running sums ----
+#pragma unroll 2
+        for (int b = 0; b < LK_NB; ++b) {
+            const int y = ybase + b;
+            float gx = 0.f, gy = 0.f, dt = 0.f;
+            if (xin && y >= 0 && y < h && y < yend) {
+                const float* Frow = D.F + (size_t)y * w;
+                const float fc = __ldg(Frow + x);
+                gx = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));
+                gy = 0.5f * (__ldg(D.F + (size_t)min(y + 1, h - 1) * w + x) -
+                             __ldg(D.F + (size_t)max(y - 1, 0) * w + x));
+                float2 f = lk_flow_at<MODE>(a, D, x, y);
+                LevelTap t = level_tap(w, h, (double)((float)x + f.x), (double)((float)y + f.y));
+                float warped = level_combine(t, __ldg(D.T + (size_t)t.y0 * w + t.x0),
+                                             __ldg(D.T + (size_t)t.y0 * w + t.x1),
+                                             __ldg(D.T + (size_t)t.y1 * w + t.x0),
+                                             __ldg(D.T + (size_t)t.y1 * w + t.x1));
+                dt = warped - fc;
+            }
+            const int slot = (y - ystart) % K;
+            float* rs = ring + ((size_t)slot * IW + c) * 3;
+            const double ogx = rs[0], ogy = rs[1], odt = rs[2];
+            rs[0] = gx;
+            rs[1] = gy;
+            rs[2] = dt;
+            const double ix = gx, iy = gy, tt = dt;
+            V0 = (V0 + ix * ix) - ogx * ogx;
+            V1 = (V1 + ix * iy) - ogx * ogy;
+            V2 = (V2 + iy * iy) - ogy * ogy;
+            V3 = (V3 + ix * tt) - ogx * odt;
+            V4 = (V4 + iy * tt) - ogy * odt;
+            const int cc = c + (c >> 3);
+            double* vb = vbuf + (size_t)b * 5 * IWP + cc;
+            vb[0] = V0;
+            vb[IWP] = V1;
+            vb[2 * IWP] = V2;
+            vb[3 * IWP] = V3;
+            vb[4 * IWP] = V4;
+        }
+        __syncthreads();
+        // ---- phase 2: horizontal sliding sums + 2x2 solve ----
+        for (int item = threadIdx.x; item < LK_NB * nruns; item += blockDim.x) {
+            const int b = item / nruns, run = item - b * nruns;
+            const int yo = ybase + b - r;
+            if (yo < y0 || yo >= yo_end) continue;
+            const int cs = run * LK_S;
+            const int nout = min(LK_S, a.tw - cs);
+            const double* vb = vbuf + (size_t)b * 5 * IWP;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+            for (int cc = cs; cc <= cs + 2 * r; ++cc) {
+                const int ci = cc + (cc >> 3);
+                s0 += vb[ci];
+                s1 += vb[IWP + ci];
+                s2 += vb[2 * IWP + ci];
+                s3 += vb[3 * IWP + ci];
+                s4 += vb[4 * IWP + ci];
+            }
+            for (int s = 0; s < nout; ++s) {
+                if (s > 0) {
+                    const int ca = cs + 2 * r + s, cb = cs + s - 1;
+                    const int ia = ca + (ca >> 3), ib = cb + (cb >> 3);
+                    s0 = (s0 + vb[ia]) - vb[ib];
+                    s1 = (s1 + vb[IWP + ia]) - vb[IWP + ib];
+                    s2 = (s2 + vb[2 * IWP + ia]) - vb[2 * IWP + ib];
+                    s3 = (s3 + vb[3 * IWP + ia]) - vb[3 * IWP + ib];
+                    s4 = (s4 + vb[4 * IWP + ia]) - vb[4 * IWP + ib];
+                }
+                const int xo = x0 + cs + s;
+                if (xo >= w) break;
+                float2 f = lk_flow_at<MODE>(a, D, xo, yo);
+                uint8_t ok = lk_ok_at<MODE>(a, D, xo, yo);
+                if (lk_solve(s0, s1, s2, s3, s4, a.eig_thresh, a.flow_cap, f.x, f.y)) ok = 1;
+                const size_t o = (size_t)yo * w + xo;
+                D.fout[o] = f;
+                D.okout[o] = ok;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================
+// K4 — flow smoothing (src/flow.cpp:113-130, 294-297): one or two fused 3x3
+// truncated-mean passes of dx and dy; at level 0 also the final cap and the
+// valid plane (src/flow.cpp:300-313).
+// ============================================================================
+constexpr int SM_TX = 32, SM_TY = 8;
+
+__global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
+    __shared__ float2 src[SM_TY + 4][SM_TX + 4];
+    __shared__ float2 p1[SM_TY + 2][SM_TX + 2];
+    const int d = blockIdx.z;
+    const float2* fin = a.fin[d];
+    const int w = a.w, h = a.h;
+    const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
+    const int halo = a.passes == 2 ? 2 : 1;
+    for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 4) * (SM_TX + 4);
+         t += SM_TX * SM_TY) {
+        int ly = t / (SM_TX + 4), lx = t - ly * (SM_TX + 4);
+        int gx = bx - 2 + lx, gy = by - 2 + ly;
+        src[ly][lx] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? fin[(size_t)gy * w + gx]
+                                                               : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    if (halo == 2) {
+        for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 2) * (SM_TX + 2);
+             t += SM_TX * SM_TY) {
+            int ly = t / (SM_TX + 2), lx = t - ly * (SM_TX + 2);
+            int gx = bx - 1 + lx, gy = by - 1 + ly;
+            float2 v = make_float2(0.f, 0.f);
+            if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+                double ax = 0.0, ay = 0.0;
+                int n = 0;
+                for (int dj = -1; dj <= 1; ++dj)
+                    for (int di = -1; di <= 1; ++di) {
+                        int xx = gx + di, yy = gy + dj;
+                        if (xx < 0 || xx >= w || yy < 0 || yy >= h) continue;
+                        float2 s = src[ly + 1 + dj][lx + 1 + di];
+                        ax += s.x;
+                        ay += s.y;
+                        ++n;
+                    }
+                v = make_float2((float)(ax / n), (float)(ay / n));
+            }
+            p1[ly][lx] = v;
+        }
+        __syncthreads();
+    }
+    const int gx = bx + threadIdx.x, gy = by + threadIdx.y;
+    if (gx >= w || gy >= h) return;
+    double ax = 0.0, ay = 0.0;
+    int n = 0;
+    for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+            int xx = gx + di, yy = gy + dj;
+            if (xx < 0 || xx >= w || yy < 0 || yy >= h) continue;
+            float2 s = halo == 2 ? p1[threadIdx.y + 1 + dj][threadIdx.x + 1 + di]
+                                 : src[threadIdx.y + 2 + dj][threadIdx.x + 2 + di];
+            ax += s.x;
+            ay += s.y;
+            ++n;
+        }
+    float vx = (float)(ax / n), vy = (float)(ay / n);
+    size_t o = (size_t)gy * w + gx;
+    if (a.final_cap > 0.f) {
+        final_cap(a.final_cap, vx, vy);
+        a.valid_out[d][o] = a.ok[d][o];
+    }
+    a.fout[d][o] = make_float2(vx, vy);
+}
+
+// Level-0 finalisation when smoothing_passes == 0 (src/flow.cpp:300-313).
+__global__ void k_finalize_flow(SmoothArgs a) {
+    const int d = blockIdx.z;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int n = a.w * a.h;
+    if (i >= n) return;
+    float2 f = a.fin[d][i];
+    final_cap(a.final_cap, f.x, f.y);
+    a.fout[d][i] = f;
+    a.valid_out[d][i] = a.ok[d][i];
+}
+
+// ============================================================================
+// K5/K6 — exact Euclidean distance transform (src/blend_field.cpp:19-86).
+//
+// Squared distances are integers, so any exact method reproduces the
+// reference's sqrt(dt) bit for bit.  The transform is separable: pass 1 is a
+// 1-D nearest-seed search along one axis (segmented so long lines run in
+// parallel), pass 2 the lower envelope of parabolas along the other axis
+// (Felzenszwalb, with exact int64 intersection comparisons, pruned at the
+// nearest on-line seeds which dominate everything behind them).  Work is
+// restricted to a domain W around the output box C; a per-pixel certificate
+// proves that no seed outside W could be closer, otherwise the fold is
+// flagged and recomputed on the full domain by the host.
+// ============================================================================
+constexpr int EDT_SEG = 64;
+
+template <class M>
+__device__ __forceinline__ void edt_line_xy(const EdtJob<M>& J, int line, int p, int& x, int& y) {
+    if (J.vfirst) {
+        x = J.W.x0 + line;
+        y = J.W.y0 + p;
+    } else {
+        x = J.W.x0 + p;
+        y = J.W.y0 + line;
+    }
+}
+
+// pass 1a: first/last seed position per (line, segment)
+template <class M>
+__global__ void k_edt_summ(EdtJob<M> J0, EdtJob<M> J1) {
+    const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
+    if (!J.active) return;
+    const int nlines = J.vfirst ? J.W.w : J.W.h;
+    const int len = J.vfirst ? J.W.h : J.W.w;
+    const int nseg = (len + EDT_SEG - 1) / EDT_SEG;
+    int line = blockIdx.x * blockDim.x + threadIdx.x;
+    int seg = blockIdx.y;
+    if (line >= nlines || seg >= nseg) return;
+    int first = -1, last = -1;
+    int p0 = seg * EDT_SEG, p1 = min(len, p0 + EDT_SEG);
+    for (int p = p0; p < p1; ++p) {
+        int x, y;
+        edt_line_xy(J, line, p, x, y);
+        if (J.mask(x, y)) {
+            if (first < 0) first = p;
+            last = p;
+        }
+    }
+    J.summ_first[(size_t)seg * nlines + line] = first;
+    J.summ_last[(size_t)seg * nlines + line] = last;
+}
+
+// pass 1b: squared 1-D distance for every output position of every line
+template <class M>
+__global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
+    const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
+    if (!J.active) return;
+    const int nlines = J.vfirst ? J.W.w : J.W.h;
+    const int len = J.vfirst ? J.W.h : J.W.w;
+    const int nseg = (len + EDT_SEG - 1) / EDT_SEG;
+    const int oa = J.vfirst ? J.C.y0 - J.W.y0 : J.C.x0 - J.W.x0;
+    const int ob = oa + (J.vfirst ? J.C.h : J.C.w);
+    int line = blockIdx.x * blockDim.x + threadIdx.x;
+    int seg = oa / EDT_SEG + blockIdx.y;
+    if (line >= nlines || seg >= nseg) return;
+    int p0 = max(seg * EDT_SEG, oa), p1 = min(min(len, (seg + 1) * EDT_SEG), ob);
+    if (p0 >= p1) return;
+    const int s0 = seg * EDT_SEG, s1 = min(len, (seg + 1) * EDT_SEG);
+    // nearest seed before the segment and after it
+    int prev = INT_MIN / 2, next = INT_MAX / 2;
+    for (int s = seg - 1; s >= 0; --s) {
+        int l = J.summ_last[(size_t)s * nlines + line];
+        if (l >= 0) {
+            prev = l;
+            break;
+        }
+    }
+    for (int s = seg + 1; s < nseg; ++s) {
+        int f = J.summ_first[(size_t)s * nlines + line];
+        if (f >= 0) {
+            next = f;
+            break;
+        }
+    }
+    const int gstride = J.vfirst ? J.W.w : J.W.h;  // pass-2 line length
+    // forward: last seed <= p
+    int last = prev;
+    for (int p = s0; p < p1; ++p) {
+        int x, y;
+        edt_line_xy(J, line, p, x, y);
+        if (J.mask(x, y)) last = p;
+        if (p >= p0) {
+            long long d = (long long)p - last;
+            J.g[(size_t)(p - oa) * gstride + line] = d < 46341 ? (int)(d * d) : kInfSq;
+        }
+    }
+    // backward: first seed >= p
+    int nxt = next;
+    for (int p = s1 - 1; p >= p0; --p) {
+        int x, y;
+        edt_line_xy(J, line, p, x, y);
+        if (J.mask(x, y)) nxt = p;
+        if (p < p1) {
+            long long d = (long long)nxt - p;
+            int dd = d < 46341 ? (int)(d * d) : kInfSq;
+            int* gp = J.g + (size_t)(p - oa) * gstride + line;
+            if (dd < *gp) *gp = dd;
+        }
+    }
+}
+
+// pass 2: lower envelope along the other axis for each output line
+template <class M>
+__global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
+                               const CanvasCount* cc) {
+    const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
+    if (!J.active) return;
+    const int nout_lines = J.vfirst ? J.C.h : J.C.w;
+    const int L = J.vfirst ? J.W.w : J.W.h;  // sites per line
+    int ol = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ol >= nout_lines) return;
+    const int* f = J.g + (size_t)ol * L;
+    int* stk = J.stack + (size_t)ol * L;
+    const int qa = J.vfirst ? J.C.x0 - J.W.x0 : J.C.y0 - J.W.y0;
+    const int qb = qa + (J.vfirst ? J.C.w : J.C.h);
+    // prune at the nearest on-line seeds (f == 0) around [qa, qb)
+    int lo = 0, hi = L - 1;
+    for (int s = qa; s >= 0; --s)
+        if (f[s] == 0) {
+            lo = s;
+            break;
+        }
+    for (int s = qb - 1; s < L; ++s)
+        if (f[s] == 0) {
+            hi = s;
+            break;
+        }
+    int n = 0;
+    for (int q = lo; q <= hi; ++q) {
+        long long fq = f[q];
+        if (fq >= kInfSq) continue;
+        while (n >= 2) {
+            // intersection (q, top) <= intersection (top, below) ?
+            int t = stk[n - 1], u = stk[n - 2];
+            long long ft = f[t], fu = f[u];
+            long long n1 = (fq + (long long)q * q) - (ft + (long long)t * t), d1 = 2LL * (q - t);
+            long long n2 = (ft + (long long)t * t) - (fu + (long long)u * u), d2 = 2LL * (t - u);
+            if (n1 * d2 <= n2 * d1)
+                --n;
+            else
+                break;
+        }
+        stk[n++] = q;
+    }
+    // certificate bound helpers
+    const bool have = J.which == 1   ? (cc->valid_count - st->cnt3) > 0
+                      : J.which == 2 ? st->cnt2 > 0
+                                     : true;
+    int k = 0;
+    bool fail = false;
+    for (int q = qa; q < qb; ++q) {
+        int dsq = kInfSq;
+        if (n > 0) {
+            while (k + 1 < n) {
+                int a0 = stk[k], a1 = stk[k + 1];
+                long long fa = f[a0], fb = f[a1];
+                long long num = (fb + (long long)a1 * a1) - (fa + (long long)a0 * a0);
+                long long den = 2LL * (a1 - a0);
+                if (num < (long long)q * den)
+                    ++k;
+                else
+                    break;
+            }
+            long long d = q - stk[k];
+            long long v = d * d + f[stk[k]];
+            dsq = v < kInfSq ? (int)v : kInfSq;
+        }
+        int x, y;
+        if (J.vfirst) {
+            x = J.W.x0 + q;
+            y = J.C.y0 + ol;
+        } else {
+            x = J.C.x0 + ol;
+            y = J.W.y0 + q;
+        }
+        J.out[(size_t)(y - J.C.y0) * J.C.w + (x - J.C.x0)] = dsq;
+        if (J.check && have) {
+            long long bnd = LLONG_MAX;
+            if (!J.e_left) bnd = min(bnd, (long long)(x - J.W.x0 + 1));
+            if (!J.e_right) bnd = min(bnd, (long long)(J.W.x1() - x));
+            if (!J.e_top) bnd = min(bnd, (long long)(y - J.W.y0 + 1));
+            if (!J.e_bottom) bnd = min(bnd, (long long)(J.W.y1() - y));
+            if (bnd != LLONG_MAX && (long long)dsq > bnd * bnd) fail = true;
+        }
+    }
+    if (fail) atomicOr((unsigned int*)&st->edt_fail, 1u << (blockIdx.z));
+}
+
+// ============================================================================
+// K7 — Code 1 blend (src/blender.cpp:72-91) on the Area3 pixels of the crop
+// box, and the composition onto the canvas (src/blender.cpp:66-71,
+// src/pipeline.cpp:201-204).
+// ============================================================================
+template <class S>
+__device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, double x, double y,
+                                             float out[3]) {
+    BiTap t = bi_tap(W, H, x, y);
+    bool v[4];
+    float4 px[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = s.valid_at(t.xs[k], t.ys[k]);
+        px[k] = v[k] ? s.value_at(t.xs[k], t.ys[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    double wsum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (v[k]) wsum += t.ws[k];
+    if (wsum <= 0.0) {
+        out[0] = out[1] = out[2] = 0.f;
+        return;
+    }
+    for (int c = 0; c < ch; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float pv = c == 0 ? px[k].x : (c == 1 ? px[k].y : px[k].z);
+            if (v[k]) acc += t.ws[k] * pv;
+        }
+        out[c] = (float)(acc / wsum);
+    }
+}
+
+struct CanvasSampler {
+    const float4* rgb;
+    const uint8_t* valid;
+    int w;
+    __device__ __forceinline__ bool valid_at(int x, int y) const {
+        return valid[(size_t)y * w + x] != 0;
+    }
+    __device__ __forceinline__ float4 value_at(int x, int y) const { return rgb[(size_t)y * w + x]; }
+};
+
+template <class V>
+__global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restrict__ flr,
+                              const float2* __restrict__ frl, const int* __restrict__ d1,
+                              const int* __restrict__ d2, const FoldStats* st,
+                              const CanvasCount* cc, double k, double coef,
+                              float4* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int j = blockIdx.y;
+    if (i >= box.w) return;
+    int x = box.x0 + i, y = box.y0 + j;
+    size_t p = (size_t)y * cv.w + x;
+    if (!(cv.valid[p] && view.valid_at(x, y))) return;  // not Area3
+    const bool have1 = (cc->valid_count - st->cnt3) > 0, have2 = st->cnt2 > 0;
+    size_t o = (size_t)j * box.w + i;
+    double blend_r = eq1_area3(have1, have2, d1[o], d2[o]);
+    double blend_l = 1.0 - blend_r;
+    float2 rl = frl[o], lr = flr[o];
+    float cl[3], cr[3];
+    CanvasSampler L{cv.rgb, cv.valid, cv.w};
+    bilinear_rgb(L, cv.w, cv.h, cv.ch, x + rl.x * (1.0 - blend_l), y + rl.y * (1.0 - blend_l), cl);
+    bilinear_rgb(view, cv.w, cv.h, cv.ch, x + lr.x * (1.0 - blend_r), y + lr.y * (1.0 - blend_r),
+                 cr);
+    double mag_rl = sqrt((double)rl.x * rl.x + (double)rl.y * rl.y);
+    double mag_lr = sqrt((double)lr.x * lr.x + (double)lr.y * lr.y);
+    double sl, sr;
+    softmax_weights(blend_l, blend_r, mag_rl, mag_lr, k, coef, sl, sr);
+    float res[3] = {0.f, 0.f, 0.f};
+    for (int c = 0; c < cv.ch; ++c) {
+        double v = cl[c] * sl + cr[c] * sr;
+        res[c] = (float)clampd(v, 0.0, 1.0);
+    }
+    out[o] = make_float4(res[0], res[1], res[2], 0.f);
+}
+
+template <class V>
+__global__ void k_compose(Canvas cv, V view, Rect box, const float4* __restrict__ blended,
+                          CanvasCount* cc, const FoldStats* st) {
+    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    int y = view.rect.y0 + blockIdx.y;
+    if (x >= view.rect.x1()) return;
+    if (!view.valid_at(x, y)) return;
+    size_t p = (size_t)y * cv.w + x;
+    if (cv.valid[p]) {  // Area3
+        cv.rgb[p] = blended[(size_t)(y - box.y0) * box.w + (x - box.x0)];
+    } else {  // Area2
+        cv.rgb[p] = view.value_at(x, y);
+        cv.valid[p] = 1;
+    }
+}
+
+// validity-only fold step used by the planner: pano valid |= view valid
+template <class V>
+__global__ void k_union_valid(Canvas cv, V view) {
+    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    int y = view.rect.y0 + blockIdx.y;
+    if (x >= view.rect.x1()) return;
+    if (view.valid_at(x, y)) cv.valid[(size_t)y * cv.w + x] = 1;
+}
+
+__global__ void k_count_update(CanvasCount* cc, const FoldStats* st) {
+    cc->valid_count += st->cnt2;
+}
+
+// K8 — 8-bit RGBA output (src/image.cpp:52-65): alpha = valid.
+__global__ void k_quantize(Canvas cv, uchar4* __restrict__ out) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y;
+    if (x >= cv.w) return;
+    size_t p = (size_t)y * cv.w + x;
+    uchar4 o = make_uchar4(0, 0, 0, 0);
+    if (cv.valid[p]) {
+        float4 v = cv.rgb[p];
+        o.x = quantize8(v.x);
+        o.y = cv.ch == 3 ? quantize8(v.y) : o.x;
+        o.z = cv.ch == 3 ? quantize8(v.z) : o.x;
+        o.w = 255;
+    }
+    out[p] = o;
+}
+
+// float output in ImageBuf layout (interleaved ch), invalid pixels are 0.
+__global__ void k_export_float(Canvas cv, float* __restrict__ out, uint8_t* __restrict__ vout) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y;
+    if (x >= cv.w) return;
+    size_t p = (size_t)y * cv.w + x;
+    bool v = cv.valid[p] != 0;
+    float4 px = v ? cv.rgb[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cv.ch == 3) {
+        out[p * 3] = px.x;
+        out[p * 3 + 1] = px.y;
+        out[p * 3 + 2] = px.z;
+    } else {
+        out[p] = px.x;
+    }
+    vout[p] = v;
+}
+
+// ============================================================================
+// Launch wrappers (host side)
+// ============================================================================
+namespace launch {
+
+static inline dim3 row_grid(int w, int h, int bx = 256) { return dim3((w + bx - 1) / bx, h); }
+
+template <class V>
+void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s) {
+    k_place_view<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, count);
+}
+template <class V>
+void partition(const Canvas& cv, const V& view, FoldStats* st, cudaStream_t s) {
+    k_partition<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv.valid, cv.w, view, st);
+}
+void check_box(FoldStats* st, const Rect& planned, cudaStream_t s) {
+    k_check_box<<<1, 1, 0, s>>>(st, planned);
+}
+template <class V>
+void crop_gray(const Canvas& cv, const V& view, const Rect& box, float* gl, float* gr,
+               cudaStream_t s) {
+    k_crop_gray<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, gl, gr);
+}
+void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
+                int nimg, cudaStream_t s) {
+    int ow = max(1, w / 2), oh = max(1, h / 2);
+    dim3 b(32, 8), g((ow + 31) / 32, (oh + 7) / 8, nimg);
+    k_downsample<<<g, b, 0, s>>>(in0, in1, out0, out1, w, h, ow, oh);
+}
+
+static bool lk_configured = false;
+void init() {
+    if (lk_configured) return;
+    cudaFuncSetAttribute(k_lk_iter<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lk_iter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lk_iter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    lk_configured = true;
+}
+cudaError_t lk_iter(const LkArgs& a0, cudaStream_t s) {
+    LkArgs a = a0;
+    int iw = 128;
+    a.tw = iw - 2 * a.r;
+    size_t smem = lk_smem_bytes(iw, a.r);
+    init();
+    dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
+    if (a.mode == 0)
+        k_lk_iter<0><<<g, iw, smem, s>>>(a);
+    else if (a.mode == 1)
+        k_lk_iter<1><<<g, iw, smem, s>>>(a);
+    else
+        k_lk_iter<2><<<g, iw, smem, s>>>(a);
+    return cudaGetLastError();
+}
+int lk_max_radius() { return 48; }
+
+void smooth(const SmoothArgs& a, cudaStream_t s) {
+    dim3 g((a.w + SM_TX - 1) / SM_TX, (a.h + SM_TY - 1) / SM_TY, a.ndir);
+    k_smooth<<<g, dim3(SM_TX, SM_TY), 0, s>>>(a);
+}
+void finalize_flow(const SmoothArgs& a, cudaStream_t s) {
+    int n = a.w * a.h;
+    k_finalize_flow<<<dim3((n + 255) / 256, 1, a.ndir), 256, 0, s>>>(a);
+}
+
+template <class M>
+void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, const CanvasCount* cc,
+         cudaStream_t s) {
+    const EdtJob<M>* js[2] = {&j0, &j1};
+    int max_lines = 0, max_seg = 0, max_oseg = 0, max_out = 0;
+    for (auto* j : js) {
+        if (!j->active) continue;
+        int nlines = j->vfirst ? j->W.w : j->W.h;
+        int len = j->vfirst ? j->W.h : j->W.w;
+        int oa = j->vfirst ? j->C.y0 - j->W.y0 : j->C.x0 - j->W.x0;
+        int olen = j->vfirst ? j->C.h : j->C.w;
+        int nseg = (len + EDT_SEG - 1) / EDT_SEG;
+        int oseg = (oa + olen - 1) / EDT_SEG - oa / EDT_SEG + 1;
+        max_lines = max(max_lines, nlines);
+        max_seg = max(max_seg, nseg);
+        max_oseg = max(max_oseg, oseg);
+        max_out = max(max_out, j->vfirst ? j->C.h : j->C.w);
+    }
+    if (max_lines == 0) return;
+    k_edt_summ<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
+    k_edt_line<M><<<dim3((max_lines + 127) / 128, max_oseg, 2), 128, 0, s>>>(j0, j1);
+    k_edt_envelope<M><<<dim3((max_out + 63) / 64, 1, 2), 64, 0, s>>>(j0, j1, st, cc);
+}
+
+template <class V>
+void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
+                 const float2* frl, const int* d1, const int* d2, const FoldStats* st,
+                 const CanvasCount* cc, double k, double coef, float4* out, cudaStream_t s) {
+    k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(cv, view, box, flr, frl, d1, d2, st,
+                                                             cc, k, coef, out);
+}
+template <class V>
+void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
+             CanvasCount* cc, const FoldStats* st, cudaStream_t s) {
+    k_compose<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, box, blended, cc, st);
+    k_count_update<<<1, 1, 0, s>>>(cc, st);
+}
+template <class V>
+void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
+    k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
+}
+template void union_valid<ViewU8>(const Canvas&, const ViewU8&, cudaStream_t);
+void quantize(const Canvas& cv, uchar4* out, cudaStream_t s) {
+    k_quantize<<<row_grid(cv.w, cv.h), 256, 0, s>>>(cv, out);
+}
+void export_float(const Canvas& cv, float* out, uint8_t* vout, cudaStream_t s) {
+    k_export_float<<<row_grid(cv.w, cv.h), 256, 0, s>>>(cv, out, vout);
+}
+
+// explicit instantiations
+template void place_view<ViewU8>(const Canvas&, const ViewU8&, CanvasCount*, cudaStream_t);
+template void place_view<ViewF4>(const Canvas&, const ViewF4&, CanvasCount*, cudaStream_t);
+template void partition<ViewU8>(const Canvas&, const ViewU8&, FoldStats*, cudaStream_t);
+template void partition<ViewF4>(const Canvas&, const ViewF4&, FoldStats*, cudaStream_t);
+template void crop_gray<ViewU8>(const Canvas&, const ViewU8&, const Rect&, float*, float*,
+                                cudaStream_t);
+template void crop_gray<ViewF4>(const Canvas&, const ViewF4&, const Rect&, float*, float*,
+                                cudaStream_t);
+template void edt<FoldMask<ViewU8>>(const EdtJob<FoldMask<ViewU8>>&,
+                                    const EdtJob<FoldMask<ViewU8>>&, const FoldStats*,
+                                    const CanvasCount*, cudaStream_t);
+template void edt<FoldMask<ViewF4>>(const EdtJob<FoldMask<ViewF4>>&,
+                                    const EdtJob<FoldMask<ViewF4>>&, const FoldStats*,
+                                    const CanvasCount*, cudaStream_t);
+template void edt<PlaneMask>(const EdtJob<PlaneMask>&, const EdtJob<PlaneMask>&,
+                             const FoldStats*, const CanvasCount*, cudaStream_t);
+template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
+                             const FoldStats*, const CanvasCount*, cudaStream_t);
+template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
+                                  const float2*, const int*, const int*, const FoldStats*,
+                                  const CanvasCount*, double, double, float4*, cudaStream_t);
+template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
+                                  const float2*, const int*, const int*, const FoldStats*,
+                                  const CanvasCount*, double, double, float4*, cudaStream_t);
+template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
+                              CanvasCount*, const FoldStats*, cudaStream_t);
+template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
+                              CanvasCount*, const FoldStats*, cudaStream_t);
+
+}  // namespace launch
+}  // namespace fs

@@ -1,0 +1,103 @@
+"""Planned device-resident fold (fs_plan_* of include/fs_b200.h).
+
+``Plan`` fixes a layout (view sizes, offsets, fold order, canvas) and owns all
+device memory; ``execute`` replays one CUDA graph that recomputes the whole
+flow+blend fold from the 8-bit views resident in HBM, ``execute_host`` is the
+end-to-end call (host views in, host RGBA canvas out).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .api import _ERRORS, FlowstitchError
+from ._native import BlendParams, FlowParams
+
+
+def _raise(st: int):
+    if st != N.FS_OK:
+        raise _ERRORS.get(st, FlowstitchError)(N.last_error())
+
+
+class Plan:
+    def __init__(self, dims: Sequence, offsets: Sequence, canvas_w: int, canvas_h: int,
+                 flow: Optional[FlowParams] = None, blend: Optional[BlendParams] = None,
+                 device: int = 0, views_rgba: Optional[Sequence[np.ndarray]] = None):
+        self.n = len(dims)
+        self.dims = [tuple(int(v) for v in d) for d in dims]
+        self.offsets = [tuple(int(v) for v in o) for o in offsets]
+        self.canvas_w, self.canvas_h = int(canvas_w), int(canvas_h)
+        self.flow = flow or FlowParams()
+        self.blend = blend or BlendParams()
+        d = np.array(self.dims, np.int32).ravel()
+        o = np.array(self.offsets, np.int32).ravel()
+        views_arg = None
+        keep = None
+        if views_rgba is not None:
+            keep = [np.ascontiguousarray(v, np.uint8) for v in views_rgba]
+            views_arg = C.cast((C.c_void_p * self.n)(*[v.ctypes.data for v in keep]), N.PP)
+        h = C.c_void_p()
+        _raise(N.lib.fs_plan_create(C.byref(h), device, self.n, d.ctypes.data_as(C.c_void_p),
+                                    o.ctypes.data_as(C.c_void_p), self.canvas_w, self.canvas_h,
+                                    C.byref(self.flow), C.byref(self.blend), views_arg))
+        self._h = h
+
+    # ---- buffers ----
+    def view_buffer(self, k: int) -> int:
+        return N.lib.fs_plan_view_buffer(self._h, k)
+
+    def output_buffer(self) -> int:
+        return N.lib.fs_plan_output_buffer(self._h)
+
+    def fold_info(self, k: int):
+        box = np.zeros(4, np.int32)
+        depth = C.c_int()
+        _raise(N.lib.fs_plan_fold_info(self._h, k, box.ctypes.data_as(C.c_void_p), C.byref(depth)))
+        return tuple(int(v) for v in box), depth.value
+
+    @property
+    def launch_count(self) -> int:
+        return N.lib.fs_plan_launch_count(self._h)
+
+    # ---- execution ----
+    def execute(self, stream: int = 0) -> None:
+        """Async on `stream` (a cudaStream_t as int): fold the views in HBM."""
+        _raise(N.lib.fs_plan_execute(self._h, C.c_void_p(stream)))
+
+    def check(self) -> None:
+        _raise(N.lib.fs_plan_check(self._h))
+
+    def execute_host(self, views: Optional[Sequence[np.ndarray]], out: Optional[np.ndarray] = None,
+                     stream: int = 0) -> Optional[np.ndarray]:
+        """End to end: copy views (RGBA8) in, fold, copy the RGBA8 canvas out."""
+        arg = None
+        keep = None
+        if views is not None:
+            keep = [np.ascontiguousarray(v, np.uint8) for v in views]
+            arg = C.cast((C.c_void_p * self.n)(*[v.ctypes.data for v in keep]), N.PP)
+        outp = None
+        if out is not None:
+            outp = C.c_void_p(out.ctypes.data)
+        _raise(N.lib.fs_plan_execute_host(self._h, arg, outp, C.c_void_p(stream)))
+        return out
+
+    def execute_ptrs(self, view_ptrs: Sequence[int], out_ptr: Optional[int],
+                     stream: int = 0) -> None:
+        """End to end with raw (e.g. pinned host) pointers."""
+        arg = C.cast((C.c_void_p * self.n)(*view_ptrs), N.PP)
+        _raise(N.lib.fs_plan_execute_host(self._h, arg, C.c_void_p(out_ptr) if out_ptr else None,
+                                          C.c_void_p(stream)))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib.fs_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

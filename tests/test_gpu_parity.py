@@ -1,0 +1,397 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle restatement
+(oracle/fs_oracle.c, itself pinned bit-exact to the compiled reference in
+test_oracle.py) on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  * integer / index / mask work (labels, counts, boxes, pyramid dims, squared
+    distances, valid bits): bit-exact;
+  * pyramid, gray, crop, EDT, Eq. 1: bit-exact (same fp32/fp64 op order, no FMA);
+  * flow: identical valid bits, mean EPE <= 1e-4 px (spec: <= 0.05 px);
+  * blend (fp32 output of fp64 math; exp() may differ by 1 ulp): |d| <= 1e-6;
+  * 8-bit output: +-1 LSB on >= 99.9% of pixels (in practice 100%).
+"""
+import numpy as np
+import pytest
+
+from paper_2006_01201_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+EPE_TOL = 1e-4
+
+
+def _img(fs, data, valid=None):
+    data = np.asarray(data, np.float32)
+    if data.ndim == 2:
+        data = data[:, :, None]
+    if valid is None:
+        valid = np.ones(data.shape[:2], np.uint8)
+    return fs.ImageBuf(data, valid)
+
+
+def _rgb(h, w, seed):
+    return np.stack([S.value_noise(h, w, seed + d) for d in (0, 101, 202)], -1)
+
+
+def _epe(a, b):
+    return float(np.sqrt(((a - b) ** 2).sum(-1)).mean())
+
+
+# ---------------------------------------------------------------- imagecore
+def test_to_gray_bit_exact(fs, oracle):
+    d = _rgb(37, 53, 1)
+    g = fs.to_gray(_img(fs, d))
+    assert np.array_equal(g.data[..., 0], oracle.to_gray(d))
+    one = S.value_noise(9, 11, 2)
+    assert np.array_equal(fs.to_gray(_img(fs, one)).data[..., 0], one)
+
+
+def test_bilinear_sample_matches(fs, oracle):
+    rng = np.random.RandomState(3)
+    d = _rgb(20, 30, 4)
+    v = (rng.rand(20, 30) > 0.3).astype(np.uint8)
+    img = _img(fs, d, v)
+    xy = rng.uniform(-5, 35, size=(400, 2))
+    got = fs.bilinear_sample_batch(img, xy)
+    exp = np.stack([oracle.bilinear_sample(d, v, x, y) for x, y in xy])
+    assert np.array_equal(got, exp)
+    # reference KATs (test_image.cpp:268-301)
+    two = _img(fs, np.array([[0.2, 0.6]], np.float32))
+    assert fs.bilinear_sample(two, 0.5, 0.0)[0] == pytest.approx(0.4)
+    one_invalid = _img(fs, np.array([[0.3, 0.9]], np.float32), np.array([[1, 0]], np.uint8))
+    assert fs.bilinear_sample(one_invalid, 0.75, 0.0)[0] == pytest.approx(0.3)
+    none_valid = _img(fs, np.array([[0.3, 0.9]], np.float32), np.array([[0, 0]], np.uint8))
+    assert fs.bilinear_sample(none_valid, 0.5, 0.0)[0] == 0.0
+
+
+@pytest.mark.parametrize("shape", [(1, 10), (13, 9), (64, 80), (3, 1)])
+def test_partition_and_crop_bit_exact(fs, oracle, shape):
+    rng = np.random.RandomState(sum(shape))
+    h, w = shape
+    ml = (rng.rand(h, w) > 0.4).astype(np.uint8)
+    mr = (rng.rand(h, w) > 0.4).astype(np.uint8)
+    part = fs.compute_partition(fs.Mask(ml), fs.Mask(mr))
+    lab, cnt = oracle.compute_partition(ml, mr)
+    assert np.array_equal(part.label, lab)
+    assert np.array_equal(part.counts, cnt)
+    d = _rgb(h, w, 5)
+    if cnt[3] == 0:
+        with pytest.raises(fs.EmptyRegionError):
+            fs.crop_overlap(_img(fs, d, ml), part)
+        return
+    c = fs.crop_overlap(_img(fs, d, ml), part)
+    od, ov, off = oracle.crop_overlap(d, ml, lab, cnt)
+    assert (c.offset_x, c.offset_y) == off
+    assert np.array_equal(c.image.data, od)
+    assert np.array_equal(c.image.valid, ov)
+
+
+def test_partition_kats(fs):
+    # test_image.cpp:331-366
+    def cols(w, h, c0, c1):
+        m = np.zeros((h, w), np.uint8)
+        m[:, c0:c1 + 1] = 1
+        return fs.Mask(m)
+    p = fs.compute_partition(cols(10, 2, 0, 3), cols(10, 2, 6, 9))
+    assert list(p.counts) == [4, 8, 8, 0]
+    p = fs.compute_partition(cols(10, 1, 0, 6), cols(10, 1, 4, 9))
+    assert list(p.label[0]) == [1, 1, 1, 1, 3, 3, 3, 2, 2, 2]
+    with pytest.raises(fs.ContractError):
+        fs.compute_partition(fs.Mask(np.zeros((3, 3), np.uint8)), fs.Mask(np.zeros((3, 4), np.uint8)))
+
+
+def test_place_on_canvas(fs, oracle):
+    d = _rgb(7, 5, 9)
+    v = np.ones((7, 5), np.uint8)
+    v[2, 3] = 0
+    c = fs.place_on_canvas(_img(fs, d, v), 6, 2, 20, 12)
+    od, ov = oracle.place_on_canvas(d, v, 6, 2, 20, 12)
+    assert np.array_equal(c.data, od) and np.array_equal(c.valid, ov)
+    with pytest.raises(fs.LayoutError):
+        fs.place_on_canvas(_img(fs, d, v), 16, 0, 20, 12)
+    with pytest.raises(fs.LayoutError):
+        fs.place_on_canvas(_img(fs, d, v), -1, 0, 20, 12)
+
+
+# ---------------------------------------------------------------- pyramid + flow
+@pytest.mark.parametrize("shape,levels", [((16, 16), 2), ((20, 20), 5), ((37, 53), 4),
+                                          ((129, 67), 6), ((8, 300), 4)])
+def test_build_pyramid_bit_exact(fs, oracle, shape, levels):
+    g = S.value_noise(*shape, seed=shape[0])
+    got = fs.build_pyramid(_img(fs, g), levels)
+    exp = oracle.build_pyramid(g, levels)
+    assert len(got) == len(exp)
+    for a, b in zip(got, exp):
+        assert np.array_equal(a.data[..., 0], b)
+
+
+def test_pyramid_depth_kat(fs):
+    # test_flow.cpp:79-84: 20 -> 10, 10/2 = 5 < 8
+    assert len(fs.build_pyramid(_img(fs, S.value_noise(20, 20, 3)), 5)) == 2
+    with pytest.raises(fs.ContractError):
+        fs.build_pyramid(_img(fs, _rgb(16, 16, 4)), 2)
+
+
+LK_CASES = [
+    ((64, 64), (3.0, 0.0), dict(levels=3, window_radius=5, iterations_per_level=3)),
+    ((128, 128), (5.0, 3.0), dict()),
+    ((96, 160), (-4.0, 1.5), dict(smoothing_passes=0)),
+    ((80, 72), (2.0, -1.0), dict(smoothing_passes=1, iterations_per_level=1)),
+    ((200, 90), (1.0, 2.0), dict(smoothing_passes=3, window_radius=3)),
+    ((256, 512), (-12.0, 0.0), dict(levels=5)),
+]
+
+
+@pytest.mark.parametrize("shape,shift,kw", LK_CASES)
+def test_dense_pyr_lk_matches_oracle(fs, oracle, shape, shift, kw):
+    h, w = shape
+    base = S.value_noise(h + 40, w + 40, seed=w)
+    frm = base[20:20 + h, 20:20 + w]
+    sx, sy = int(round(shift[0])), int(round(shift[1]))
+    to = base[20 - sy:20 - sy + h, 20 - sx:20 - sx + w]
+    p = fs.FlowParams(**kw)
+    f = fs.dense_pyr_lk(_img(fs, frm), _img(fs, to), p)
+    vec, valid = oracle.dense_pyr_lk(frm, to, p)
+    assert np.array_equal(f.valid, valid)
+    assert _epe(f.vec, vec) <= EPE_TOL
+    assert np.abs(f.vec - vec).max() <= 1e-2
+
+
+def test_lk_reference_kats(fs):
+    # zero-motion fixpoint (test_flow.cpp:91-102)
+    img = _img(fs, S.value_noise(48, 48, 21))
+    f = fs.dense_pyr_lk(img, img, fs.FlowParams(levels=3, window_radius=5))
+    assert np.sqrt((f.vec ** 2).sum(-1)).max() <= 1e-3
+    # textureless -> zero and invalid (test_flow.cpp:126-137)
+    flat = _img(fs, np.full((32, 32), 0.7, np.float32))
+    f = fs.dense_pyr_lk(flat, flat, fs.FlowParams(levels=2))
+    assert np.all(f.vec == 0.0) and np.all(f.valid == 0)
+    # contract checks (test_flow.cpp:139-146)
+    with pytest.raises(fs.ContractError):
+        fs.dense_pyr_lk(img, _img(fs, S.value_noise(48, 24, 1)))
+    with pytest.raises(fs.ContractError):
+        fs.dense_pyr_lk(img, img, fs.FlowParams(levels=0))
+
+
+def test_bidirectional_flow_matches_oracle(fs, oracle):
+    L = _rgb(120, 90, 11)
+    R = np.roll(L, (1, 4), axis=(0, 1))
+    lr, rl = fs.bidirectional_flow(_img(fs, L), _img(fs, R))
+    (olr, olv), (orl, orv) = oracle.bidirectional_flow(L, R)
+    assert np.array_equal(lr.valid, olv) and np.array_equal(rl.valid, orv)
+    assert _epe(lr.vec, olr) <= EPE_TOL and _epe(rl.vec, orl) <= EPE_TOL
+    m = lr.vec[20:-20, 20:-20].mean((0, 1))
+    assert m[0] == pytest.approx(4.0, abs=0.3) and m[1] == pytest.approx(1.0, abs=0.3)
+
+
+def test_flow_helpers(fs, oracle):
+    rng = np.random.RandomState(17)
+    vec = rng.uniform(-10, 10, size=(4, 5, 2)).astype(np.float32)
+    ff = fs.FlowField(vec, np.ones((4, 5), np.uint8))
+    assert np.array_equal(fs.flow_magnitude(ff), oracle.flow_magnitude(vec))
+    e = fs.embed_flow(ff, 5, 7, 20, 15)
+    ov, oval = oracle.embed_flow(vec, np.ones((4, 5), np.uint8), 5, 7, 20, 15)
+    assert np.array_equal(e.vec, ov) and np.array_equal(e.valid, oval)
+    with pytest.raises(fs.ContractError):
+        fs.embed_flow(ff, 19, 0, 20, 15)
+
+
+# ---------------------------------------------------------------- EDT + Eq. 1
+@pytest.mark.parametrize("shape,density,seed", [((8, 8), 0.0, 0), ((37, 51), 1 / 7, 1),
+                                                ((1, 60), 0.1, 2), ((60, 1), 0.1, 3),
+                                                ((200, 31), 0.002, 4), ((31, 300), 0.01, 5),
+                                                ((128, 128), 0.3, 6)])
+def test_distance_transform_bit_exact(fs, oracle, shape, density, seed):
+    rng = np.random.RandomState(seed)
+    m = (rng.rand(*shape) < density).astype(np.uint8)
+    m[rng.randint(shape[0]), rng.randint(shape[1])] = 1
+    d = fs.distance_transform(fs.Mask(m))
+    assert np.array_equal(d.d, oracle.distance_transform(m))
+
+
+def test_distance_transform_kats(fs):
+    m = np.zeros((8, 8), np.uint8)
+    m[0, 0] = 1
+    d = fs.distance_transform(fs.Mask(m)).d
+    assert d[4, 3] == 5.0 and d[0, 0] == 0.0 and d[0, 7] == 7.0
+    with pytest.raises(fs.EmptyRegionError):
+        fs.distance_transform(fs.Mask(np.zeros((4, 4), np.uint8)))
+
+
+def _rect_masks(w, h, rng):
+    lx1 = w // 2 + rng.randint(w // 2)
+    rx0 = rng.randint(lx1 - 1)
+    l = np.zeros((h, w), np.uint8)
+    r = np.zeros((h, w), np.uint8)
+    l[rng.randint(4):h - rng.randint(4), :lx1 + 1] = 1
+    r[rng.randint(4):h - rng.randint(4), rx0:] = 1
+    return l, r
+
+
+def test_compute_blend_bit_exact(fs, oracle):
+    rng = np.random.RandomState(7)
+    for _ in range(10):
+        l, r = _rect_masks(24 + rng.randint(41), 16 + rng.randint(33), rng)
+        part = fs.compute_partition(fs.Mask(l), fs.Mask(r))
+        b = fs.compute_blend(part)
+        assert np.array_equal(b.b, oracle.compute_blend(part.label, part.counts))
+    # 10x1 strip KAT (test_blend_field.cpp:89-96)
+    l = np.zeros((1, 10), np.uint8)
+    r = np.zeros((1, 10), np.uint8)
+    l[0, :7] = 1
+    r[0, 4:] = 1
+    b = fs.compute_blend(fs.compute_partition(fs.Mask(l), fs.Mask(r))).b[0]
+    assert b[4] == pytest.approx(0.25) and b[5] == pytest.approx(0.5) and b[6] == pytest.approx(0.75)
+    # empty side -> 0.5 (test_blend_field.cpp:147-159)
+    l = np.zeros((4, 8), np.uint8)
+    l[:, :6] = 1
+    r = l.copy()
+    r[:, 6] = 1
+    b = fs.compute_blend(fs.compute_partition(fs.Mask(l), fs.Mask(r))).b
+    assert np.all(b[:, :6] == 0.5)
+
+
+# ---------------------------------------------------------------- blender
+def test_softmax_kats(fs, oracle):
+    sl, sr = fs.softmax_weights(0.75, 0.25, 0.0, 0.0, fs.BlendParams(10.0, 0.37))
+    assert sl == pytest.approx(0.99330714907571527, rel=1e-15)
+    rng = np.random.RandomState(4)
+    for _ in range(200):
+        b = rng.rand()
+        args = (1 - b, b, rng.rand() * 20, rng.rand() * 20)
+        assert fs.softmax_weights(*args) == oracle.softmax_weights(*args)
+    sl, sr = fs.softmax_weights(1.0, 0.0, 100.0, 0.0, fs.BlendParams(5000.0))
+    assert np.isfinite(sl) and sl == pytest.approx(1.0)
+
+
+def _overlap_case(fs, oracle, w, h, seed, random_flow=True, mag=6.0):
+    L = _rgb(h, w, seed)
+    R = _rgb(h, w, seed + 5)
+    third = w // 3
+    vl = np.ones((h, w), np.uint8)
+    vr = np.ones((h, w), np.uint8)
+    vl[:, 2 * third:] = 0
+    vr[:, :third] = 0
+    part = fs.compute_partition(fs.Mask(vl), fs.Mask(vr))
+    b = fs.compute_blend(part)
+    rng = np.random.RandomState(seed + 11)
+    if random_flow:
+        flr = rng.uniform(-mag, mag, size=(h, w, 2)).astype(np.float32)
+        frl = rng.uniform(-mag, mag, size=(h, w, 2)).astype(np.float32)
+    else:
+        flr = np.zeros((h, w, 2), np.float32)
+        frl = np.zeros((h, w, 2), np.float32)
+    return L, vl, R, vr, part, b, flr, frl
+
+
+def test_blend_pair_matches_oracle(fs, oracle):
+    for seed in (10, 20, 30):
+        L, vl, R, vr, part, b, flr, frl = _overlap_case(fs, oracle, 128, 128, seed)
+        ones = np.ones(part.label.shape, np.uint8)
+        F = fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                          fs.FlowField(frl, ones), b, part)
+        OF, OV = oracle.blend_pair(L, vl, R, vr, flr, frl, b.b, part.label)
+        assert np.array_equal(F.valid, OV)
+        assert np.abs(F.data - OF).max() <= 1e-6
+
+
+def test_blend_pair_contracts_and_regions(fs, oracle):
+    L, vl, R, vr, part, b, flr, frl = _overlap_case(fs, oracle, 30, 12, 12, False)
+    ones = np.ones(part.label.shape, np.uint8)
+    F = fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                      fs.FlowField(frl, ones), b, part)
+    a1 = part.label == 1
+    assert np.array_equal(F.data[a1], L[a1])
+    bad = flr.copy()
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(fs.ContractError):
+        fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(bad, ones),
+                      fs.FlowField(frl, ones), b, part)
+    with pytest.raises(fs.ContractError):
+        fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                      fs.FlowField(frl, ones), b, part, fs.BlendParams(0.0))
+
+
+def test_feather_and_warp_constituents(fs, oracle):
+    L, vl, R, vr, part, b, flr, frl = _overlap_case(fs, oracle, 64, 48, 7)
+    ones = np.ones(part.label.shape, np.uint8)
+    Fe = fs.feather_blend(_img(fs, L, vl), _img(fs, R, vr), b, part)
+    a3 = part.label == 3
+    exp = (1 - b.b[..., None]) * L + b.b[..., None] * R
+    assert np.abs(Fe.data[a3] - exp[a3]).max() <= 1e-6
+    wl, wr = fs.warp_constituents(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                                  fs.FlowField(frl, ones), b, part)
+    F = fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                      fs.FlowField(frl, ones), b, part)
+    lo = np.minimum(wl.data, wr.data) - 1e-6
+    hi = np.maximum(wl.data, wr.data) + 1e-6
+    assert np.all(F.data[a3] >= lo[a3]) and np.all(F.data[a3] <= hi[a3])
+
+
+# ---------------------------------------------------------------- fold
+def _fold_both(fs, oracle, lay, params):
+    fv = lay.float_views()
+    placed = [fs.PlacedImage(fs.ImageBuf(d, v), x, y) for (d, v), (x, y) in zip(fv, lay.offsets)]
+    pano, rep = fs.stitch_placed(placed, lay.canvas_w, lay.canvas_h, params)
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    return pano, rep, od, ov
+
+
+@pytest.mark.parametrize("builder,kw", [(S.small_strip, dict(levels=3, window_radius=5,
+                                                               iterations_per_level=2)),
+                                        (S.small_panorama, dict(levels=3))])
+def test_stitch_placed_matches_oracle(fs, oracle, builder, kw):
+    lay = builder(seed=3)
+    pano, rep, od, ov = _fold_both(fs, oracle, lay, fs.FlowParams(**kw))
+    assert np.array_equal(pano.valid, ov)
+    assert np.abs(pano.data - od).max() <= 1e-5
+    assert len(rep.pairs) == len(lay.views) - 1
+    q_gpu = np.rint(np.clip(pano.data, 0, 1) * 255)
+    q_ref = np.rint(np.clip(od, 0, 1) * 255)
+    assert np.mean(np.abs(q_gpu - q_ref) <= 1) >= 0.999
+
+
+def test_stitch_errors(fs):
+    img = fs.ImageBuf(_rgb(40, 40, 2), np.ones((40, 40), np.uint8))
+    with pytest.raises(fs.EmptyRegionError):
+        fs.stitch_placed([fs.PlacedImage(img, 0, 0), fs.PlacedImage(img, 100, 0)], 200, 40)
+    with pytest.raises(fs.ContractError):
+        fs.stitch_placed([fs.PlacedImage(img, 0, 0)], 200, 40)
+    with pytest.raises(fs.LayoutError):
+        fs.stitch_placed([fs.PlacedImage(img, 0, 0), fs.PlacedImage(img, 170, 0)], 200, 40)
+
+
+def test_identity_stitch(fs):
+    # test_pipeline.cpp:84-94: two identical placements reproduce the input
+    d = _rgb(60, 80, 5)
+    img = fs.ImageBuf(d, np.ones((60, 80), np.uint8))
+    pano, rep = fs.stitch_placed([fs.PlacedImage(img, 0, 0), fs.PlacedImage(img, 0, 0)], 80, 60,
+                                 fs.FlowParams(levels=3, window_radius=5, iterations_per_level=2))
+    assert rep.pairs[0].overlap_pixels == 80 * 60
+    assert np.allclose(pano.data, d, rtol=1e-4, atol=1e-6)
+
+
+def test_plan_matches_oracle(fs, oracle):
+    lay = S.small_panorama(seed=5)
+    params = fs.FlowParams(levels=3)
+    fv = lay.float_views()
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params)
+    out = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    plan.execute_host(lay.views, out)
+    assert np.array_equal(out[..., 3] == 255, ov == 1)
+    q = np.rint(np.clip(od, 0, 1) * 255).astype(np.int32)
+    diff = np.abs(out[..., :3].astype(np.int32) - q)[ov == 1]
+    assert diff.max() <= 1 and np.mean(diff == 0) >= 0.999
+    # masks given at plan time produce the same boxes
+    plan2 = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params,
+                    views_rgba=lay.views)
+    for k in range(1, len(lay.views)):
+        assert plan.fold_info(k) == plan2.fold_info(k)
+    out2 = np.empty_like(out)
+    plan.execute_host(lay.views, out2)
+    assert np.array_equal(out, out2), "replay is not deterministic"
+    plan.close()
+    plan2.close()
