@@ -182,6 +182,17 @@ fs_status fs_plan_check(fs_plan plan);
 int fs_plan_launch_count(fs_plan plan);
 /* fold geometry: for fold k (1..n-1) the Area3 box {x0,y0,w,h} and depth */
 fs_status fs_plan_fold_info(fs_plan plan, int k, int* box, int* depth);
+/* one un-captured execution with CUDA events around every kernel launch on
+ * `stream`; per kernel family: launches, summed device ms and algorithmic
+ * bytes.  total_ms spans the whole execution. */
+typedef struct {
+    char name[24];
+    int launches;
+    double ms;
+    double bytes;
+} fs_kernel_stat;
+fs_status fs_plan_profile(fs_plan plan, void* stream, fs_kernel_stat* out, int max_out,
+                          int* n_out, double* total_ms);
 void fs_plan_destroy(fs_plan plan);
 
 /* ---- runtime (parallel.hpp:9-18): kept for drop-in completeness; the GPU

@@ -55,6 +55,11 @@ class PairStats(C.Structure):
                 ("blend_seconds", C.c_double), ("crop_box", C.c_int32 * 4)]
 
 
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 24), ("launches", C.c_int), ("ms", C.c_double),
+                ("bytes", C.c_double)]
+
+
 P = C.c_void_p
 I = C.c_int
 D = C.c_double
@@ -96,6 +101,7 @@ SIGNATURES = {
     "fs_plan_check": (I, [P]),
     "fs_plan_launch_count": (I, [P]),
     "fs_plan_fold_info": (I, [P, I, P, P]),
+    "fs_plan_profile": (I, [P, P, C.POINTER(KernelStat), I, C.POINTER(I), C.POINTER(D)]),
     "fs_plan_destroy": (None, [P]),
     "fs_set_thread_count": (None, [I]),
     "fs_thread_count": (I, []),

@@ -15,6 +15,30 @@ std::string& last_error_slot() {
     return msg;
 }
 
+KernelProf*& kernel_prof() {
+    thread_local KernelProf* p = nullptr;
+    return p;
+}
+KernelProf::~KernelProf() {
+    for (auto& r : recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+}
+ProfScope::ProfScope(const char* name, double bytes, cudaStream_t s_) : s(s_) {
+    KernelProf* p = kernel_prof();
+    on = p != nullptr;
+    if (!on) return;
+    KernelProf::Rec r{name, bytes, nullptr, nullptr};
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+    p->recs.push_back(r);
+}
+ProfScope::~ProfScope() {
+    if (on) cudaEventRecord(kernel_prof()->recs.back().b, s);
+}
+
 void cuda_check(cudaError_t e, const char* what) {
     if (e == cudaErrorMemoryAllocation) raise(FS_ERR_OOM, std::string("device allocation failed: ") + what);
     if (e != cudaSuccess) raise(FS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -98,6 +122,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     ws.pyr[0][0] = const_cast<float*>(g0);
     ws.pyr[1][0] = const_cast<float*>(g1);
     for (int l = 1; l < ws.depth; ++l) {
+        // read level l-1 once, write level l: (4 n_{l-1} + 4 n_l) per image
+        double bytes = 2.0 * 4.0 * ((double)ws.lv[l - 1].w * ws.lv[l - 1].h +
+                                    (double)ws.lv[l].w * ws.lv[l].h);
+        ProfScope ps("pyramid", bytes, s);
         launch::downsample(ws.pyr[0][l - 1], ws.pyr[1][l - 1], ws.pyr[0][l], ws.pyr[1][l],
                            ws.lv[l - 1].w, ws.lv[l - 1].h, 2, s);
         ++launches;
@@ -133,7 +161,13 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.d[d].fout = ws.fb[d][fcur ^ 1];
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
             }
-            FS_CK(launch::lk_iter(a, s));
+            {
+                // per pixel and direction: F 4 + T 4 + flow/ok out 9, plus flow/ok
+                // in 9 (mode 1) or the coarse level's 9/4 (mode 2)
+                double in = a.mode == 1 ? 9.0 : (a.mode == 2 ? 2.25 : 0.0);
+                ProfScope ps("lk_iter", (17.0 + in) * L.w * L.h * ws.ndir, s);
+                FS_CK(launch::lk_iter(a, s));
+            }
             ++launches;
             fcur ^= 1;
             okcur ^= 1;
@@ -155,7 +189,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.ok[d] = ws.ok[d][okcur];
                 a.valid_out[d] = out_valid[d];
             }
-            launch::smooth(a, s);
+            {
+                ProfScope ps("smooth", (16.0 + (fin ? 2.0 : 0.0)) * L.w * L.h * ws.ndir, s);
+                launch::smooth(a, s);
+            }
             ++launches;
             if (!fin) fcur ^= 1;
         }
@@ -171,7 +208,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.ok[d] = ws.ok[d][okcur];
                 a.valid_out[d] = out_valid[d];
             }
-            launch::finalize_flow(a, s);
+            {
+                ProfScope ps("smooth", 18.0 * L.w * L.h * ws.ndir, s);
+                launch::finalize_flow(a, s);
+            }
             ++launches;
         }
     }
@@ -273,7 +313,10 @@ void init_count(CanvasCount* cc, cudaStream_t s) { k_init_count<<<1, 1, 0, s>>>(
 template <class V>
 int fold_enqueue_pre(FoldWS<V>& f, const Canvas& cv, const V& view, cudaStream_t s) {
     init_stats(f.st, s);
-    launch::partition(cv, view, f.st, s);
+    {
+        ProfScope ps("partition", 5.0 * view.rect.area(), s);  // view 4 B + pano valid 1 B
+        launch::partition(cv, view, f.st, s);
+    }
     return 2;
 }
 
@@ -283,7 +326,11 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasC
                           cudaEvent_t ev_flow1) {
     int launches = 0;
     launch::check_box(f.st, f.box, s);
-    launch::crop_gray(cv, view, f.box, f.gray[0], f.gray[1], s);
+    {
+        // pano rgb 16 + valid 1 + view 4 in, two gray planes 8 out
+        ProfScope ps("crop_gray", 29.0 * f.box.area(), s);
+        launch::crop_gray(cv, view, f.box, f.gray[0], f.gray[1], s);
+    }
     launches += 2;
     if (ev_flow0) FS_CK(cudaEventRecord(ev_flow0, s));
     launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s);
@@ -308,7 +355,13 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasC
         j[m].e_bottom = P.e_bottom;
         j[m].check = P.check;
     }
-    launch::edt(j[0], j[1], f.st, cc, s);
+    {
+        // per mask: the seed mask over the domain (pano valid 1 + view 4) + d^2 out on C
+        double bytes = 0;
+        for (int m = 0; m < 2; ++m) bytes += 5.0 * f.ep[m].W.area() + 4.0 * f.box.area();
+        ProfScope ps("edt", bytes, s);
+        launch::edt(j[0], j[1], f.st, cc, s);
+    }
     launches += 3;
     FS_CK(cudaGetLastError());
     return launches;
@@ -318,9 +371,17 @@ template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
                        const fs_blend_params& bp, cudaStream_t s) {
     int launches = 0;
-    launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out, f.st,
-                        cc, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
-    launch::compose(cv, view, f.box, f.blended, cc, f.st, s);
+    {
+        // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
+        ProfScope ps("blend", 61.0 * f.box.area(), s);
+        launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
+                            f.st, cc, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
+    }
+    {
+        // view 4 + pano valid 1 in, rgb 16 + valid 1 out on the view; blended 16 in on Area3
+        ProfScope ps("compose", 22.0 * view.rect.area() + 16.0 * f.box.area(), s);
+        launch::compose(cv, view, f.box, f.blended, cc, f.st, s);
+    }
     launches += 3;
     FS_CK(cudaGetLastError());
     return launches;

@@ -28,6 +28,26 @@ void validate_blend_params(const fs_blend_params& p);  // src/blender.cpp:11-16
 int pyramid_depth(int w, int h, int levels);           // src/flow.cpp:178-185
 void ensure_device();                                  // throws FS_ERR_CUDA without sm_100
 
+// Per-launch kernel timing (fs_plan_profile): when a profile run installs a
+// KernelProf, every launch site records CUDA events around its kernel on the
+// launching stream plus the launch's algorithmic bytes.
+struct KernelProf {
+    struct Rec {
+        const char* name;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    ~KernelProf();
+};
+KernelProf*& kernel_prof();  // thread-local; nullptr = profiling off
+struct ProfScope {
+    cudaStream_t s;
+    bool on;
+    ProfScope(const char* name, double bytes, cudaStream_t s);
+    ~ProfScope();
+};
+
 // Bump allocator: run the layout once with base == nullptr to size it, then
 // again over one device allocation.
 struct Arena {

@@ -64,9 +64,15 @@ ViewU8 view_of(const fs_plan_s* p, int k) { return ViewU8{p->views[k], p->rects[
 // Enqueue one full execution on stream s (captured into the graph).
 int enqueue_all(fs_plan_s* p, cudaStream_t s) {
     int launches = 0;
-    FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
+    {
+        ProfScope ps("clear", (double)p->cw * p->chh, s);
+        FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
+    }
     init_count(p->cc, s);
-    launch::place_view(p->cv, view_of(p, 0), p->cc, s);
+    {
+        ProfScope ps("place", 21.0 * p->rects[0].area(), s);  // view 4 in, rgb 16 + valid 1 out
+        launch::place_view(p->cv, view_of(p, 0), p->cc, s);
+    }
     launches += 2;
     for (int k = 1; k < p->n; ++k) {
         FoldWS<ViewU8>& f = p->folds[k - 1];
@@ -75,7 +81,10 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s) {
         launches += fold_enqueue_flow_edt(f, p->cv, v, p->cc, p->fp, s, nullptr, nullptr);
         launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
     }
-    launch::quantize(p->cv, p->out, s);
+    {
+        ProfScope ps("quantize", 21.0 * p->cw * p->chh, s);  // rgb 16 + valid 1 in, rgba8 out
+        launch::quantize(p->cv, p->out, s);
+    }
     launches += 1;
     FS_CK(cudaGetLastError());
     return launches;
@@ -317,6 +326,51 @@ fs_status fs_plan_execute_host(fs_plan p, const uint8_t* const* views_rgba, uint
             if (c == FS_OK) return;
             if (attempt == 1 || p->exec) raise(c, last_error_slot());
         }
+    });
+}
+
+fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_out, int* n_out,
+                          double* total_ms) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        KernelProf prof;
+        cudaEvent_t e0, e1;
+        FS_CK(cudaEventCreate(&e0));
+        FS_CK(cudaEventCreate(&e1));
+        kernel_prof() = &prof;
+        try {
+            FS_CK(cudaEventRecord(e0, s));
+            enqueue_all(p, s);
+            FS_CK(cudaEventRecord(e1, s));
+        } catch (...) {
+            kernel_prof() = nullptr;
+            throw;
+        }
+        kernel_prof() = nullptr;
+        FS_CK(cudaStreamSynchronize(s));
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (total_ms) *total_ms = tot;
+        int n = 0;
+        for (auto& r : prof.recs) {
+            float ms = 0.f;
+            FS_CK(cudaEventElapsedTime(&ms, r.a, r.b));
+            int k = 0;
+            while (k < n && std::strncmp(out[k].name, r.name, sizeof(out[k].name)) != 0) ++k;
+            if (k == n) {
+                if (n == max_out) continue;
+                std::memset(&out[n], 0, sizeof(out[n]));
+                std::strncpy(out[n].name, r.name, sizeof(out[n].name) - 1);
+                ++n;
+            }
+            out[k].launches += 1;
+            out[k].ms += ms;
+            out[k].bytes += r.bytes;
+        }
+        *n_out = n;
     });
 }
 

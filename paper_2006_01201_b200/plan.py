@@ -91,6 +91,19 @@ class Plan:
         _raise(N.lib.fs_plan_execute_host(self._h, arg, C.c_void_p(out_ptr) if out_ptr else None,
                                           C.c_void_p(stream)))
 
+    def profile(self, stream: int = 0):
+        """One un-captured execution with CUDA events around every launch.
+        Returns ({family: {"launches", "ms", "bytes"}}, total_ms)."""
+        stats = (N.KernelStat * 32)()
+        n = C.c_int()
+        tot = C.c_double()
+        _raise(N.lib.fs_plan_profile(self._h, C.c_void_p(stream), stats, 32, C.byref(n),
+                                     C.byref(tot)))
+        out = {}
+        for s in stats[:n.value]:
+            out[s.name.decode()] = {"launches": s.launches, "ms": s.ms, "bytes": s.bytes}
+        return out, tot.value
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             N.lib.fs_plan_destroy(self._h)

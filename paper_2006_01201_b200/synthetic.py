@@ -19,25 +19,53 @@ INV255 = np.float32(1.0) / np.float32(255.0)  # 1.0f/255.0f as the reference com
 
 
 def value_noise(h: int, w: int, seed: int, octaves=range(1, 8)) -> np.ndarray:
-    """Multi-octave smoothstep value noise in [0.1, 0.9], float32 (h, w)."""
+    """Multi-octave smoothstep value noise in [0.1, 0.9], float32 (h, w).
+    Large rasters are interpolated with torch on the GPU when one is present
+    (same lattice, same formula; input generation only, outside any timed
+    region; bitwise results may differ from numpy by float rounding, which
+    only matters within one run, where every arm reads the same bytes)."""
+    if h * w >= (1 << 22):
+        try:
+            return _value_noise_torch(h, w, seed, octaves)
+        except ImportError:
+            pass
     rng = np.random.RandomState(seed)
     acc = np.zeros((h, w), np.float32)
     for o in octaves:
         cell = 2 ** o
         amp = np.float32(2.0 ** (o / 2.0))
-        lat = rng.uniform(-1.0, 1.0, size=(h // cell + 2, w // cell + 2)).astype(np.float32)
-        ys = np.arange(h, dtype=np.float64) / cell
-        xs = np.arange(w, dtype=np.float64) / cell
-        y0 = np.floor(ys).astype(np.int64)
-        x0 = np.floor(xs).astype(np.int64)
-        fy = (ys - y0).astype(np.float32)
-        fx = (xs - x0).astype(np.float32)
-        sy = fy * fy * (3 - 2 * fy)
-        sx = fx * fx * (3 - 2 * fx)
-        t = lat[:, x0] * (1 - sx) + lat[:, x0 + 1] * sx  # (ly, w)
-        acc += amp * (t[y0] * (1 - sy)[:, None] + t[y0 + 1] * sy[:, None])
+        ny, nx = h // cell + 1, w // cell + 1  # lattice cells covering the image
+        lat = rng.uniform(-1.0, 1.0, size=(ny + 1, nx + 1)).astype(np.float32)
+        f = np.arange(cell, dtype=np.float32) / np.float32(cell)
+        s = f * f * (3 - 2 * f)  # smoothstep weights, identical for every cell
+        # x: each lattice column pair feeds `cell` consecutive pixels
+        t = (lat[:, :-1, None] * (1 - s) + lat[:, 1:, None] * s).reshape(ny + 1, nx * cell)
+        t = t[:, :w]
+        # y: same per lattice row pair
+        v = (t[:-1, None, :] * (1 - s)[None, :, None] + t[1:, None, :] * s[None, :, None])
+        acc += amp * v.reshape(ny * cell, w)[:h]
     lo, hi = float(acc.min()), float(acc.max())
     return (0.1 + 0.8 * (acc - lo) / max(hi - lo, 1e-6)).astype(np.float32)
+
+
+def _value_noise_torch(h, w, seed, octaves):
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    rng = np.random.RandomState(seed)
+    acc = torch.zeros((h, w), dtype=torch.float32, device=dev)
+    for o in octaves:
+        cell = 2 ** o
+        amp = float(2.0 ** (o / 2.0))
+        ny, nx = h // cell + 1, w // cell + 1
+        lat = torch.from_numpy(
+            rng.uniform(-1.0, 1.0, size=(ny + 1, nx + 1)).astype(np.float32)).to(dev)
+        f = torch.arange(cell, dtype=torch.float32, device=dev) / cell
+        s = f * f * (3 - 2 * f)
+        t = (lat[:, :-1, None] * (1 - s) + lat[:, 1:, None] * s).reshape(ny + 1, nx * cell)[:, :w]
+        v = t[:-1, None, :] * (1 - s)[None, :, None] + t[1:, None, :] * s[None, :, None]
+        acc.add_(v.reshape(ny * cell, w)[:h], alpha=amp)
+    lo, hi = float(acc.min()), float(acc.max())
+    return (0.1 + 0.8 * (acc - lo) / max(hi - lo, 1e-6)).cpu().numpy().astype(np.float32)
 
 
 def rgb_scene(h: int, w: int, seed: int) -> np.ndarray:
