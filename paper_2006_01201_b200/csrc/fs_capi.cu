@@ -131,8 +131,7 @@ void full_edt(Stage& st, const M& m0, const M* m1, int w, int h, int* out0, int*
         j[q].C = R;
         j[q].vfirst = h >= w;
         j[q].g = ws.g;
-        j[q].summ_first = ws.summ_first;
-        j[q].summ_last = ws.summ_last;
+        j[q].bits = ws.bits;
         j[q].stack = ws.stack;
         j[q].out = outs[q];
     }

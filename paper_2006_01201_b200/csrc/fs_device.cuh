@@ -78,7 +78,9 @@ struct LkDir {
     const float2* fin;     // level flow in (mode 1) or coarse flow (mode 2)
     const uint8_t* okin;   // level ok in (mode 1) or coarse ok (mode 2)
     float2* fout;
-    uint8_t* okout;
+    uint8_t* okout;   // written by the first iteration of a level only
+    float4* coef;     // level-constant (c/det, b/det, a/det, ok): written by the
+                      // first iteration, read by the later ones (nullptr: unused)
 };
 struct LkArgs {
     LkDir d[2];
@@ -88,7 +90,7 @@ struct LkArgs {
     double sx, sy;
     int mode;    // 0 zero, 1 flow-in, 2 upsample-from-coarse
     int r;
-    int tw, th;  // output tile
+    int tw, th;  // output tile (th <= 0: chosen per level)
     double eig_thresh;
     float flow_cap;
 };
@@ -144,8 +146,7 @@ struct EdtJob {
     Rect W, C;       // seed domain, output box (C inside W)
     int vfirst = 1;  // 1: columns 1-D first, envelope along rows
     int* g = nullptr;           // pass-1 output, laid out line-contiguous for pass 2
-    int* summ_first = nullptr;  // [nseg][nlines]
-    int* summ_last = nullptr;
+    unsigned long long* bits = nullptr;  // [nseg][nlines] seed bits per 64-position segment
     int* stack = nullptr;       // [pass-2 lines][sites]
     int* out = nullptr;         // squared distance on C, row-major C.w
     int e_left = 1, e_right = 1, e_top = 1, e_bottom = 1;  // W side == seed-bbox side

@@ -109,11 +109,13 @@ void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
         for (int l = 1; l < depth; ++l) pyr[i][l] = a.take<float>((size_t)lv[l].w * lv[l].h);
     }
     size_t n = (size_t)w * h;
-    for (int d = 0; d < ndir; ++d)
+    for (int d = 0; d < ndir; ++d) {
         for (int q = 0; q < 2; ++q) {
             fb[d][q] = a.take<float2>(n);
             ok[d][q] = a.take<uint8_t>(n);
         }
+        coef[d] = a.take<float4>(n);
+    }
 }
 
 int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_params& p,
@@ -149,7 +151,7 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.sy = static_cast<double>(a.ch) / L.h;
             }
             a.r = r;
-            a.th = 64;
+            a.th = 0;  // per-level choice (launch::lk_tile_rows)
             a.eig_thresh = eig_thresh;
             a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
             for (int d = 0; d < ws.ndir; ++d) {
@@ -160,17 +162,22 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.d[d].okin = ws.ok[d][okcur];
                 a.d[d].fout = ws.fb[d][fcur ^ 1];
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
+                a.d[d].coef = p.iterations_per_level > 1 ? ws.coef[d] : nullptr;
             }
             {
-                // per pixel and direction: F 4 + T 4 + flow/ok out 9, plus flow/ok
-                // in 9 (mode 1) or the coarse level's 9/4 (mode 2)
-                double in = a.mode == 1 ? 9.0 : (a.mode == 2 ? 2.25 : 0.0);
-                ProfScope ps("lk_iter", (17.0 + in) * L.w * L.h * ws.ndir, s);
+                // per pixel and direction: F 4 + T 4 + flow out 8, and
+                //  first iteration: ok out 1 + coef out 16 + (mode 2) the coarse
+                //                   level's flow/ok 9/4;
+                //  later ones:      flow in 8 + coef in 16
+                double per = a.mode == 1 ? 16.0 + 8.0 + 16.0
+                                         : 16.0 + 1.0 + (a.d[0].coef ? 16.0 : 0.0) +
+                                               (a.mode == 2 ? 2.25 : 0.0);
+                ProfScope ps("lk_iter", per * L.w * L.h * ws.ndir, s);
                 FS_CK(launch::lk_iter(a, s));
             }
             ++launches;
             fcur ^= 1;
-            okcur ^= 1;
+            if (it == 0) okcur ^= 1;  // ever_ok is final after a level's first iteration
         }
         int P = p.smoothing_passes;
         while (P > 0) {
@@ -262,8 +269,7 @@ void EdtWS::layout(Arena& a, const Rect& C, const Rect& E) {
     size_t nseg = ((vfirst ? E.h : E.w) + 63) / 64;
     g = a.take<int>(gsz);
     stack = a.take<int>(gsz);
-    summ_first = a.take<int>(nlines * nseg);
-    summ_last = a.take<int>(nlines * nseg);
+    bits = a.take<unsigned long long>(nlines * nseg);
     out = a.take<int>((size_t)C.w * C.h);
 }
 
@@ -345,8 +351,7 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasC
         j[m].C = P.C;
         j[m].vfirst = P.vfirst;
         j[m].g = f.edt[m].g;
-        j[m].summ_first = f.edt[m].summ_first;
-        j[m].summ_last = f.edt[m].summ_last;
+        j[m].bits = f.edt[m].bits;
         j[m].stack = f.edt[m].stack;
         j[m].out = f.edt[m].out;
         j[m].e_left = P.e_left;

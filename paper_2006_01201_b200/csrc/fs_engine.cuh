@@ -73,6 +73,7 @@ struct FlowWS {
     std::vector<float*> pyr[2];  // level pointers (level 0 = caller's gray buffers)
     float2* fb[2][2] = {};       // [dir][pingpong] level flow
     uint8_t* ok[2][2] = {};
+    float4* coef[2] = {};        // [dir] level-constant inverse structure tensor
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
 // Enqueue the whole coarse-to-fine flow on stream s.  ndir = 1: from=g0,
@@ -90,8 +91,8 @@ struct EdtPlan {
 };
 EdtPlan edt_plan(const Rect& C, const Rect& E, bool full_domain);
 struct EdtWS {
-    int *g = nullptr, *summ_first = nullptr, *summ_last = nullptr, *stack = nullptr,
-        *out = nullptr;
+    int *g = nullptr, *stack = nullptr, *out = nullptr;
+    unsigned long long* bits = nullptr;
     void layout(Arena& a, const Rect& C, const Rect& E);  // sized for the full domain E
 };
 

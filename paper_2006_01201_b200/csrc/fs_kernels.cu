@@ -17,48 +17,93 @@ namespace fs {
 // src/image.cpp:164-177 (place_on_canvas) for the first view of a fold: the
 // canvas valid plane was cleared; the view's pixels and validity are written
 // at its offset and its valid pixels counted.
+// Rows of a view rectangle are covered by 256-thread blocks that each walk
+// PART_ROWS rows; per-block results are reduced in shared memory so each
+// block issues one atomic per statistic (thousands, not millions).
+constexpr int PART_ROWS = 8;
+
 template <class V>
-__global__ void k_place_view(Canvas cv, V view, CanvasCount* count) {
-    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    int y = view.rect.y0 + blockIdx.y;
+__global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCount* count) {
+    __shared__ int red[8];
+    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
+    const int yb = min(ya + PART_ROWS, view.rect.y1());
     int n = 0;
-    if (x < view.rect.x1()) {
-        size_t p = (size_t)y * cv.w + x;
-        bool v = view.valid_at(x, y);
-        cv.rgb[p] = view.value_at(x, y);
-        cv.valid[p] = v ? 1 : 0;
-        n = v;
-    }
+    if (x < view.rect.x1())
+        for (int y = ya; y < yb; ++y) {
+            size_t p = (size_t)y * cv.w + x;
+            bool v = view.valid_at(x, y);
+            cv.rgb[p] = view.value_at(x, y);
+            cv.valid[p] = v ? 1 : 0;
+            n += v;
+        }
     n = __reduce_add_sync(0xffffffffu, n);
-    if ((threadIdx.x & 31) == 0 && n) atomicAdd(&count->valid_count, (unsigned long long)n);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        if (t) atomicAdd(&count->valid_count, (unsigned long long)t);
+    }
 }
 
 // src/image.cpp:115-132 + :140-148, restricted to the view rectangle (Area2 and
 // Area3 live there): Area2/Area3 counts and the Area3 bounding box.
 template <class V>
-__global__ void k_partition(const uint8_t* __restrict__ pvalid, int cw, V view, FoldStats* st) {
-    int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    int y = view.rect.y0 + blockIdx.y;
-    bool a2 = false, a3 = false;
-    if (x < view.rect.x1() && view.valid_at(x, y)) {
-        bool l = pvalid[(size_t)y * cw + x] != 0;
-        a3 = l;
-        a2 = !l;
-    }
-    unsigned m3 = __ballot_sync(0xffffffffu, a3);
-    unsigned m2 = __ballot_sync(0xffffffffu, a2);
-    int lane = threadIdx.x & 31;
-    int minx = a3 ? x : INT_MAX, maxx = a3 ? x : -1;
+__global__ void __launch_bounds__(256) k_partition(const uint8_t* __restrict__ pvalid, int cw,
+                                                   V view, FoldStats* st) {
+    __shared__ int red[5][8];
+    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
+    const int yb = min(ya + PART_ROWS, view.rect.y1());
+    int n2 = 0, n3 = 0, minx = INT_MAX, maxx = -1, miny = INT_MAX, maxy = -1;
+    if (x < view.rect.x1())
+        for (int y = ya; y < yb; ++y) {
+            if (!view.valid_at(x, y)) continue;
+            if (pvalid[(size_t)y * cw + x]) {
+                ++n3;
+                minx = min(minx, x);
+                maxx = max(maxx, x);
+                miny = min(miny, y);
+                maxy = max(maxy, y);
+            } else {
+                ++n2;
+            }
+        }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    n2 = __reduce_add_sync(0xffffffffu, n2);
+    n3 = __reduce_add_sync(0xffffffffu, n3);
     minx = __reduce_min_sync(0xffffffffu, minx);
     maxx = __reduce_max_sync(0xffffffffu, maxx);
+    miny = __reduce_min_sync(0xffffffffu, miny);
+    maxy = __reduce_max_sync(0xffffffffu, maxy);
     if (lane == 0) {
-        if (m2) atomicAdd(&st->cnt2, (unsigned long long)__popc(m2));
-        if (m3) {
-            atomicAdd(&st->cnt3, (unsigned long long)__popc(m3));
-            atomicMin(&st->bx0, minx);
-            atomicMax(&st->bx1, maxx);
-            atomicMin(&st->by0, y);
-            atomicMax(&st->by1, y);
+        red[0][wid] = n2;
+        red[1][wid] = n3;
+        red[2][wid] = minx;
+        red[3][wid] = maxx;
+        red[4][wid] = (maxy << 0);
+    }
+    __shared__ int rminy[8];
+    if (lane == 0) rminy[wid] = miny;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t2 = 0, t3 = 0, mnx = INT_MAX, mxx = -1, mny = INT_MAX, mxy = -1;
+        for (int k = 0; k < 8; ++k) {
+            t2 += red[0][k];
+            t3 += red[1][k];
+            mnx = min(mnx, red[2][k]);
+            mxx = max(mxx, red[3][k]);
+            mny = min(mny, rminy[k]);
+            mxy = max(mxy, red[4][k]);
+        }
+        if (t2) atomicAdd(&st->cnt2, (unsigned long long)t2);
+        if (t3) {
+            atomicAdd(&st->cnt3, (unsigned long long)t3);
+            atomicMin(&st->bx0, mnx);
+            atomicMax(&st->bx1, mxx);
+            atomicMin(&st->by0, mny);
+            atomicMax(&st->by1, mxy);
         }
     }
 }
@@ -134,10 +179,11 @@ constexpr int LK_NB = 8;
 constexpr int LK_S = 8;
 
 __host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
-__host__ inline size_t lk_smem_bytes(int iw, int r) {
-    size_t ring = (size_t)(2 * r + 1) * iw * 3 * sizeof(float);
-    ring = (ring + 15) & ~size_t(15);
-    return ring + (size_t)LK_NB * 5 * lk_iwp(iw) * sizeof(double);
+__host__ __device__ inline size_t lk_ring_bytes(int iw, int r) {
+    return ((size_t)(2 * r + 1) * iw * 3 * sizeof(float) + 15) & ~size_t(15);
+}
+__host__ inline size_t lk_smem_bytes(int iw, int r, int nq) {
+    return lk_ring_bytes(iw, r) + (size_t)LK_NB * nq * lk_iwp(iw) * sizeof(double);
 }
 
 template <int MODE>
@@ -159,21 +205,30 @@ __device__ __forceinline__ uint8_t lk_ok_at(const LkArgs& a, const LkDir& D, int
     return D.okin[(size_t)t.yn * a.cw + t.xn];
 }
 
-template <int MODE>
+// FULL (first iteration of a level, MODE 0 or 2): all five window sums, the
+// eigenvalue test (src/flow.cpp:267-275) and the reference's division-form
+// update; it also stores, per pixel, the level-constant inverse structure
+// tensor (c/det, b/det, a/det, ok) for the later iterations.  The structure
+// tensor depends only on the from-level's gradients, so it is identical in
+// every iteration of a level — as is the eigenvalue decision.
+// !FULL (iterations >= 1, MODE 1): only the two mismatch sums (sum Ix*It,
+// sum Iy*It) are formed; the update is -(M^-1 b) with the stored inverse.
+template <int MODE, bool FULL>
 __global__ void __launch_bounds__(128) k_lk_iter(LkArgs a) {
+    constexpr int NQ = FULL ? 5 : 2;
     extern __shared__ __align__(16) unsigned char smem[];
     const int IW = blockDim.x;
     const int r = a.r, K = 2 * r + 1;
     const int IWP = lk_iwp(IW);
-    size_t ring_bytes = ((size_t)K * IW * 3 * sizeof(float) + 15) & ~size_t(15);
     float* ring = reinterpret_cast<float*>(smem);
-    double* vbuf = reinterpret_cast<double*>(smem + ring_bytes);
+    double* vbuf = reinterpret_cast<double*>(smem + lk_ring_bytes(IW, r));
     const LkDir& D = a.d[blockIdx.z];
     const int w = a.w, h = a.h;
     const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
     const int c = threadIdx.x;
     const int x = x0 - r + c;
     const bool xin = x >= 0 && x < w;
+    const int xc = clampi(x, 0, w - 1);
     const int xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
 
     for (int k = 0; k < K; ++k) {
@@ -182,51 +237,66 @@ __global__ void __launch_bounds__(128) k_lk_iter(LkArgs a) {
         rs[1] = 0.f;
         rs[2] = 0.f;
     }
-    double V0 = 0.0, V1 = 0.0, V2 = 0.0, V3 = 0.0, V4 = 0.0;
+    double V[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) V[q] = 0.0;
     const int yo_end = min(y0 + a.th, h);
     const int ystart = y0 - r;
     const int yend = yo_end + r;
     const int nruns = (a.tw + LK_S - 1) / LK_S;
+    const int cc = c + (c >> 3);
 
     for (int ybase = ystart; ybase < yend; ybase += LK_NB) {
-        // ---- phase 1: per-column products and vertical running sums ----
-#pragma unroll 2
+        // ---- phase 1: per-column products and vertical running sums.  The
+        // batch's independent loads are issued together (rows unrolled), then
+        // the flow-dependent gathers of `to`, then the arithmetic.
+        float fc[LK_NB], gxs[LK_NB], gys[LK_NB];
+        float2 fl[LK_NB];
+        bool in[LK_NB];
+#pragma unroll
         for (int b = 0; b < LK_NB; ++b) {
             const int y = ybase + b;
-            float gx = 0.f, gy = 0.f, dt = 0.f;
-            if (xin && y >= 0 && y < h && y < yend) {
-                const float* Frow = D.F + (size_t)y * w;
-                const float fc = __ldg(Frow + x);
-                gx = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));
-                gy = 0.5f * (__ldg(D.F + (size_t)min(y + 1, h - 1) * w + x) -
-                             __ldg(D.F + (size_t)max(y - 1, 0) * w + x));
-                float2 f = lk_flow_at<MODE>(a, D, x, y);
-                LevelTap t = level_tap(w, h, (double)((float)x + f.x), (double)((float)y + f.y));
-                float warped = level_combine(t, __ldg(D.T + (size_t)t.y0 * w + t.x0),
-                                             __ldg(D.T + (size_t)t.y0 * w + t.x1),
-                                             __ldg(D.T + (size_t)t.y1 * w + t.x0),
-                                             __ldg(D.T + (size_t)t.y1 * w + t.x1));
-                dt = warped - fc;
-            }
-            const int slot = (y - ystart) % K;
+            in[b] = xin && y >= 0 && y < h && y < yend;
+            const int yy = clampi(y, 0, h - 1);
+            const float* Frow = D.F + (size_t)yy * w;
+            fc[b] = __ldg(Frow + xc);
+            gxs[b] = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));
+            gys[b] = 0.5f * (__ldg(D.F + (size_t)min(yy + 1, h - 1) * w + xc) -
+                             __ldg(D.F + (size_t)max(yy - 1, 0) * w + xc));
+            fl[b] = in[b] ? lk_flow_at<MODE>(a, D, xc, yy) : make_float2(0.f, 0.f);
+        }
+        float warped[LK_NB];
+#pragma unroll
+        for (int b = 0; b < LK_NB; ++b) {
+            const int yy = clampi(ybase + b, 0, h - 1);
+            LevelTap t = level_tap(w, h, (double)((float)xc + fl[b].x), (double)((float)yy + fl[b].y));
+            warped[b] = level_combine(t, __ldg(D.T + (size_t)t.y0 * w + t.x0),
+                                      __ldg(D.T + (size_t)t.y0 * w + t.x1),
+                                      __ldg(D.T + (size_t)t.y1 * w + t.x0),
+                                      __ldg(D.T + (size_t)t.y1 * w + t.x1));
+        }
+#pragma unroll
+        for (int b = 0; b < LK_NB; ++b) {
+            const float gx = in[b] ? gxs[b] : 0.f;
+            const float gy = in[b] ? gys[b] : 0.f;
+            const float dt = in[b] ? warped[b] - fc[b] : 0.f;
+            const int slot = (ybase + b - ystart) % K;
             float* rs = ring + ((size_t)slot * IW + c) * 3;
             const double ogx = rs[0], ogy = rs[1], odt = rs[2];
             rs[0] = gx;
             rs[1] = gy;
             rs[2] = dt;
             const double ix = gx, iy = gy, tt = dt;
-            V0 = (V0 + ix * ix) - ogx * ogx;
-            V1 = (V1 + ix * iy) - ogx * ogy;
-            V2 = (V2 + iy * iy) - ogy * ogy;
-            V3 = (V3 + ix * tt) - ogx * odt;
-            V4 = (V4 + iy * tt) - ogy * odt;
-            const int cc = c + (c >> 3);
-            double* vb = vbuf + (size_t)b * 5 * IWP + cc;
-            vb[0] = V0;
-            vb[IWP] = V1;
-            vb[2 * IWP] = V2;
-            vb[3 * IWP] = V3;
-            vb[4 * IWP] = V4;
+            double* vb = vbuf + (size_t)b * NQ * IWP + cc;
+            if (FULL) {
+                V[0] = (V[0] + ix * ix) - ogx * ogx;
+                V[1] = (V[1] + ix * iy) - ogx * ogy;
+                V[2] = (V[2] + iy * iy) - ogy * ogy;
+            }
+            V[NQ - 2] = (V[NQ - 2] + ix * tt) - ogx * odt;
+            V[NQ - 1] = (V[NQ - 1] + iy * tt) - ogy * odt;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) vb[q * IWP] = V[q];
         }
         __syncthreads();
         // ---- phase 2: horizontal sliding sums + 2x2 solve ----
@@ -236,34 +306,49 @@ __global__ void __launch_bounds__(128) k_lk_iter(LkArgs a) {
             if (yo < y0 || yo >= yo_end) continue;
             const int cs = run * LK_S;
             const int nout = min(LK_S, a.tw - cs);
-            const double* vb = vbuf + (size_t)b * 5 * IWP;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
-            for (int cc = cs; cc <= cs + 2 * r; ++cc) {
-                const int ci = cc + (cc >> 3);
-                s0 += vb[ci];
-                s1 += vb[IWP + ci];
-                s2 += vb[2 * IWP + ci];
-                s3 += vb[3 * IWP + ci];
-                s4 += vb[4 * IWP + ci];
+            const double* vb = vbuf + (size_t)b * NQ * IWP;
+            double s[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) s[q] = 0.0;
+            for (int k = cs; k <= cs + 2 * r; ++k) {
+                const int ci = k + (k >> 3);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) s[q] += vb[q * IWP + ci];
             }
-            for (int s = 0; s < nout; ++s) {
-                if (s > 0) {
-                    const int ca = cs + 2 * r + s, cb = cs + s - 1;
+            for (int o = 0; o < nout; ++o) {
+                if (o > 0) {
+                    const int ca = cs + 2 * r + o, cb = cs + o - 1;
                     const int ia = ca + (ca >> 3), ib = cb + (cb >> 3);
-                    s0 = (s0 + vb[ia]) - vb[ib];
-                    s1 = (s1 + vb[IWP + ia]) - vb[IWP + ib];
-                    s2 = (s2 + vb[2 * IWP + ia]) - vb[2 * IWP + ib];
-                    s3 = (s3 + vb[3 * IWP + ia]) - vb[3 * IWP + ib];
-                    s4 = (s4 + vb[4 * IWP + ia]) - vb[4 * IWP + ib];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) s[q] = (s[q] + vb[q * IWP + ia]) - vb[q * IWP + ib];
                 }
-                const int xo = x0 + cs + s;
+                const int xo = x0 + cs + o;
                 if (xo >= w) break;
+                const size_t oi = (size_t)yo * w + xo;
                 float2 f = lk_flow_at<MODE>(a, D, xo, yo);
-                uint8_t ok = lk_ok_at<MODE>(a, D, xo, yo);
-                if (lk_solve(s0, s1, s2, s3, s4, a.eig_thresh, a.flow_cap, f.x, f.y)) ok = 1;
-                const size_t o = (size_t)yo * w + xo;
-                D.fout[o] = f;
-                D.okout[o] = ok;
+                if (FULL) {
+                    uint8_t ok = lk_ok_at<MODE>(a, D, xo, yo);
+                    const double A = s[0], B = s[1], Cc = s[2];
+                    float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (lk_solve(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y)) {
+                        ok = 1;
+                        const double det = A * Cc - B * B;
+                        coef = make_float4((float)(Cc / det), (float)(B / det), (float)(A / det), 1.f);
+                    }
+                    D.okout[oi] = ok;
+                    if (D.coef) D.coef[oi] = coef;
+                } else {
+                    const float4 cf = D.coef[oi];
+                    if (cf.w != 0.f) {
+                        const double bx = s[0], by = s[1];
+                        const double ux = -((double)cf.x * bx - (double)cf.y * by);
+                        const double uy = -((double)cf.z * by - (double)cf.y * bx);
+                        float ndx = f.x + (float)ux, ndy = f.y + (float)uy;
+                        final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
+                        f = make_float2(ndx, ndy);
+                    }
+                }
+                D.fout[oi] = f;
             }
         }
         __syncthreads();
@@ -281,7 +366,7 @@ __global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
     __shared__ float2 src[SM_TY + 4][SM_TX + 4];
     __shared__ float2 p1[SM_TY + 2][SM_TX + 2];
     const int d = blockIdx.z;
-    const float2* fin = a.fin[d];
+    const float2* fin = d ? a.fin[1] : a.fin[0];
     const int w = a.w, h = a.h;
     const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
     const int halo = a.passes == 2 ? 2 : 1;
@@ -335,9 +420,9 @@ __global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
     size_t o = (size_t)gy * w + gx;
     if (a.final_cap > 0.f) {
         final_cap(a.final_cap, vx, vy);
-        a.valid_out[d][o] = a.ok[d][o];
+        (d ? a.valid_out[1] : a.valid_out[0])[o] = (d ? a.ok[1] : a.ok[0])[o];
     }
-    a.fout[d][o] = make_float2(vx, vy);
+    (d ? a.fout[1] : a.fout[0])[o] = make_float2(vx, vy);
 }
 
 // Level-0 finalisation when smoothing_passes == 0 (src/flow.cpp:300-313).
@@ -346,10 +431,10 @@ __global__ void k_finalize_flow(SmoothArgs a) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int n = a.w * a.h;
     if (i >= n) return;
-    float2 f = a.fin[d][i];
+    float2 f = (d ? a.fin[1] : a.fin[0])[i];
     final_cap(a.final_cap, f.x, f.y);
-    a.fout[d][i] = f;
-    a.valid_out[d][i] = a.ok[d][i];
+    (d ? a.fout[1] : a.fout[0])[i] = f;
+    (d ? a.valid_out[1] : a.valid_out[0])[i] = (d ? a.ok[1] : a.ok[0])[i];
 }
 
 // ============================================================================
@@ -378,32 +463,44 @@ __device__ __forceinline__ void edt_line_xy(const EdtJob<M>& J, int line, int p,
     }
 }
 
-// pass 1a: first/last seed position per (line, segment)
+// pass 1a: the seed mask of every (line, 64-position segment) as a bit set.
+// Columns-first: a thread per (column, segment), consecutive threads read
+// consecutive columns.  Rows-first: a warp per (row, segment), two ballots.
 template <class M>
-__global__ void k_edt_summ(EdtJob<M> J0, EdtJob<M> J1) {
+__global__ void k_edt_bits(EdtJob<M> J0, EdtJob<M> J1) {
     const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
     if (!J.active) return;
     const int nlines = J.vfirst ? J.W.w : J.W.h;
     const int len = J.vfirst ? J.W.h : J.W.w;
     const int nseg = (len + EDT_SEG - 1) / EDT_SEG;
-    int line = blockIdx.x * blockDim.x + threadIdx.x;
-    int seg = blockIdx.y;
-    if (line >= nlines || seg >= nseg) return;
-    int first = -1, last = -1;
-    int p0 = seg * EDT_SEG, p1 = min(len, p0 + EDT_SEG);
-    for (int p = p0; p < p1; ++p) {
-        int x, y;
-        edt_line_xy(J, line, p, x, y);
-        if (J.mask(x, y)) {
-            if (first < 0) first = p;
-            last = p;
+    const int seg = blockIdx.y;
+    if (seg >= nseg) return;
+    const int p0 = seg * EDT_SEG;
+    if (J.vfirst) {
+        const int line = blockIdx.x * blockDim.x + threadIdx.x;
+        if (line >= nlines) return;
+        const int n = min(EDT_SEG, len - p0);
+        unsigned long long bits = 0;
+#pragma unroll 16
+        for (int k = 0; k < EDT_SEG; ++k) {
+            if (k < n && J.mask(J.W.x0 + line, J.W.y0 + p0 + k)) bits |= 1ull << k;
         }
+        J.bits[(size_t)seg * nlines + line] = bits;
+    } else {
+        const int lane = threadIdx.x & 31;
+        const int line = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if (line >= nlines) return;
+        const int pa = p0 + lane, pb = p0 + 32 + lane;
+        bool a = pa < len && J.mask(J.W.x0 + pa, J.W.y0 + line);
+        bool b = pb < len && J.mask(J.W.x0 + pb, J.W.y0 + line);
+        unsigned lo = __ballot_sync(0xffffffffu, a), hi = __ballot_sync(0xffffffffu, b);
+        if (lane == 0)
+            J.bits[(size_t)seg * nlines + line] = (unsigned long long)lo | ((unsigned long long)hi << 32);
     }
-    J.summ_first[(size_t)seg * nlines + line] = first;
-    J.summ_last[(size_t)seg * nlines + line] = last;
 }
 
-// pass 1b: squared 1-D distance for every output position of every line
+// pass 1b: squared 1-D distance to the nearest seed along the line, for every
+// output position (C's extent along the line), from the segment bit sets.
 template <class M>
 __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
     const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
@@ -413,56 +510,47 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
     const int nseg = (len + EDT_SEG - 1) / EDT_SEG;
     const int oa = J.vfirst ? J.C.y0 - J.W.y0 : J.C.x0 - J.W.x0;
     const int ob = oa + (J.vfirst ? J.C.h : J.C.w);
-    int line = blockIdx.x * blockDim.x + threadIdx.x;
-    int seg = oa / EDT_SEG + blockIdx.y;
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    const int seg = oa / EDT_SEG + blockIdx.y;
     if (line >= nlines || seg >= nseg) return;
-    int p0 = max(seg * EDT_SEG, oa), p1 = min(min(len, (seg + 1) * EDT_SEG), ob);
+    const int s0 = seg * EDT_SEG;
+    const int p0 = max(s0, oa), p1 = min(min(len, s0 + EDT_SEG), ob);
     if (p0 >= p1) return;
-    const int s0 = seg * EDT_SEG, s1 = min(len, (seg + 1) * EDT_SEG);
-    // nearest seed before the segment and after it
-    int prev = INT_MIN / 2, next = INT_MAX / 2;
+    const unsigned long long* B = J.bits + line;
+    const unsigned long long mine = B[(size_t)seg * nlines];
+    long long prev = -(1LL << 40), next = 1LL << 40;  // nearest seed before / after the segment
     for (int s = seg - 1; s >= 0; --s) {
-        int l = J.summ_last[(size_t)s * nlines + line];
-        if (l >= 0) {
-            prev = l;
+        unsigned long long m = B[(size_t)s * nlines];
+        if (m) {
+            prev = (long long)s * EDT_SEG + 63 - __clzll((long long)m);
             break;
         }
     }
     for (int s = seg + 1; s < nseg; ++s) {
-        int f = J.summ_first[(size_t)s * nlines + line];
-        if (f >= 0) {
-            next = f;
+        unsigned long long m = B[(size_t)s * nlines];
+        if (m) {
+            next = (long long)s * EDT_SEG + __ffsll((long long)m) - 1;
             break;
         }
     }
     const int gstride = J.vfirst ? J.W.w : J.W.h;  // pass-2 line length
-    // forward: last seed <= p
-    int last = prev;
-    for (int p = s0; p < p1; ++p) {
-        int x, y;
-        edt_line_xy(J, line, p, x, y);
-        if (J.mask(x, y)) last = p;
-        if (p >= p0) {
-            long long d = (long long)p - last;
-            J.g[(size_t)(p - oa) * gstride + line] = d < 46341 ? (int)(d * d) : kInfSq;
-        }
-    }
-    // backward: first seed >= p
-    int nxt = next;
-    for (int p = s1 - 1; p >= p0; --p) {
-        int x, y;
-        edt_line_xy(J, line, p, x, y);
-        if (J.mask(x, y)) nxt = p;
-        if (p < p1) {
-            long long d = (long long)nxt - p;
-            int dd = d < 46341 ? (int)(d * d) : kInfSq;
-            int* gp = J.g + (size_t)(p - oa) * gstride + line;
-            if (dd < *gp) *gp = dd;
-        }
+    for (int p = p0; p < p1; ++p) {
+        const int k = p - s0;
+        const unsigned long long upto = k == 63 ? ~0ull : ((2ull << k) - 1);
+        const unsigned long long lowm = mine & upto, highm = mine & ~((1ull << k) - 1);
+        const long long last = lowm ? (long long)s0 + 63 - __clzll((long long)lowm) : prev;
+        const long long nxt = highm ? (long long)s0 + __ffsll((long long)highm) - 1 : next;
+        const long long d = min((long long)p - last, nxt - (long long)p);
+        J.g[(size_t)(p - oa) * gstride + line] = d < 46341 ? (int)(d * d) : kInfSq;
     }
 }
 
-// pass 2: lower envelope along the other axis for each output line
+// pass 2: lower envelope of parabolas along the other axis, a warp per output
+// line: ballot search of the nearest on-line seeds around the output range
+// (they dominate every site behind them), ballot compaction of the finite
+// sites in between, envelope built by lane 0 with exact int64 intersection
+// comparisons (Felzenszwalb, src/blend_field.cpp:19-47), then every lane
+// evaluates its outputs by binary search over the envelope's breakpoints.
 template <class M>
 __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
                                const CanvasCount* cc) {
@@ -470,62 +558,84 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
     if (!J.active) return;
     const int nout_lines = J.vfirst ? J.C.h : J.C.w;
     const int L = J.vfirst ? J.W.w : J.W.h;  // sites per line
-    int ol = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int ol = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (ol >= nout_lines) return;
     const int* f = J.g + (size_t)ol * L;
     int* stk = J.stack + (size_t)ol * L;
     const int qa = J.vfirst ? J.C.x0 - J.W.x0 : J.C.y0 - J.W.y0;
     const int qb = qa + (J.vfirst ? J.C.w : J.C.h);
-    // prune at the nearest on-line seeds (f == 0) around [qa, qb)
     int lo = 0, hi = L - 1;
-    for (int s = qa; s >= 0; --s)
-        if (f[s] == 0) {
-            lo = s;
+    for (int base = qa; base >= 0; base -= 32) {
+        const int s = base - lane;
+        const unsigned m = __ballot_sync(0xffffffffu, s >= 0 && f[s] == 0);
+        if (m) {
+            lo = base - (__ffs(m) - 1);
             break;
         }
-    for (int s = qb - 1; s < L; ++s)
-        if (f[s] == 0) {
-            hi = s;
-            break;
-        }
-    int n = 0;
-    for (int q = lo; q <= hi; ++q) {
-        long long fq = f[q];
-        if (fq >= kInfSq) continue;
-        while (n >= 2) {
-            // intersection (q, top) <= intersection (top, below) ?
-            int t = stk[n - 1], u = stk[n - 2];
-            long long ft = f[t], fu = f[u];
-            long long n1 = (fq + (long long)q * q) - (ft + (long long)t * t), d1 = 2LL * (q - t);
-            long long n2 = (ft + (long long)t * t) - (fu + (long long)u * u), d2 = 2LL * (t - u);
-            if (n1 * d2 <= n2 * d1)
-                --n;
-            else
-                break;
-        }
-        stk[n++] = q;
     }
-    // certificate bound helpers
-    const bool have = J.which == 1   ? (cc->valid_count - st->cnt3) > 0
-                      : J.which == 2 ? st->cnt2 > 0
-                                     : true;
-    int k = 0;
-    bool fail = false;
-    for (int q = qa; q < qb; ++q) {
-        int dsq = kInfSq;
-        if (n > 0) {
-            while (k + 1 < n) {
-                int a0 = stk[k], a1 = stk[k + 1];
-                long long fa = f[a0], fb = f[a1];
-                long long num = (fb + (long long)a1 * a1) - (fa + (long long)a0 * a0);
-                long long den = 2LL * (a1 - a0);
-                if (num < (long long)q * den)
-                    ++k;
+    for (int base = qb - 1; base < L; base += 32) {
+        const int s = base + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, s < L && f[s] == 0);
+        if (m) {
+            hi = base + __ffs(m) - 1;
+            break;
+        }
+    }
+    int n = 0;
+    const unsigned lt = (1u << lane) - 1;
+    for (int base = lo; base <= hi; base += 32) {
+        const int s = base + lane;
+        const bool fin = s <= hi && f[s] < kInfSq;
+        const unsigned m = __ballot_sync(0xffffffffu, fin);
+        if (fin) stk[n + __popc(m & lt)] = s;
+        n += __popc(m);
+    }
+    __syncwarp();
+    int ne = 0;
+    if (lane == 0) {
+        for (int i = 0; i < n; ++i) {
+            const int q = stk[i];
+            const long long fq = f[q];
+            while (ne >= 2) {
+                const int t = stk[ne - 1], u = stk[ne - 2];
+                const long long ft = f[t], fu = f[u];
+                const long long n1 = (fq + (long long)q * q) - (ft + (long long)t * t);
+                const long long d1 = 2LL * (q - t);
+                const long long n2 = (ft + (long long)t * t) - (fu + (long long)u * u);
+                const long long d2 = 2LL * (t - u);
+                if (n1 * d2 <= n2 * d1)
+                    --ne;
                 else
                     break;
             }
-            long long d = q - stk[k];
-            long long v = d * d + f[stk[k]];
+            stk[ne++] = q;
+        }
+    }
+    ne = __shfl_sync(0xffffffffu, ne, 0);
+    __syncwarp();
+    const bool have = J.which == 1   ? (cc->valid_count - st->cnt3) > 0
+                      : J.which == 2 ? st->cnt2 > 0
+                                     : true;
+    bool fail = false;
+    for (int q = qa + lane; q < qb; q += 32) {
+        int dsq = kInfSq;
+        if (ne > 0) {
+            // k = largest j with breakpoint z_j < q (z_0 = -inf)
+            int klo = 0, khi = ne - 1;
+            while (klo < khi) {
+                const int mid = (klo + khi + 1) >> 1;
+                const int a0 = stk[mid - 1], a1 = stk[mid];
+                const long long num = ((long long)f[a1] + (long long)a1 * a1) -
+                                      ((long long)f[a0] + (long long)a0 * a0);
+                const long long den = 2LL * (a1 - a0);
+                if (num < (long long)q * den)
+                    klo = mid;
+                else
+                    khi = mid - 1;
+            }
+            const long long d = q - stk[klo];
+            const long long v = d * d + f[stk[klo]];
             dsq = v < kInfSq ? (int)v : kInfSq;
         }
         int x, y;
@@ -546,7 +656,8 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
             if (bnd != LLONG_MAX && (long long)dsq > bnd * bnd) fail = true;
         }
     }
-    if (fail) atomicOr((unsigned int*)&st->edt_fail, 1u << (blockIdx.z));
+    if (__any_sync(0xffffffffu, fail) && lane == 0)
+        atomicOr((unsigned int*)&st->edt_fail, 1u << (blockIdx.z));
 }
 
 // ============================================================================
@@ -701,11 +812,13 @@ static inline dim3 row_grid(int w, int h, int bx = 256) { return dim3((w + bx - 
 
 template <class V>
 void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s) {
-    k_place_view<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, count);
+    k_place_view<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
+        cv, view, count);
 }
 template <class V>
 void partition(const Canvas& cv, const V& view, FoldStats* st, cudaStream_t s) {
-    k_partition<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv.valid, cv.w, view, st);
+    k_partition<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
+        cv.valid, cv.w, view, st);
 }
 void check_box(FoldStats* st, const Rect& planned, cudaStream_t s) {
     k_check_box<<<1, 1, 0, s>>>(st, planned);
@@ -725,24 +838,39 @@ void downsample(const float* in0, const float* in1, float* out0, float* out1, in
 static bool lk_configured = false;
 void init() {
     if (lk_configured) return;
-    cudaFuncSetAttribute(k_lk_iter<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_lk_iter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_lk_iter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int mx = 200 * 1024;
+    cudaFuncSetAttribute(k_lk_iter<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_iter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_iter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     lk_configured = true;
+}
+// Output tile: 128 - 2r columns (one thread per input column) by th rows; th
+// shrinks on small levels so the grid still covers the SMs (a CTA's sweep is
+// a serial chain of th + 2r rows).
+int lk_tile_rows(int w, int h, int r, int ndir) {
+    const int tw = 128 - 2 * r;
+    const int cols = (w + tw - 1) / tw;
+    for (int th : {64, 32}) {
+        long ctas = (long)cols * ((h + th - 1) / th) * ndir;
+        if (ctas >= 148L * 4) return th;
+    }
+    return 16;
 }
 cudaError_t lk_iter(const LkArgs& a0, cudaStream_t s) {
     LkArgs a = a0;
-    int iw = 128;
+    const int iw = 128;
     a.tw = iw - 2 * a.r;
-    size_t smem = lk_smem_bytes(iw, a.r);
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir);
+    const bool full = a.mode != 1;
+    const size_t smem = lk_smem_bytes(iw, a.r, full ? 5 : 2);
     init();
     dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
     if (a.mode == 0)
-        k_lk_iter<0><<<g, iw, smem, s>>>(a);
+        k_lk_iter<0, true><<<g, iw, smem, s>>>(a);
     else if (a.mode == 1)
-        k_lk_iter<1><<<g, iw, smem, s>>>(a);
+        k_lk_iter<1, false><<<g, iw, smem, s>>>(a);
     else
-        k_lk_iter<2><<<g, iw, smem, s>>>(a);
+        k_lk_iter<2, true><<<g, iw, smem, s>>>(a);
     return cudaGetLastError();
 }
 int lk_max_radius() { return 48; }
@@ -775,9 +903,15 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, const Ca
         max_out = max(max_out, j->vfirst ? j->C.h : j->C.w);
     }
     if (max_lines == 0) return;
-    k_edt_summ<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
+    if (j0.vfirst == j1.vfirst || !j1.active || !j0.active) {
+        const bool vf = j0.active ? j0.vfirst : j1.vfirst;
+        if (vf)
+            k_edt_bits<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
+        else
+            k_edt_bits<M><<<dim3((max_lines + 7) / 8, max_seg, 2), 256, 0, s>>>(j0, j1);
+    }
     k_edt_line<M><<<dim3((max_lines + 127) / 128, max_oseg, 2), 128, 0, s>>>(j0, j1);
-    k_edt_envelope<M><<<dim3((max_out + 63) / 64, 1, 2), 64, 0, s>>>(j0, j1, st, cc);
+    k_edt_envelope<M><<<dim3((max_out + 7) / 8, 1, 2), 256, 0, s>>>(j0, j1, st, cc);
 }
 
 template <class V>
