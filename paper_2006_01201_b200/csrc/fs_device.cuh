@@ -81,6 +81,8 @@ struct LkDir {
     uint8_t* okout;   // written by the first iteration of a level only
     float4* coef;     // level-constant (c/det, b/det, a/det, ok): written by the
                       // first iteration, read by the later ones (nullptr: unused)
+    const float* dtin;  // It of this iteration (written by prep / the previous sweep)
+    float* dtout;       // It of the next iteration (nullptr: level's last iteration)
 };
 struct LkArgs {
     LkDir d[2];
@@ -154,7 +156,8 @@ struct EdtJob {
 };
 
 namespace launch {
-void init();  // one-time kernel attributes (call before any graph capture)
+void init();     // one-time kernel attributes (call before any graph capture)
+void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
 template <class V> void partition(const Canvas&, const V&, FoldStats*, cudaStream_t);
@@ -163,7 +166,8 @@ template <class V>
 void crop_gray(const Canvas&, const V&, const Rect&, float*, float*, cudaStream_t);
 void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
                 int nimg, cudaStream_t);
-cudaError_t lk_iter(const LkArgs&, cudaStream_t);
+cudaError_t lk_prep(const LkArgs&, cudaStream_t);              // mode 0 or 2
+cudaError_t lk_sweep(const LkArgs&, bool full, cudaStream_t);  // one LK iteration
 int lk_max_radius();
 void smooth(const SmoothArgs&, cudaStream_t);
 void finalize_flow(const SmoothArgs&, cudaStream_t);

@@ -113,6 +113,7 @@ void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
         for (int q = 0; q < 2; ++q) {
             fb[d][q] = a.take<float2>(n);
             ok[d][q] = a.take<uint8_t>(n);
+            dt[d][q] = a.take<float>(n);
         }
         coef[d] = a.take<float4>(n);
     }
@@ -135,49 +136,75 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     const int r = p.window_radius;
     const double win_area = static_cast<double>(2 * r + 1) * (2 * r + 1);
     const double eig_thresh = p.min_eigen_eps * win_area;  // src/flow.cpp:205-206
-    int fcur = 0, okcur = 0;
+    static const char* kSweepNames[2][8] = {
+        {"lk_iter", "lk_iter_L1", "lk_iter_L2", "lk_iter_L3", "lk_iter_L4", "lk_iter_L5",
+         "lk_iter_L6", "lk_iter_L7"},
+        {"lk_first", "lk_first_L1", "lk_first_L2", "lk_first_L3", "lk_first_L4",
+         "lk_first_L5", "lk_first_L6", "lk_first_L7"}};
+    int fcur = 0, okcur = 0, dcur = 0;
     for (int l = ws.depth - 1; l >= 0; --l) {
         const Level L = ws.lv[l];
+        const double npx = (double)L.w * L.h * ws.ndir;
+        LkArgs a{};
+        a.ndir = ws.ndir;
+        a.w = L.w;
+        a.h = L.h;
+        a.r = r;
+        a.th = 0;  // per-level choice (launch::lk_tile_rows)
+        a.eig_thresh = eig_thresh;
+        a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
+        a.mode = l == ws.depth - 1 ? 0 : 2;
+        if (a.mode == 2) {
+            a.cw = ws.lv[l + 1].w;
+            a.ch = ws.lv[l + 1].h;
+            a.sx = static_cast<double>(a.cw) / L.w;  // src/flow.cpp:145-146
+            a.sy = static_cast<double>(a.ch) / L.h;
+        }
+        for (int d = 0; d < ws.ndir; ++d) {
+            int src = ws.ndir == 1 ? 0 : d;
+            a.d[d].F = ws.pyr[src][l];
+            a.d[d].T = ws.pyr[1 - src][l];
+            a.d[d].coef = p.iterations_per_level > 1 ? ws.coef[d] : nullptr;
+        }
+        // level start: flow (zero / upsampled), ever_ok, It
+        for (int d = 0; d < ws.ndir; ++d) {
+            a.d[d].fin = ws.fb[d][fcur];
+            a.d[d].okin = ws.ok[d][okcur];
+            a.d[d].fout = ws.fb[d][fcur ^ 1];
+            a.d[d].okout = ws.ok[d][okcur ^ 1];
+            a.d[d].dtout = ws.dt[d][dcur];
+        }
+        {
+            // F 4 + T 4 + flow 8 + ok 1 + It 4 out, + the coarser flow/ok 9/4
+            ProfScope ps("lk_prep", (21.0 + (a.mode == 2 ? 2.25 : 0.0)) * npx, s);
+            FS_CK(launch::lk_prep(a, s));
+        }
+        ++launches;
+        fcur ^= 1;
+        okcur ^= 1;
         for (int it = 0; it < p.iterations_per_level; ++it) {
-            LkArgs a{};
-            a.ndir = ws.ndir;
-            a.w = L.w;
-            a.h = L.h;
-            a.mode = it > 0 ? 1 : (l == ws.depth - 1 ? 0 : 2);
-            if (a.mode == 2) {
-                a.cw = ws.lv[l + 1].w;
-                a.ch = ws.lv[l + 1].h;
-                a.sx = static_cast<double>(a.cw) / L.w;  // src/flow.cpp:145-146
-                a.sy = static_cast<double>(a.ch) / L.h;
-            }
-            a.r = r;
-            a.th = 0;  // per-level choice (launch::lk_tile_rows)
-            a.eig_thresh = eig_thresh;
-            a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
+            const bool full = it == 0, last = it + 1 == p.iterations_per_level;
             for (int d = 0; d < ws.ndir; ++d) {
-                int src = ws.ndir == 1 ? 0 : d;
-                a.d[d].F = ws.pyr[src][l];
-                a.d[d].T = ws.pyr[1 - src][l];
                 a.d[d].fin = ws.fb[d][fcur];
                 a.d[d].okin = ws.ok[d][okcur];
                 a.d[d].fout = ws.fb[d][fcur ^ 1];
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
-                a.d[d].coef = p.iterations_per_level > 1 ? ws.coef[d] : nullptr;
+                a.d[d].dtin = ws.dt[d][dcur];
+                a.d[d].dtout = last ? nullptr : ws.dt[d][dcur ^ 1];
             }
             {
-                // per pixel and direction: F 4 + T 4 + flow out 8, and
-                //  first iteration: ok out 1 + coef out 16 + (mode 2) the coarse
-                //                   level's flow/ok 9/4;
-                //  later ones:      flow in 8 + coef in 16
-                double per = a.mode == 1 ? 16.0 + 8.0 + 16.0
-                                         : 16.0 + 1.0 + (a.d[0].coef ? 16.0 : 0.0) +
-                                               (a.mode == 2 ? 2.25 : 0.0);
-                ProfScope ps("lk_iter", per * L.w * L.h * ws.ndir, s);
-                FS_CK(launch::lk_iter(a, s));
+                // per pixel and direction: F 4 + It 4 + flow 8 in, flow 8 out;
+                //  first iteration: ok 1 in/out + coef 16 out; later: coef 16 in;
+                //  not the level's last: F 4 + T 4 in, It 4 out for the next one
+                double per = 24.0 + (full ? 2.0 + (a.d[0].coef ? 16.0 : 0.0) : 16.0) +
+                             (last ? 0.0 : 12.0);
+                ProfScope ps(kSweepNames[full][std::min(l, 7)], per * npx, s);
+                FS_CK(launch::lk_sweep(a, full, s));
             }
             ++launches;
             fcur ^= 1;
-            if (it == 0) okcur ^= 1;  // ever_ok is final after a level's first iteration
+            if (!last) dcur ^= 1;
+            if (full) okcur ^= 1;  // ever_ok is final after a level's first iteration
         }
         int P = p.smoothing_passes;
         while (P > 0) {
@@ -197,7 +224,8 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.valid_out[d] = out_valid[d];
             }
             {
-                ProfScope ps("smooth", (16.0 + (fin ? 2.0 : 0.0)) * L.w * L.h * ws.ndir, s);
+                ProfScope ps(l == 0 ? "smooth" : "smooth_coarse",
+                             (16.0 + (fin ? 2.0 : 0.0)) * L.w * L.h * ws.ndir, s);
                 launch::smooth(a, s);
             }
             ++launches;

@@ -160,207 +160,16 @@ __global__ void k_downsample(const float* __restrict__ in0, const float* __restr
     out[(size_t)j * ow + i] = acc;
 }
 
-// ============================================================================
-// K2+K3 — one fused LK iteration (src/flow.cpp:225-291), both directions.
-//
-// A CTA owns an output tile of tw columns x th rows and sweeps its input rows
-// top to bottom.  Thread c owns input column x0-r+c and keeps the five
-// vertical running window sums (double) of its column in registers; the
-// per-pixel inputs (gx, gy, dt) of the last 2r+1 rows live in a shared-memory
-// ring so the row leaving the window is subtracted exactly.  Every LK_NB rows
-// the column sums are staged in shared memory and turned into horizontal
-// (2r+1)-tap sums by sliding runs of LK_S outputs, then solved.  Products are
-// exact in double (float x float); the window sums are double, so they agree
-// with the reference's double prefix tables to ~1e-12 relative.  Upsampling of
-// the coarser level's flow (src/flow.cpp:138-170) is fused into the first
-// iteration of each level (MODE 2).
-// ============================================================================
-constexpr int LK_NB = 8;
-constexpr int LK_S = 8;
-
-__host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
-__host__ __device__ inline size_t lk_ring_bytes(int iw, int r) {
-    return ((size_t)(2 * r + 1) * iw * 3 * sizeof(float) + 15) & ~size_t(15);
-}
-__host__ inline size_t lk_smem_bytes(int iw, int r, int nq) {
-    return lk_ring_bytes(iw, r) + (size_t)LK_NB * nq * lk_iwp(iw) * sizeof(double);
-}
-
-template <int MODE>
-__device__ __forceinline__ float2 lk_flow_at(const LkArgs& a, const LkDir& D, int x, int y) {
-    if (MODE == 0) return make_float2(0.f, 0.f);
-    if (MODE == 1) return D.fin[(size_t)y * a.w + x];
-    UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
-    float2 f00 = D.fin[(size_t)t.y0 * a.cw + t.x0], f10 = D.fin[(size_t)t.y0 * a.cw + t.x1];
-    float2 f01 = D.fin[(size_t)t.y1 * a.cw + t.x0], f11 = D.fin[(size_t)t.y1 * a.cw + t.x1];
-    return make_float2(up_combine(t, f00.x, f10.x, f01.x, f11.x),
-                       up_combine(t, f00.y, f10.y, f01.y, f11.y));
-}
-
-template <int MODE>
-__device__ __forceinline__ uint8_t lk_ok_at(const LkArgs& a, const LkDir& D, int x, int y) {
-    if (MODE == 0) return 0;
-    if (MODE == 1) return D.okin[(size_t)y * a.w + x];
-    UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
-    return D.okin[(size_t)t.yn * a.cw + t.xn];
-}
-
-// FULL (first iteration of a level, MODE 0 or 2): all five window sums, the
-// eigenvalue test (src/flow.cpp:267-275) and the reference's division-form
-// update; it also stores, per pixel, the level-constant inverse structure
-// tensor (c/det, b/det, a/det, ok) for the later iterations.  The structure
-// tensor depends only on the from-level's gradients, so it is identical in
-// every iteration of a level — as is the eigenvalue decision.
-// !FULL (iterations >= 1, MODE 1): only the two mismatch sums (sum Ix*It,
-// sum Iy*It) are formed; the update is -(M^-1 b) with the stored inverse.
-template <int MODE, bool FULL>
-__global__ void __launch_bounds__(128) k_lk_iter(LkArgs a) {
-    constexpr int NQ = FULL ? 5 : 2;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int IW = blockDim.x;
-    const int r = a.r, K = 2 * r + 1;
-    const int IWP = lk_iwp(IW);
-    float* ring = reinterpret_cast<float*>(smem);
-    double* vbuf = reinterpret_cast<double*>(smem + lk_ring_bytes(IW, r));
-    const LkDir& D = a.d[blockIdx.z];
-    const int w = a.w, h = a.h;
-    const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
-    const int c = threadIdx.x;
-    const int x = x0 - r + c;
-    const bool xin = x >= 0 && x < w;
-    const int xc = clampi(x, 0, w - 1);
-    const int xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
-
-    for (int k = 0; k < K; ++k) {
-        float* rs = ring + ((size_t)k * IW + c) * 3;
-        rs[0] = 0.f;
-        rs[1] = 0.f;
-        rs[2] = 0.f;
-    }
-    double V[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) V[q] = 0.0;
-    const int yo_end = min(y0 + a.th, h);
-    const int ystart = y0 - r;
-    const int yend = yo_end + r;
-    const int nruns = (a.tw + LK_S - 1) / LK_S;
-    const int cc = c + (c >> 3);
-
-    for (int ybase = ystart; ybase < yend; ybase += LK_NB) {
-        // ---- phase 1: per-column products and vertical running sums.  The
-        // batch's independent loads are issued together (rows unrolled), then
-        // the flow-dependent gathers of `to`, then the arithmetic.
-        float fc[LK_NB], gxs[LK_NB], gys[LK_NB];
-        float2 fl[LK_NB];
-        bool in[LK_NB];
-#pragma unroll
-        for (int b = 0; b < LK_NB; ++b) {
-            const int y = ybase + b;
-            in[b] = xin && y >= 0 && y < h && y < yend;
-            const int yy = clampi(y, 0, h - 1);
-            const float* Frow = D.F + (size_t)yy * w;
-            fc[b] = __ldg(Frow + xc);
-            gxs[b] = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));
-            gys[b] = 0.5f * (__ldg(D.F + (size_t)min(yy + 1, h - 1) * w + xc) -
-                             __ldg(D.F + (size_t)max(yy - 1, 0) * w + xc));
-            fl[b] = in[b] ? lk_flow_at<MODE>(a, D, xc, yy) : make_float2(0.f, 0.f);
-        }
-        float warped[LK_NB];
-#pragma unroll
-        for (int b = 0; b < LK_NB; ++b) {
-            const int yy = clampi(ybase + b, 0, h - 1);
-            LevelTap t = level_tap(w, h, (double)((float)xc + fl[b].x), (double)((float)yy + fl[b].y));
-            warped[b] = level_combine(t, __ldg(D.T + (size_t)t.y0 * w + t.x0),
-                                      __ldg(D.T + (size_t)t.y0 * w + t.x1),
-                                      __ldg(D.T + (size_t)t.y1 * w + t.x0),
-                                      __ldg(D.T + (size_t)t.y1 * w + t.x1));
-        }
-#pragma unroll
-        for (int b = 0; b < LK_NB; ++b) {
-            const float gx = in[b] ? gxs[b] : 0.f;
-            const float gy = in[b] ? gys[b] : 0.f;
-            const float dt = in[b] ? warped[b] - fc[b] : 0.f;
-            const int slot = (ybase + b - ystart) % K;
-            float* rs = ring + ((size_t)slot * IW + c) * 3;
-            const double ogx = rs[0], ogy = rs[1], odt = rs[2];
-            rs[0] = gx;
-            rs[1] = gy;
-            rs[2] = dt;
-            const double ix = gx, iy = gy, tt = dt;
-            double* vb = vbuf + (size_t)b * NQ * IWP + cc;
-            if (FULL) {
-                V[0] = (V[0] + ix * ix) - ogx * ogx;
-                V[1] = (V[1] + ix * iy) - ogx * ogy;
-                V[2] = (V[2] + iy * iy) - ogy * ogy;
-            }
-            V[NQ - 2] = (V[NQ - 2] + ix * tt) - ogx * odt;
-            V[NQ - 1] = (V[NQ - 1] + iy * tt) - ogy * odt;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) vb[q * IWP] = V[q];
-        }
-        __syncthreads();
-        // ---- phase 2: horizontal sliding sums + 2x2 solve ----
-        for (int item = threadIdx.x; item < LK_NB * nruns; item += blockDim.x) {
-            const int b = item / nruns, run = item - b * nruns;
-            const int yo = ybase + b - r;
-            if (yo < y0 || yo >= yo_end) continue;
-            const int cs = run * LK_S;
-            const int nout = min(LK_S, a.tw - cs);
-            const double* vb = vbuf + (size_t)b * NQ * IWP;
-            double s[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) s[q] = 0.0;
-            for (int k = cs; k <= cs + 2 * r; ++k) {
-                const int ci = k + (k >> 3);
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) s[q] += vb[q * IWP + ci];
-            }
-            for (int o = 0; o < nout; ++o) {
-                if (o > 0) {
-                    const int ca = cs + 2 * r + o, cb = cs + o - 1;
-                    const int ia = ca + (ca >> 3), ib = cb + (cb >> 3);
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) s[q] = (s[q] + vb[q * IWP + ia]) - vb[q * IWP + ib];
-                }
-                const int xo = x0 + cs + o;
-                if (xo >= w) break;
-                const size_t oi = (size_t)yo * w + xo;
-                float2 f = lk_flow_at<MODE>(a, D, xo, yo);
-                if (FULL) {
-                    uint8_t ok = lk_ok_at<MODE>(a, D, xo, yo);
-                    const double A = s[0], B = s[1], Cc = s[2];
-                    float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (lk_solve(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y)) {
-                        ok = 1;
-                        const double det = A * Cc - B * B;
-                        coef = make_float4((float)(Cc / det), (float)(B / det), (float)(A / det), 1.f);
-                    }
-                    D.okout[oi] = ok;
-                    if (D.coef) D.coef[oi] = coef;
-                } else {
-                    const float4 cf = D.coef[oi];
-                    if (cf.w != 0.f) {
-                        const double bx = s[0], by = s[1];
-                        const double ux = -((double)cf.x * bx - (double)cf.y * by);
-                        const double uy = -((double)cf.z * by - (double)cf.y * bx);
-                        float ndx = f.x + (float)ux, ndy = f.y + (float)uy;
-                        final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
-                        f = make_float2(ndx, ndy);
-                    }
-                }
-                D.fout[oi] = f;
-            }
-        }
-        __syncthreads();
-    }
-}
+// K2+K3 (the fused LK iteration) lives in fs_lk.cu.
 
 // ============================================================================
 // K4 — flow smoothing (src/flow.cpp:113-130, 294-297): one or two fused 3x3
 // truncated-mean passes of dx and dy; at level 0 also the final cap and the
 // valid plane (src/flow.cpp:300-313).
 // ============================================================================
-constexpr int SM_TX = 32, SM_TY = 8;
+constexpr int SM_TX = 32, SM_TY = 16;
+__constant__ double kInvSmall[10] = {0.0,       1.0,       1.0 / 2, 1.0 / 3, 1.0 / 4,
+                                     1.0 / 5,   1.0 / 6,   1.0 / 7, 1.0 / 8, 1.0 / 9};
 
 __global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
     __shared__ float2 src[SM_TY + 4][SM_TX + 4];
@@ -396,7 +205,8 @@ __global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
                         ay += s.y;
                         ++n;
                     }
-                v = make_float2((float)(ax / n), (float)(ay / n));
+                v = make_float2(div_to_float(ax, n, kInvSmall[n]),
+                                div_to_float(ay, n, kInvSmall[n]));
             }
             p1[ly][lx] = v;
         }
@@ -416,7 +226,7 @@ __global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
             ay += s.y;
             ++n;
         }
-    float vx = (float)(ax / n), vy = (float)(ay / n);
+    float vx = div_to_float(ax, n, kInvSmall[n]), vy = div_to_float(ay, n, kInvSmall[n]);
     size_t o = (size_t)gy * w + gx;
     if (a.final_cap > 0.f) {
         final_cap(a.final_cap, vx, vy);
@@ -835,45 +645,8 @@ void downsample(const float* in0, const float* in1, float* out0, float* out1, in
     k_downsample<<<g, b, 0, s>>>(in0, in1, out0, out1, w, h, ow, oh);
 }
 
-static bool lk_configured = false;
-void init() {
-    if (lk_configured) return;
-    const int mx = 200 * 1024;
-    cudaFuncSetAttribute(k_lk_iter<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_iter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_iter<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    lk_configured = true;
-}
-// Output tile: 128 - 2r columns (one thread per input column) by th rows; th
-// shrinks on small levels so the grid still covers the SMs (a CTA's sweep is
-// a serial chain of th + 2r rows).
-int lk_tile_rows(int w, int h, int r, int ndir) {
-    const int tw = 128 - 2 * r;
-    const int cols = (w + tw - 1) / tw;
-    for (int th : {64, 32}) {
-        long ctas = (long)cols * ((h + th - 1) / th) * ndir;
-        if (ctas >= 148L * 4) return th;
-    }
-    return 16;
-}
-cudaError_t lk_iter(const LkArgs& a0, cudaStream_t s) {
-    LkArgs a = a0;
-    const int iw = 128;
-    a.tw = iw - 2 * a.r;
-    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir);
-    const bool full = a.mode != 1;
-    const size_t smem = lk_smem_bytes(iw, a.r, full ? 5 : 2);
-    init();
-    dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
-    if (a.mode == 0)
-        k_lk_iter<0, true><<<g, iw, smem, s>>>(a);
-    else if (a.mode == 1)
-        k_lk_iter<1, false><<<g, iw, smem, s>>>(a);
-    else
-        k_lk_iter<2, true><<<g, iw, smem, s>>>(a);
-    return cudaGetLastError();
-}
-int lk_max_radius() { return 48; }
+void init() { lk_init(); }
+
 
 void smooth(const SmoothArgs& a, cudaStream_t s) {
     dim3 g((a.w + SM_TX - 1) / SM_TX, (a.h + SM_TY - 1) / SM_TY, a.ndir);

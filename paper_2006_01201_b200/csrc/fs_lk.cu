@@ -1,0 +1,341 @@
+// K2+K3 — pyramidal LK iterations (src/flow.cpp:209-291), both directions.
+//
+// Per level the flow is refined by:
+//   k_lk_prep   one thread per pixel: the level's starting flow (zero at the
+//               coarsest level, else the fused 2x upsample of the coarser
+//               flow, src/flow.cpp:138-170), its ever_ok, and the temporal
+//               difference It = to(p + d) - from(p) (src/flow.cpp:248-249).
+//   k_lk_sweep  one launch per iteration: window sums + 2x2 solve + update,
+//               and, unless it is the level's last iteration, It for the next
+//               iteration at the updated flow.
+// Every gather of `to` thus happens in a per-pixel epilogue (independent
+// loads, no dependent chain), and the sweep itself streams only coalesced
+// loads.
+//
+// k_lk_sweep: a CTA owns an output tile of tw = 128 - 2r columns by th rows
+// and sweeps its th + 2r input rows, warp-specialised:
+//  producer warps 0-3 (thread c = input column x0 - r + c): per row the
+//    central-difference gradient of `from` (src/flow.cpp:225-237) and It;
+//    the exact double products enter the column's vertical running window
+//    sums in registers.  (Ix, Iy, It) of the last 2r + 1 rows live in a
+//    shared-memory ring so the row leaving the window is subtracted exactly.
+//    Every NB rows the column sums are staged into one of two buffers.
+//  consumer warps 4-7: horizontal (2r+1)-tap sums of a staged batch by
+//    sliding runs of S outputs, the solve and update, the next It — while
+//    the producers sweep the next batch.  Buffers are handed over with named
+//    barriers (bar.arrive / bar.sync).
+// FULL (a level's first iteration): five window sums, the eigenvalue test and
+// the reference's division-form update (src/flow.cpp:267-291); it also stores
+// the level-constant inverse structure tensor (c/det, b/det, a/det, ok) — the
+// structure tensor depends only on the from-level gradients, so it and the
+// eigenvalue decision are the same in every iteration of a level.  Later
+// iterations form only the two mismatch sums and update by -(M^-1 b).
+// Products are exact in double (float x float) and all window sums are double,
+// agreeing with the reference's double prefix tables to ~1e-12 relative.
+#include "fs_device.cuh"
+
+namespace fs {
+
+template <bool FULL>
+struct LkCfg {
+    static constexpr int NQ = FULL ? 5 : 2;  // window sums carried
+    static constexpr int NB = FULL ? 4 : 8;  // rows per staged batch
+    static constexpr int S = FULL ? 4 : 8;   // outputs per horizontal run
+};
+
+constexpr int LK_IW = 128;  // producer threads = input columns per CTA
+constexpr int LK_THREADS = 2 * LK_IW;
+
+__host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
+__host__ __device__ inline size_t lk_ring_bytes(int r) {
+    return ((size_t)(2 * r + 1) * LK_IW * 3 * sizeof(float) + 15) & ~size_t(15);
+}
+template <bool FULL>
+__host__ __device__ inline size_t lk_stage_doubles() {
+    return (size_t)LkCfg<FULL>::NB * LkCfg<FULL>::NQ * lk_iwp(LK_IW);
+}
+template <bool FULL>
+__host__ inline size_t lk_smem_bytes(int r) {
+    return lk_ring_bytes(r) + 2 * lk_stage_doubles<FULL>() * sizeof(double);
+}
+
+__device__ __forceinline__ void bar_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
+}
+
+// src/flow.cpp:248-249: It = sample_level(to, i + dx, j + dy) - from(i, j)
+__device__ __forceinline__ float lk_it(const float* __restrict__ T, const float* __restrict__ F,
+                                       int w, int h, int x, int y, float2 f) {
+    LevelTap t = level_tap(w, h, (double)((float)x + f.x), (double)((float)y + f.y));
+    float warped = level_combine(t, __ldg(T + (size_t)t.y0 * w + t.x0),
+                                 __ldg(T + (size_t)t.y0 * w + t.x1),
+                                 __ldg(T + (size_t)t.y1 * w + t.x0),
+                                 __ldg(T + (size_t)t.y1 * w + t.x1));
+    return warped - __ldg(F + (size_t)y * w + x);
+}
+
+// ---- per-level start: flow, ever_ok and It ---------------------------------
+template <int MODE>  // 0: zero flow (coarsest level), 2: upsample the coarser level
+__global__ void __launch_bounds__(256) k_lk_prep(LkArgs a) {
+    const LkDir& D = a.d[blockIdx.z];
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (x >= a.w || y >= a.h) return;
+    float2 f = make_float2(0.f, 0.f);
+    uint8_t ok = 0;
+    if (MODE == 2) {
+        UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
+        float2 f00 = D.fin[(size_t)t.y0 * a.cw + t.x0], f10 = D.fin[(size_t)t.y0 * a.cw + t.x1];
+        float2 f01 = D.fin[(size_t)t.y1 * a.cw + t.x0], f11 = D.fin[(size_t)t.y1 * a.cw + t.x1];
+        f = make_float2(up_combine(t, f00.x, f10.x, f01.x, f11.x),
+                        up_combine(t, f00.y, f10.y, f01.y, f11.y));
+        ok = D.okin[(size_t)t.yn * a.cw + t.xn];
+    }
+    const size_t o = (size_t)y * a.w + x;
+    D.fout[o] = f;
+    D.okout[o] = ok;
+    D.dtout[o] = lk_it(D.T, D.F, a.w, a.h, x, y, f);
+}
+
+// ---- producer: sweep rows, stage vertical window sums ----------------------
+template <bool FULL>
+__device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, float* ring,
+                                           double* stage, int x0, int ystart, int yend, int nbat) {
+    using Cfg = LkCfg<FULL>;
+    constexpr int NB = Cfg::NB, NQ = Cfg::NQ;
+    const int r = a.r, K = 2 * r + 1, w = a.w, h = a.h;
+    const int IWP = lk_iwp(LK_IW);
+    const int c = threadIdx.x;
+    const int x = x0 - r + c;
+    const bool xin = x >= 0 && x < w;
+    const int xc = clampi(x, 0, w - 1);
+    const int xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
+    const int cc = c + (c >> 3);
+    for (int k = 0; k < K; ++k) {
+        float* rs = ring + ((size_t)k * LK_IW + c) * 3;
+        rs[0] = 0.f;
+        rs[1] = 0.f;
+        rs[2] = 0.f;
+    }
+    double V[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) V[q] = 0.0;
+    for (int i = 0; i < nbat; ++i) {
+        const int buf = i & 1;
+        const int ybase = ystart + i * NB;
+        float gxs[NB], gys[NB], dts[NB];
+        bool in[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {  // coalesced, independent loads of the batch
+            const int y = ybase + b;
+            in[b] = xin && y >= 0 && y < h && y < yend;
+            const int yy = clampi(y, 0, h - 1);
+            const float* Frow = D.F + (size_t)yy * w;
+            gxs[b] = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));  // src/flow.cpp:230-235
+            gys[b] = 0.5f * (__ldg(D.F + (size_t)min(yy + 1, h - 1) * w + xc) -
+                             __ldg(D.F + (size_t)max(yy - 1, 0) * w + xc));
+            dts[b] = __ldg(D.dtin + (size_t)yy * w + xc);
+        }
+        if (i >= 2) bar_sync(3 + buf);  // consumers released this buffer
+        double* st = stage + (size_t)buf * lk_stage_doubles<FULL>();
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const float gx = in[b] ? gxs[b] : 0.f;
+            const float gy = in[b] ? gys[b] : 0.f;
+            const float dt = in[b] ? dts[b] : 0.f;
+            const int slot = (ybase + b - ystart) % K;
+            float* rs = ring + ((size_t)slot * LK_IW + c) * 3;
+            const double ogx = rs[0], ogy = rs[1], odt = rs[2];
+            rs[0] = gx;
+            rs[1] = gy;
+            rs[2] = dt;
+            const double ix = gx, iy = gy, tt = dt;
+            if (FULL) {
+                V[0] = (V[0] + ix * ix) - ogx * ogx;
+                V[1] = (V[1] + ix * iy) - ogx * ogy;
+                V[2] = (V[2] + iy * iy) - ogy * ogy;
+            }
+            V[NQ - 2] = (V[NQ - 2] + ix * tt) - ogx * odt;
+            V[NQ - 1] = (V[NQ - 1] + iy * tt) - ogy * odt;
+            double* vb = st + (size_t)b * NQ * IWP + cc;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) vb[q * IWP] = V[q];
+        }
+        bar_arrive(1 + buf);  // batch staged
+    }
+}
+
+// ---- consumer: horizontal sums, solve, update, next It ---------------------
+template <bool FULL>
+__device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, const double* stage,
+                                           int x0, int y0, int ystart, int yo_end, int nbat) {
+    using Cfg = LkCfg<FULL>;
+    constexpr int NB = Cfg::NB, NQ = Cfg::NQ, S = Cfg::S;
+    const int r = a.r, w = a.w, h = a.h;
+    const int IWP = lk_iwp(LK_IW);
+    const int nruns = (a.tw + S - 1) / S;
+    const int t = threadIdx.x - LK_IW;
+    const int b = t / nruns, run = t - b * nruns;  // NB * nruns <= 128 by construction
+    const int cs = run * S;
+    for (int i = 0; i < nbat; ++i) {
+        const int buf = i & 1;
+        const int yo = ystart + i * NB + b - r;
+        const bool active = t < NB * nruns && yo >= y0 && yo < yo_end && x0 + cs < w;
+        const int nout = active ? min(min(S, a.tw - cs), w - (x0 + cs)) : 0;
+        // prefetch the run's own flow / ok / coefficients before waiting
+        float2 fo[S];
+        float4 cf[S];
+        uint8_t okv[S];
+        if (active) {
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                const size_t oi = (size_t)yo * w + min(x0 + cs + o, w - 1);
+                fo[o] = D.fin[oi];
+                if (FULL)
+                    okv[o] = D.okin[oi];
+                else
+                    cf[o] = D.coef[oi];
+            }
+        }
+        bar_sync(1 + buf);
+        if (active) {
+            const double* vb =
+                stage + (size_t)buf * lk_stage_doubles<FULL>() + (size_t)b * NQ * IWP;
+            double s[NQ], s2[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) s[q] = s2[q] = 0.0;
+            int k = cs;
+            for (; k + 1 <= cs + 2 * r; k += 2) {  // two accumulators, no single chain
+                const int ci = k + (k >> 3), cj = (k + 1) + ((k + 1) >> 3);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    s[q] += vb[q * IWP + ci];
+                    s2[q] += vb[q * IWP + cj];
+                }
+            }
+            if (k <= cs + 2 * r) {
+                const int ci = k + (k >> 3);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) s[q] += vb[q * IWP + ci];
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) s[q] += s2[q];
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                if (o >= nout) break;
+                if (o > 0) {
+                    const int ca = cs + 2 * r + o, cb = cs + o - 1;
+                    const int ia = ca + (ca >> 3), ib = cb + (cb >> 3);
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        s[q] = (s[q] + vb[q * IWP + ia]) - vb[q * IWP + ib];
+                }
+                const size_t oi = (size_t)yo * w + (x0 + cs + o);
+                float2 f = fo[o];
+                if (FULL) {
+                    uint8_t ok = okv[o];
+                    const double A = s[0], B = s[1], Cc = s[2];
+                    float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (lk_solve(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y)) {
+                        ok = 1;
+                        const double inv_det = 1.0 / (A * Cc - B * B);
+                        coef = make_float4((float)(Cc * inv_det), (float)(B * inv_det),
+                                           (float)(A * inv_det), 1.f);
+                    }
+                    D.okout[oi] = ok;
+                    if (D.coef) D.coef[oi] = coef;
+                } else if (cf[o].w != 0.f) {
+                    const double bx = s[0], by = s[1];
+                    const double ux = -((double)cf[o].x * bx - (double)cf[o].y * by);
+                    const double uy = -((double)cf[o].z * by - (double)cf[o].y * bx);
+                    float ndx = f.x + (float)ux, ndy = f.y + (float)uy;
+                    final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
+                    f = make_float2(ndx, ndy);
+                }
+                fo[o] = f;
+                D.fout[oi] = f;
+            }
+            if (D.dtout) {  // It of the next iteration at the updated flow
+#pragma unroll
+                for (int o = 0; o < S; ++o) {
+                    if (o >= nout) break;
+                    const int xo = x0 + cs + o;
+                    D.dtout[(size_t)yo * w + xo] = lk_it(D.T, D.F, w, h, xo, yo, fo[o]);
+                }
+            }
+        }
+        if (i + 2 < nbat) bar_arrive(3 + buf);  // buffer free for batch i + 2
+    }
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(LK_THREADS, 2) k_lk_sweep(LkArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);
+    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes(a.r));
+    const LkDir& D = a.d[blockIdx.z];
+    const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
+    const int yo_end = min(y0 + a.th, a.h);
+    const int ystart = y0 - a.r;
+    const int yend = yo_end + a.r;
+    const int nbat = (yend - ystart + LkCfg<FULL>::NB - 1) / LkCfg<FULL>::NB;
+    if (threadIdx.x < LK_IW)
+        lk_produce<FULL>(a, D, ring, stage, x0, ystart, yend, nbat);
+    else
+        lk_consume<FULL>(a, D, stage, x0, y0, ystart, yo_end, nbat);
+}
+
+namespace launch {
+
+static bool lk_configured = false;
+void lk_init() {
+    if (lk_configured) return;
+    const int mx = 200 * 1024;
+    cudaFuncSetAttribute(k_lk_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    lk_configured = true;
+}
+
+// th shrinks on small levels so the grid still covers the SMs (a CTA's sweep
+// is a serial chain of th + 2r rows).
+int lk_tile_rows(int w, int h, int r, int ndir) {
+    const int tw = LK_IW - 2 * r;
+    const int cols = (w + tw - 1) / tw;
+    for (int th : {64, 32}) {
+        long ctas = (long)cols * ((h + th - 1) / th) * ndir;
+        if (ctas >= 148L * 3) return th;
+    }
+    return 16;
+}
+
+cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
+    dim3 g((a.w + 31) / 32, (a.h + 7) / 8, a.ndir);
+    if (a.mode == 2)
+        k_lk_prep<2><<<g, 256, 0, s>>>(a);
+    else
+        k_lk_prep<0><<<g, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t lk_sweep(const LkArgs& a0, bool full, cudaStream_t s) {
+    LkArgs a = a0;
+    a.tw = LK_IW - 2 * a.r;
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir);
+    lk_init();
+    dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
+    if (full)
+        k_lk_sweep<true><<<g, LK_THREADS, lk_smem_bytes<true>(a.r), s>>>(a);
+    else
+        k_lk_sweep<false><<<g, LK_THREADS, lk_smem_bytes<false>(a.r), s>>>(a);
+    return cudaGetLastError();
+}
+
+// NB * nruns must fit the 128 consumer threads: tw = 128 - 2r, runs of 4
+// (FULL, NB = 4) or 8 (NB = 8) => any r <= 48 keeps tw >= 32.
+int lk_max_radius() { return 48; }
+
+}  // namespace launch
+}  // namespace fs

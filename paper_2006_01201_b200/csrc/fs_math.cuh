@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #ifdef __CUDACC__
 #define FS_HD __host__ __device__ __forceinline__
@@ -101,6 +102,27 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
     dx = ndx;
     dy = ndy;
     return true;
+}
+
+// (float)(acc / n) for a small positive integer n, as the reference rounds it
+// (double division, then float conversion), without a double division in
+// the common case: q = acc * (1/n) is within 1 ulp of the correctly rounded
+// quotient, so both convert to the same float unless q sits within a few ulp
+// of a float rounding boundary (the midpoint between two floats, low 29
+// mantissa bits == 2^28) — only then is the exact division taken.
+FS_HD float div_to_float(double acc, int n, double inv_n) {
+    double q = acc * inv_n;
+#ifdef __CUDA_ARCH__
+    long long bits = __double_as_longlong(q);
+#else
+    long long bits;
+    memcpy(&bits, &q, sizeof bits);
+#endif
+    long long low = bits & ((1LL << 29) - 1);
+    long long dist = low - (1LL << 28);
+    if (dist < 0) dist = -dist;
+    if (dist <= 8) q = acc / n;
+    return static_cast<float>(q);
 }
 
 // src/flow.cpp:300-311 — final magnitude cap.
