@@ -136,7 +136,7 @@ void full_edt(Stage& st, const M& m0, const M* m1, int w, int h, int* out0, int*
         j[q].out = outs[q];
     }
     if (!m1) j[1].active = 0;
-    launch::edt(j[0], j[1], nullptr, nullptr, st.s);
+    launch::edt(j[0], j[1], nullptr, st.s);
     FS_CK(cudaGetLastError());
 }
 
@@ -571,8 +571,10 @@ fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* con
             FoldWS<ViewF4> f;
             FoldStats* fst = st.tmp<FoldStats>(1);
             f.st = fst;
+            const PanoPlane pano{cv.valid, cv.rgb, cv.w};
             init_stats(fst, st.s);
-            if (v.rect.w > 0 && v.rect.h > 0) launch::partition(cv, v, fst, st.s);
+            if (v.rect.w > 0 && v.rect.h > 0) launch::partition(pano, v, fst, st.s);
+            launch::snapshot_count(fst, cc, st.s);
             FoldStats hs;
             st.read(&hs, fst, 1);
             if (hs.cnt3 == 0)
@@ -585,13 +587,13 @@ fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* con
             a1.base = static_cast<char*>(st.alloc(a0.off));
             f.layout(a1, box, pb, v.rect, *flow);
             FS_CK(cudaMemcpyAsync(f.st, fst, sizeof(FoldStats), cudaMemcpyDeviceToDevice, st.s));
-            fold_enqueue_flow_edt(f, cv, v, cc, *flow, st.s, ev[0], ev[1]);
+            fold_enqueue_flow_edt(f, pano, pano, v, ch, *flow, st.s, ev[0], ev[1]);
             FoldStats hs2;
             st.read(&hs2, f.st, 1);
             if (hs2.edt_fail) {  // bounded domain not provably exact: redo on the full domain
                 f.full_domain = true;
                 f.replan_edt();
-                fold_enqueue_flow_edt(f, cv, v, cc, *flow, st.s, ev[0], ev[1]);
+                fold_enqueue_flow_edt(f, pano, pano, v, ch, *flow, st.s, ev[0], ev[1]);
             }
             FS_CK(cudaEventRecord(ev[2], st.s));
             fold_enqueue_blend(f, cv, v, cc, *blend, st.s);

@@ -58,8 +58,44 @@ struct ViewF4 {
     }
 };
 
+// Validity (and value) of the panorama before a fold, read from the canvas.
+struct PanoPlane {
+    const uint8_t* valid;
+    const float4* rgb;
+    int w;
+    __device__ __forceinline__ bool valid_at(int x, int y) const {
+        return valid[(size_t)y * w + x] != 0;
+    }
+    __device__ __forceinline__ float4 value_at(int x, int y) const {
+        return rgb[(size_t)y * w + x];
+    }
+};
+
+// The same, derived from the views folded so far: the panorama's validity is
+// the union of their masks (src/pipeline.cpp:201-204), and a pixel that no
+// earlier fold blended holds the value of the first view that covered it
+// (Area2 copies R, src/blender.cpp:69-71).  Lets a fold's partition, distance
+// transforms and (when its Area3 box is disjoint from every earlier one) its
+// L crop run without waiting for the earlier folds.
+constexpr int kMaxDagViews = 16;
+struct PanoViews {
+    int n;
+    ViewU8 v[kMaxDagViews];
+    __device__ __forceinline__ bool valid_at(int x, int y) const {
+        for (int m = 0; m < n; ++m)
+            if (v[m].valid_at(x, y)) return true;
+        return false;
+    }
+    __device__ __forceinline__ float4 value_at(int x, int y) const {
+        for (int m = 0; m < n; ++m)
+            if (v[m].valid_at(x, y)) return v[m].value_at(x, y);
+        return make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+};
+
 // Per-fold device bookkeeping (written by the partition kernel).
 struct FoldStats {
+    unsigned long long pv_count;  // |pano valid| before this fold (Area1 + Area3)
     unsigned long long cnt2;  // Area2 pixels
     unsigned long long cnt3;  // Area3 pixels
     int bx0, by0, bx1, by1;   // Area3 bbox (inclusive max), init (INT_MAX, INT_MAX, -1, -1)
@@ -109,14 +145,13 @@ struct SmoothArgs {
 // ---- distance transform ----
 // Seed masks of the fold: Area1 = pano valid && !view valid, Area2 = view
 // valid && !pano valid (src/blend_field.cpp:100-104 on src/image.cpp:115-132).
-template <class V>
+template <class V, class P>
 struct FoldMask {
-    const uint8_t* pvalid;
-    int cw;
+    P pano;
     V view;
     int which;  // 1 or 2
     __device__ __forceinline__ bool operator()(int x, int y) const {
-        bool pv = pvalid[(size_t)y * cw + x] != 0;
+        bool pv = pano.valid_at(x, y);
         bool rv = view.valid_at(x, y);
         return which == 1 ? (pv && !rv) : (rv && !pv);
     }
@@ -160,10 +195,13 @@ void init();     // one-time kernel attributes (call before any graph capture)
 void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
-template <class V> void partition(const Canvas&, const V&, FoldStats*, cudaStream_t);
+template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
+// pv_count of fold k = |view 0 valid| + sum of the Area2 counts of folds < k
+void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cudaStream_t);
+void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
 void check_box(FoldStats*, const Rect&, cudaStream_t);
-template <class V>
-void crop_gray(const Canvas&, const V&, const Rect&, float*, float*, cudaStream_t);
+template <class V, class P>
+void crop_gray(const P&, const V&, const Rect&, int ch, float*, float*, cudaStream_t);
 void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
                 int nimg, cudaStream_t);
 cudaError_t lk_prep(const LkArgs&, cudaStream_t);              // mode 0 or 2
@@ -172,11 +210,10 @@ int lk_max_radius();
 void smooth(const SmoothArgs&, cudaStream_t);
 void finalize_flow(const SmoothArgs&, cudaStream_t);
 template <class M>
-void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, const CanvasCount*, cudaStream_t);
+void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, cudaStream_t);
 template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
-                 const int*, const FoldStats*, const CanvasCount*, double, double, float4*,
-                 cudaStream_t);
+                 const int*, const FoldStats*, double, double, float4*, cudaStream_t);
 template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);

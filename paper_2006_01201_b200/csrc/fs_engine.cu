@@ -344,18 +344,18 @@ __global__ void k_init_count(CanvasCount* cc) { cc->valid_count = 0; }
 void init_stats(FoldStats* st, cudaStream_t s) { k_init_stats<<<1, 1, 0, s>>>(st); }
 void init_count(CanvasCount* cc, cudaStream_t s) { k_init_count<<<1, 1, 0, s>>>(cc); }
 
-template <class V>
-int fold_enqueue_pre(FoldWS<V>& f, const Canvas& cv, const V& view, cudaStream_t s) {
+template <class V, class P>
+int fold_enqueue_pre(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s) {
     init_stats(f.st, s);
     {
         ProfScope ps("partition", 5.0 * view.rect.area(), s);  // view 4 B + pano valid 1 B
-        launch::partition(cv, view, f.st, s);
+        launch::partition(pano, view, f.st, s);
     }
     return 2;
 }
 
-template <class V>
-int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+template <class V, class P, class PC>
+int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1) {
     int launches = 0;
@@ -363,37 +363,37 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasC
     {
         // pano rgb 16 + valid 1 + view 4 in, two gray planes 8 out
         ProfScope ps("crop_gray", 29.0 * f.box.area(), s);
-        launch::crop_gray(cv, view, f.box, f.gray[0], f.gray[1], s);
+        launch::crop_gray(crop_src, view, f.box, ch, f.gray[0], f.gray[1], s);
     }
     launches += 2;
     if (ev_flow0) FS_CK(cudaEventRecord(ev_flow0, s));
     launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s);
     if (ev_flow1) FS_CK(cudaEventRecord(ev_flow1, s));
-    EdtJob<FoldMask<V>> j[2];
+    EdtJob<FoldMask<V, P>> j[2];
     for (int m = 0; m < 2; ++m) {
-        const EdtPlan& P = f.ep[m];
-        j[m].mask = FoldMask<V>{cv.valid, cv.w, view, m + 1};
+        const EdtPlan& E = f.ep[m];
+        j[m].mask = FoldMask<V, P>{pano, view, m + 1};
         j[m].which = m + 1;
         j[m].active = 1;
-        j[m].W = P.W;
-        j[m].C = P.C;
-        j[m].vfirst = P.vfirst;
+        j[m].W = E.W;
+        j[m].C = E.C;
+        j[m].vfirst = E.vfirst;
         j[m].g = f.edt[m].g;
         j[m].bits = f.edt[m].bits;
         j[m].stack = f.edt[m].stack;
         j[m].out = f.edt[m].out;
-        j[m].e_left = P.e_left;
-        j[m].e_right = P.e_right;
-        j[m].e_top = P.e_top;
-        j[m].e_bottom = P.e_bottom;
-        j[m].check = P.check;
+        j[m].e_left = E.e_left;
+        j[m].e_right = E.e_right;
+        j[m].e_top = E.e_top;
+        j[m].e_bottom = E.e_bottom;
+        j[m].check = E.check;
     }
     {
         // per mask: the seed mask over the domain (pano valid 1 + view 4) + d^2 out on C
         double bytes = 0;
         for (int m = 0; m < 2; ++m) bytes += 5.0 * f.ep[m].W.area() + 4.0 * f.box.area();
         ProfScope ps("edt", bytes, s);
-        launch::edt(j[0], j[1], f.st, cc, s);
+        launch::edt(j[0], j[1], f.st, s);
     }
     launches += 3;
     FS_CK(cudaGetLastError());
@@ -408,7 +408,7 @@ int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCoun
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
         ProfScope ps("blend", 61.0 * f.box.area(), s);
         launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
-                            f.st, cc, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
+                            f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
     }
     {
         // view 4 + pano valid 1 in, rgb 16 + valid 1 out on the view; blended 16 in on Area3
@@ -422,14 +422,24 @@ int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCoun
 
 template struct FoldWS<ViewU8>;
 template struct FoldWS<ViewF4>;
-template int fold_enqueue_pre<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&, cudaStream_t);
-template int fold_enqueue_pre<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&, cudaStream_t);
-template int fold_enqueue_flow_edt<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
-                                           CanvasCount*, const fs_flow_params&, cudaStream_t,
-                                           cudaEvent_t, cudaEvent_t);
-template int fold_enqueue_flow_edt<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
-                                           CanvasCount*, const fs_flow_params&, cudaStream_t,
-                                           cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_pre<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoViews&, const ViewU8&,
+                                                 cudaStream_t);
+template int fold_enqueue_pre<ViewU8, PanoPlane>(FoldWS<ViewU8>&, const PanoPlane&, const ViewU8&,
+                                                 cudaStream_t);
+template int fold_enqueue_pre<ViewF4, PanoPlane>(FoldWS<ViewF4>&, const PanoPlane&, const ViewF4&,
+                                                 cudaStream_t);
+template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoViews>(
+    FoldWS<ViewU8>&, const PanoViews&, const PanoViews&, const ViewU8&, int,
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoPlane>(
+    FoldWS<ViewU8>&, const PanoViews&, const PanoPlane&, const ViewU8&, int,
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_flow_edt<ViewU8, PanoPlane, PanoPlane>(
+    FoldWS<ViewU8>&, const PanoPlane&, const PanoPlane&, const ViewU8&, int,
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+template int fold_enqueue_flow_edt<ViewF4, PanoPlane, PanoPlane>(
+    FoldWS<ViewF4>&, const PanoPlane&, const PanoPlane&, const ViewF4&, int,
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t);
 template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,

@@ -115,11 +115,13 @@ struct FoldWS {
                 const fs_flow_params& fp);
     void replan_edt();
 };
-template <class V>
-int fold_enqueue_pre(FoldWS<V>& f, const Canvas& cv, const V& view, cudaStream_t s);
-// check box, crop+gray, pyramid, flow (both directions), distance transforms
-template <class V>
-int fold_enqueue_flow_edt(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
+// init the fold's statistics + partition (P: the pano's validity before the fold)
+template <class V, class P>
+int fold_enqueue_pre(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
+// check box, crop+gray (L from crop_src), pyramid, flow (both directions),
+// distance transforms (seed masks from `pano`'s validity)
+template <class V, class P, class PC>
+int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1);
 // Code 1 blend on Area3 + composition of the view onto the canvas

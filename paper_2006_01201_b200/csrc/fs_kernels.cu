@@ -49,9 +49,8 @@ __global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCou
 
 // src/image.cpp:115-132 + :140-148, restricted to the view rectangle (Area2 and
 // Area3 live there): Area2/Area3 counts and the Area3 bounding box.
-template <class V>
-__global__ void __launch_bounds__(256) k_partition(const uint8_t* __restrict__ pvalid, int cw,
-                                                   V view, FoldStats* st) {
+template <class V, class P>
+__global__ void __launch_bounds__(256) k_partition(P pano, V view, FoldStats* st) {
     __shared__ int red[5][8];
     const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
@@ -60,7 +59,7 @@ __global__ void __launch_bounds__(256) k_partition(const uint8_t* __restrict__ p
     if (x < view.rect.x1())
         for (int y = ya; y < yb; ++y) {
             if (!view.valid_at(x, y)) continue;
-            if (pvalid[(size_t)y * cw + x]) {
+            if (pano.valid_at(x, y)) {
                 ++n3;
                 minx = min(minx, x);
                 maxx = max(maxx, x);
@@ -115,21 +114,36 @@ __global__ void k_check_box(FoldStats* st, Rect planned) {
     if (!ok) st->box_mismatch = 1;
 }
 
+// |pano valid| before each fold: view 0's count plus the Area2 pixels every
+// earlier fold added (the union of the masks, src/pipeline.cpp:201-204).
+struct FoldStatsPtrs {
+    FoldStats* p[64];
+};
+__global__ void k_prefix_counts(FoldStatsPtrs st, int n, const CanvasCount* cc) {
+    unsigned long long c = cc->valid_count;
+    for (int k = 0; k < n; ++k) {
+        st.p[k]->pv_count = c;
+        c += st.p[k]->cnt2;
+    }
+}
+__global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
+    st->pv_count = cc->valid_count;
+}
+
 // src/image.cpp:134-162 then src/image.cpp:70-83: crop of both sides over the
 // Area3 box (invalid pixels zeroed) and their gray levels.
-template <class V>
-__global__ void k_crop_gray(Canvas cv, V view, Rect box, float* __restrict__ gl,
+template <class V, class P>
+__global__ void k_crop_gray(P pano, V view, Rect box, int ch, float* __restrict__ gl,
                             float* __restrict__ gr) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
     int x = box.x0 + i, y = box.y0 + j;
-    size_t p = (size_t)y * cv.w + x;
-    float4 l = cv.valid[p] ? cv.rgb[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 l = pano.valid_at(x, y) ? pano.value_at(x, y) : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 r = view.valid_at(x, y) ? view.value_at(x, y) : make_float4(0.f, 0.f, 0.f, 0.f);
     size_t o = (size_t)j * box.w + i;
-    gl[o] = cv.ch == 3 ? gray3(l.x, l.y, l.z) : l.x;
-    gr[o] = cv.ch == 3 ? gray3(r.x, r.y, r.z) : r.x;
+    gl[o] = ch == 3 ? gray3(l.x, l.y, l.z) : l.x;
+    gr[o] = ch == 3 ? gray3(r.x, r.y, r.z) : r.x;
 }
 
 // ============================================================================
@@ -362,8 +376,7 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
 // comparisons (Felzenszwalb, src/blend_field.cpp:19-47), then every lane
 // evaluates its outputs by binary search over the envelope's breakpoints.
 template <class M>
-__global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
-                               const CanvasCount* cc) {
+__global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st) {
     const EdtJob<M>& J = blockIdx.z == 0 ? J0 : J1;
     if (!J.active) return;
     const int nout_lines = J.vfirst ? J.C.h : J.C.w;
@@ -424,7 +437,7 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st,
     }
     ne = __shfl_sync(0xffffffffu, ne, 0);
     __syncwarp();
-    const bool have = J.which == 1   ? (cc->valid_count - st->cnt3) > 0
+    const bool have = J.which == 1   ? (st->pv_count - st->cnt3) > 0
                       : J.which == 2 ? st->cnt2 > 0
                                      : true;
     bool fail = false;
@@ -518,16 +531,15 @@ struct CanvasSampler {
 template <class V>
 __global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
-                              const int* __restrict__ d2, const FoldStats* st,
-                              const CanvasCount* cc, double k, double coef,
-                              float4* __restrict__ out) {
+                              const int* __restrict__ d2, const FoldStats* st, double k,
+                              double coef, float4* __restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
     int x = box.x0 + i, y = box.y0 + j;
     size_t p = (size_t)y * cv.w + x;
     if (!(cv.valid[p] && view.valid_at(x, y))) return;  // not Area3
-    const bool have1 = (cc->valid_count - st->cnt3) > 0, have2 = st->cnt2 > 0;
+    const bool have1 = (st->pv_count - st->cnt3) > 0, have2 = st->cnt2 > 0;
     size_t o = (size_t)j * box.w + i;
     double blend_r = eq1_area3(have1, have2, d1[o], d2[o]);
     double blend_l = 1.0 - blend_r;
@@ -625,18 +637,26 @@ void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_
     k_place_view<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
         cv, view, count);
 }
-template <class V>
-void partition(const Canvas& cv, const V& view, FoldStats* st, cudaStream_t s) {
+template <class V, class P>
+void partition(const P& pano, const V& view, FoldStats* st, cudaStream_t s) {
     k_partition<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
-        cv.valid, cv.w, view, st);
+        pano, view, st);
+}
+void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cudaStream_t s) {
+    FoldStatsPtrs p{};
+    for (int k = 0; k < nfolds && k < 64; ++k) p.p[k] = st[k];
+    k_prefix_counts<<<1, 1, 0, s>>>(p, nfolds < 64 ? nfolds : 64, cc);
+}
+void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t s) {
+    k_snapshot_count<<<1, 1, 0, s>>>(st, cc);
 }
 void check_box(FoldStats* st, const Rect& planned, cudaStream_t s) {
     k_check_box<<<1, 1, 0, s>>>(st, planned);
 }
-template <class V>
-void crop_gray(const Canvas& cv, const V& view, const Rect& box, float* gl, float* gr,
+template <class V, class P>
+void crop_gray(const P& pano, const V& view, const Rect& box, int ch, float* gl, float* gr,
                cudaStream_t s) {
-    k_crop_gray<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, gl, gr);
+    k_crop_gray<<<row_grid(box.w, box.h), 256, 0, s>>>(pano, view, box, ch, gl, gr);
 }
 void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
                 int nimg, cudaStream_t s) {
@@ -646,7 +666,6 @@ void downsample(const float* in0, const float* in1, float* out0, float* out1, in
 }
 
 void init() { lk_init(); }
-
 
 void smooth(const SmoothArgs& a, cudaStream_t s) {
     dim3 g((a.w + SM_TX - 1) / SM_TX, (a.h + SM_TY - 1) / SM_TY, a.ndir);
@@ -658,8 +677,7 @@ void finalize_flow(const SmoothArgs& a, cudaStream_t s) {
 }
 
 template <class M>
-void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, const CanvasCount* cc,
-         cudaStream_t s) {
+void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, cudaStream_t s) {
     const EdtJob<M>* js[2] = {&j0, &j1};
     int max_lines = 0, max_seg = 0, max_oseg = 0, max_out = 0;
     for (auto* j : js) {
@@ -676,23 +694,22 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, const Ca
         max_out = max(max_out, j->vfirst ? j->C.h : j->C.w);
     }
     if (max_lines == 0) return;
-    if (j0.vfirst == j1.vfirst || !j1.active || !j0.active) {
-        const bool vf = j0.active ? j0.vfirst : j1.vfirst;
-        if (vf)
-            k_edt_bits<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
-        else
-            k_edt_bits<M><<<dim3((max_lines + 7) / 8, max_seg, 2), 256, 0, s>>>(j0, j1);
-    }
+    // both jobs of a fold share the output box, hence the pass order
+    const bool vf = j0.active ? j0.vfirst : j1.vfirst;
+    if (vf)
+        k_edt_bits<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
+    else
+        k_edt_bits<M><<<dim3((max_lines + 7) / 8, max_seg, 2), 256, 0, s>>>(j0, j1);
     k_edt_line<M><<<dim3((max_lines + 127) / 128, max_oseg, 2), 128, 0, s>>>(j0, j1);
-    k_edt_envelope<M><<<dim3((max_out + 7) / 8, 1, 2), 256, 0, s>>>(j0, j1, st, cc);
+    k_edt_envelope<M><<<dim3((max_out + 7) / 8, 1, 2), 256, 0, s>>>(j0, j1, st);
 }
 
 template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
-                 const float2* frl, const int* d1, const int* d2, const FoldStats* st,
-                 const CanvasCount* cc, double k, double coef, float4* out, cudaStream_t s) {
+                 const float2* frl, const int* d1, const int* d2, const FoldStats* st, double k,
+                 double coef, float4* out, cudaStream_t s) {
     k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(cv, view, box, flr, frl, d1, d2, st,
-                                                             cc, k, coef, out);
+                                                             k, coef, out);
 }
 template <class V>
 void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -704,7 +721,6 @@ template <class V>
 void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
-template void union_valid<ViewU8>(const Canvas&, const ViewU8&, cudaStream_t);
 void quantize(const Canvas& cv, uchar4* out, cudaStream_t s) {
     k_quantize<<<row_grid(cv.w, cv.h), 256, 0, s>>>(cv, out);
 }
@@ -713,30 +729,40 @@ void export_float(const Canvas& cv, float* out, uint8_t* vout, cudaStream_t s) {
 }
 
 // explicit instantiations
+template void union_valid<ViewU8>(const Canvas&, const ViewU8&, cudaStream_t);
 template void place_view<ViewU8>(const Canvas&, const ViewU8&, CanvasCount*, cudaStream_t);
 template void place_view<ViewF4>(const Canvas&, const ViewF4&, CanvasCount*, cudaStream_t);
-template void partition<ViewU8>(const Canvas&, const ViewU8&, FoldStats*, cudaStream_t);
-template void partition<ViewF4>(const Canvas&, const ViewF4&, FoldStats*, cudaStream_t);
-template void crop_gray<ViewU8>(const Canvas&, const ViewU8&, const Rect&, float*, float*,
-                                cudaStream_t);
-template void crop_gray<ViewF4>(const Canvas&, const ViewF4&, const Rect&, float*, float*,
-                                cudaStream_t);
-template void edt<FoldMask<ViewU8>>(const EdtJob<FoldMask<ViewU8>>&,
-                                    const EdtJob<FoldMask<ViewU8>>&, const FoldStats*,
-                                    const CanvasCount*, cudaStream_t);
-template void edt<FoldMask<ViewF4>>(const EdtJob<FoldMask<ViewF4>>&,
-                                    const EdtJob<FoldMask<ViewF4>>&, const FoldStats*,
-                                    const CanvasCount*, cudaStream_t);
+template void partition<ViewU8, PanoPlane>(const PanoPlane&, const ViewU8&, FoldStats*,
+                                           cudaStream_t);
+template void partition<ViewU8, PanoViews>(const PanoViews&, const ViewU8&, FoldStats*,
+                                           cudaStream_t);
+template void partition<ViewF4, PanoPlane>(const PanoPlane&, const ViewF4&, FoldStats*,
+                                           cudaStream_t);
+template void crop_gray<ViewU8, PanoPlane>(const PanoPlane&, const ViewU8&, const Rect&, int,
+                                           float*, float*, cudaStream_t);
+template void crop_gray<ViewU8, PanoViews>(const PanoViews&, const ViewU8&, const Rect&, int,
+                                           float*, float*, cudaStream_t);
+template void crop_gray<ViewF4, PanoPlane>(const PanoPlane&, const ViewF4&, const Rect&, int,
+                                           float*, float*, cudaStream_t);
+template void edt<FoldMask<ViewU8, PanoViews>>(const EdtJob<FoldMask<ViewU8, PanoViews>>&,
+                                               const EdtJob<FoldMask<ViewU8, PanoViews>>&,
+                                               const FoldStats*, cudaStream_t);
+template void edt<FoldMask<ViewU8, PanoPlane>>(const EdtJob<FoldMask<ViewU8, PanoPlane>>&,
+                                               const EdtJob<FoldMask<ViewU8, PanoPlane>>&,
+                                               const FoldStats*, cudaStream_t);
+template void edt<FoldMask<ViewF4, PanoPlane>>(const EdtJob<FoldMask<ViewF4, PanoPlane>>&,
+                                               const EdtJob<FoldMask<ViewF4, PanoPlane>>&,
+                                               const FoldStats*, cudaStream_t);
 template void edt<PlaneMask>(const EdtJob<PlaneMask>&, const EdtJob<PlaneMask>&,
-                             const FoldStats*, const CanvasCount*, cudaStream_t);
+                             const FoldStats*, cudaStream_t);
 template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
-                             const FoldStats*, const CanvasCount*, cudaStream_t);
+                             const FoldStats*, cudaStream_t);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
-                                  const float2*, const int*, const int*, const FoldStats*,
-                                  const CanvasCount*, double, double, float4*, cudaStream_t);
+                                  const float2*, const int*, const int*, const FoldStats*, double,
+                                  double, float4*, cudaStream_t);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
-                                  const float2*, const int*, const int*, const FoldStats*,
-                                  const CanvasCount*, double, double, float4*, cudaStream_t);
+                                  const float2*, const int*, const int*, const FoldStats*, double,
+                                  double, float4*, cudaStream_t);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

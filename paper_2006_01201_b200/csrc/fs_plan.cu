@@ -32,6 +32,14 @@ struct fs_plan_s {
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
     std::string err;
+    // DAG schedule (n <= kMaxDagViews): per-fold branch streams for the
+    // partition-independent work, an ordered blend/compose chain on the main
+    // stream; crop_from_views[k]: fold k's L crop can be read from the views.
+    bool dag = false;
+    std::vector<cudaStream_t> branch;
+    std::vector<cudaEvent_t> ev_branch, ev_compose;
+    cudaEvent_t ev_pro = nullptr;
+    std::vector<char> crop_from_views;
 };
 
 namespace {
@@ -61,9 +69,20 @@ Rect rect_inter(const Rect& a, const Rect& b) {
 
 ViewU8 view_of(const fs_plan_s* p, int k) { return ViewU8{p->views[k], p->rects[k]}; }
 
-// Enqueue one full execution on stream s (captured into the graph).
-int enqueue_all(fs_plan_s* p, cudaStream_t s) {
+PanoViews views_before(const fs_plan_s* p, int k) {
+    PanoViews pv{};
+    pv.n = k;
+    for (int m = 0; m < k; ++m) pv.v[m] = view_of(p, m);
+    return pv;
+}
+
+// Enqueue one full execution on stream s (captured into the graph).  With
+// dag, each fold's partition / crop / pyramid / flow / distance transforms
+// run on its own branch stream as soon as their inputs exist, and only the
+// blend + compose of the folds form an ordered chain on s.
+int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag) {
     int launches = 0;
+    const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
     {
         ProfScope ps("clear", (double)p->cw * p->chh, s);
         FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
@@ -74,12 +93,42 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s) {
         launch::place_view(p->cv, view_of(p, 0), p->cc, s);
     }
     launches += 2;
-    for (int k = 1; k < p->n; ++k) {
-        FoldWS<ViewU8>& f = p->folds[k - 1];
-        ViewU8 v = view_of(p, k);
-        launches += fold_enqueue_pre(f, p->cv, v, s);
-        launches += fold_enqueue_flow_edt(f, p->cv, v, p->cc, p->fp, s, nullptr, nullptr);
-        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
+    if (!dag) {
+        for (int k = 1; k < p->n; ++k) {
+            FoldWS<ViewU8>& f = p->folds[k - 1];
+            ViewU8 v = view_of(p, k);
+            launches += fold_enqueue_pre(f, plane, v, s);
+            launch::snapshot_count(f.st, p->cc, s);
+            launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr);
+            launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
+        }
+    } else {
+        // prologue: every fold's partition from the union of the earlier views
+        std::vector<FoldStats*> sts;
+        for (int k = 1; k < p->n; ++k) {
+            launches += fold_enqueue_pre(p->folds[k - 1], views_before(p, k), view_of(p, k), s);
+            sts.push_back(p->folds[k - 1].st);
+        }
+        launch::prefix_counts(sts.data(), (int)sts.size(), p->cc, s);
+        ++launches;
+        FS_CK(cudaEventRecord(p->ev_pro, s));
+        for (int k = 1; k < p->n; ++k) {
+            FoldWS<ViewU8>& f = p->folds[k - 1];
+            ViewU8 v = view_of(p, k);
+            cudaStream_t b = p->branch[k - 1];
+            FS_CK(cudaStreamWaitEvent(b, p->ev_pro, 0));
+            const PanoViews pv = views_before(p, k);
+            if (p->crop_from_views[k]) {
+                launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr);
+            } else {  // an earlier Area3 box overlaps: L is the composed panorama
+                FS_CK(cudaStreamWaitEvent(b, p->ev_compose[k - 1], 0));
+                launches += fold_enqueue_flow_edt(f, pv, plane, v, 3, p->fp, b, nullptr, nullptr);
+            }
+            FS_CK(cudaEventRecord(p->ev_branch[k], b));
+            FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
+            launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
+            FS_CK(cudaEventRecord(p->ev_compose[k], s));
+        }
     }
     {
         ProfScope ps("quantize", 21.0 * p->cw * p->chh, s);  // rgb 16 + valid 1 in, rgba8 out
@@ -95,7 +144,7 @@ void build_graph(fs_plan_s* p) {
     FS_CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
     int launches = 0;
     try {
-        launches = enqueue_all(p, p->cap);
+        launches = enqueue_all(p, p->cap, p->dag);
     } catch (...) {
         cudaGraph_t g;
         cudaStreamEndCapture(p->cap, &g);
@@ -137,7 +186,7 @@ std::vector<Rect> boxes_from_masks(fs_plan_s* p, const uint8_t* const* views_rgb
         for (int k = 1; k < p->n; ++k) {
             ViewU8 v{tmp[k], p->rects[k]};
             init_stats(st + k, s);
-            launch::partition(cv, v, st + k, s);
+            launch::partition(PanoPlane{valid, nullptr, p->cw}, v, st + k, s);
             launch::union_valid(cv, v, s);
         }
         std::vector<FoldStats> hs(p->n);
@@ -230,6 +279,30 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         }
         FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
         std::vector<Rect> boxes = views_rgba ? boxes_from_masks(p, views_rgba) : boxes_from_rects(p);
+        // DAG: fold k's L crop may come straight from the views when no earlier
+        // fold's Area3 box overlaps its own (those pixels hold the first
+        // covering view's value); partitions and distance transforms always can.
+        p->dag = n <= kMaxDagViews;
+        p->crop_from_views.assign(n, 0);
+        for (int k = 1; k < n; ++k) {
+            bool disjoint = true;
+            for (int m = 1; m < k; ++m) {
+                Rect i = rect_inter(boxes[m], boxes[k]);
+                if (i.w > 0 && i.h > 0) disjoint = false;
+            }
+            p->crop_from_views[k] = disjoint;
+        }
+        if (p->dag) {
+            p->branch.assign(n - 1, nullptr);
+            p->ev_branch.assign(n, nullptr);
+            p->ev_compose.assign(n, nullptr);
+            for (auto& b : p->branch) FS_CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+            for (int k = 0; k < n; ++k) {
+                FS_CK(cudaEventCreateWithFlags(&p->ev_branch[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_compose[k], cudaEventDisableTiming));
+            }
+            FS_CK(cudaEventCreateWithFlags(&p->ev_pro, cudaEventDisableTiming));
+        }
         p->pano_bbox.assign(n, Rect{});
         Rect pb = p->rects[0];
         for (int k = 1; k < n; ++k) {
@@ -341,7 +414,7 @@ fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_
         kernel_prof() = &prof;
         try {
             FS_CK(cudaEventRecord(e0, s));
-            enqueue_all(p, s);
+            enqueue_all(p, s, false);  // serial, so each kernel is timed alone
             FS_CK(cudaEventRecord(e1, s));
         } catch (...) {
             kernel_prof() = nullptr;
@@ -377,6 +450,13 @@ fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_
 void fs_plan_destroy(fs_plan p) {
     if (!p) return;
     drop_graph(p);
+    for (auto b : p->branch)
+        if (b) cudaStreamDestroy(b);
+    for (auto e : p->ev_branch)
+        if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_compose)
+        if (e) cudaEventDestroy(e);
+    if (p->ev_pro) cudaEventDestroy(p->ev_pro);
     if (p->arena) cudaFree(p->arena);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;
