@@ -395,3 +395,30 @@ def test_plan_matches_oracle(fs, oracle):
     assert np.array_equal(out, out2), "replay is not deterministic"
     plan.close()
     plan2.close()
+
+
+# ---------------------------------------------------------------- golden vectors (made by the reference)
+def test_gpu_matches_golden_vectors(fs):
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz"))
+    p = g["strip_params"]
+    params = fs.FlowParams(int(p[0]), int(p[1]), int(p[2]), float(p[3]), int(p[4]))
+    placed = [fs.PlacedImage(fs.ImageBuf(g["strip_view%d" % k], g["strip_valid%d" % k]), int(x), int(y))
+              for k, (x, y) in enumerate(g["strip_offsets"])]
+    cw, ch = (int(v) for v in g["strip_canvas"])
+    pano, _ = fs.stitch_placed(placed, cw, ch, params)
+    assert np.array_equal(pano.valid, g["strip_out_valid"])
+    assert np.abs(pano.data - g["strip_out"]).max() <= 1e-5
+    f = fs.dense_pyr_lk(_img(fs, g["lk_from"]), _img(fs, g["lk_to"]))
+    assert np.array_equal(f.valid, g["lk_valid"]) and _epe(f.vec, g["lk_vec"]) <= EPE_TOL
+    assert np.array_equal(fs.distance_transform(fs.Mask(g["edt_mask"])).d, g["edt_out"])
+    part = fs.RegionPartition(g["bf_label"], g["bf_counts"])
+    assert np.array_equal(fs.compute_blend(part).b, g["bf_out"])
+    ones = np.ones(g["bp_label"].shape, np.uint8)
+    F = fs.blend_pair(_img(fs, g["bp_L"], g["bp_vl"]), _img(fs, g["bp_R"], g["bp_vr"]),
+                      fs.FlowField(g["bp_flr"], ones), fs.FlowField(g["bp_frl"], ones),
+                      fs.BlendField(g["bp_b"]), fs.RegionPartition(g["bp_label"], np.zeros(4, np.int64)))
+    assert np.array_equal(F.valid, g["bp_out_valid"]) and np.abs(F.data - g["bp_out"]).max() <= 1e-6
+    pyr = fs.build_pyramid(_img(fs, g["pyr_in"]), 4)
+    for k, lv in enumerate(pyr):
+        assert np.array_equal(lv.data[..., 0], g["pyr_l%d" % k])
