@@ -1,7 +1,8 @@
 /* fs_b200.h — C-ABI of the B200 flow+blend path (the drop-in boundary).
  *
  * One extern "C" entry point per function of the reference's hot-path API
- * (namespace flowstitch, /root/reference/proj/include/flowstitch/*.hpp), each
+ * (namespace flowstitch, /root/reference/proj/include/flowstitch/{image,flow,
+ * blend_field,blender,pipeline}.hpp), each
  * citing the declaration it replaces.  Plain pointers and sizes only; the
  * data layouts are the reference's value types:
  *   image : float[w*h*ch] interleaved, ch = 1 or 3, plus uint8 valid[w*h]
