@@ -148,29 +148,54 @@ def cpu_reference_run(lay, threads: int):
 
 
 def run_reference_arm(args, ws, rank):
+    """The reference's CPU fold (oracle/_ref, all host threads).  A step is
+    one fold of a continuously running fold chain over the panorama's views
+    (fold k = the reference's stitch of [panorama after fold k-1, view k],
+    which is exactly fold k of stitch_placed); after the last fold the chain
+    restarts from view 0.  value = canvas Mpx x (folds timed / folds per
+    panorama) / time, i.e. panoramas per second in canvas Mpx."""
     if rank != 0:
         return
+    import numpy as np
+    from oracle import reference
     lay = make_layout(args.config, 0)
     threads = os.cpu_count() or 1
+    ref = reference()
+    ref.set_threads(threads)
+    fv = lay.float_views()
+    nfold = len(fv) - 1
+    params = (lay.levels, 8, 3, 1e-4, 2)
+    pano = None
     times = []
     for i in range(args.warmup + args.steps):
-        dt, _, used = cpu_reference_run(lay, threads)
+        k = i % nfold + 1
+        if k == 1:
+            d0, v0 = fv[0]
+            pano = ref.place_on_canvas(d0, v0, lay.offsets[0][0], lay.offsets[0][1], lay.canvas_w,
+                                       lay.canvas_h)
+        t0 = time.perf_counter()
+        pano = ref.stitch_placed([pano[0], fv[k][0]], [pano[1], fv[k][1]],
+                                 [(0, 0), lay.offsets[k]], lay.canvas_w, lay.canvas_h, params)
+        dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-    s = statistics.mean(times)
-    value = lay.canvas_mpx / s
+    used = ref.threads()
+    total = sum(times)
+    s = total / len(times) * nfold  # seconds per panorama
+    value = lay.canvas_mpx * (len(times) / nfold) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(s * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(total / len(times) * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak",
         "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
         "config": {"workload": workload_name(lay, args.config), "canvas": [lay.canvas_w, lay.canvas_h],
                    "flow_params": [lay.levels, 8, 3, 1e-4, 2], "blend_params": [10.0, 0.05],
                    "parallelism": "host threads (reference parallel_rows)"},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": used, "kind": "reference",
-                         "sample": "one full %s fold per step (all %d folds), the reference "
-                                   "compiled from /root/reference with its Release flags"
-                                   % (args.config.upper(), len(lay.views) - 1)},
+                         "sample": "one fold per step of a running %d-fold %s chain (%d folds "
+                                   "timed), the reference compiled from /root/reference with its "
+                                   "Release flags" % (nfold, args.config.upper(), len(times))},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0, "s_per_panorama": round(s, 3)},
     }
