@@ -199,6 +199,8 @@ template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaS
 // pv_count of fold k = |view 0 valid| + sum of the Area2 counts of folds < k
 void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cudaStream_t);
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
+// pv_count = prev->pv_count + prev->cnt2 (prev: the previous fold), or cc for fold 1
+void chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc, cudaStream_t);
 void check_box(FoldStats*, const Rect&, cudaStream_t);
 template <class V, class P>
 void crop_gray(const P&, const V&, const Rect&, int ch, float*, float*, cudaStream_t);
@@ -218,6 +220,7 @@ template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);
 void quantize(const Canvas&, uchar4*, cudaStream_t);
+void quantize_rect(const Canvas&, const Rect&, uchar4*, cudaStream_t);  // canvas-indexed out
 void export_float(const Canvas&, float*, uint8_t*, cudaStream_t);
 }  // namespace launch
 

@@ -129,6 +129,9 @@ __global__ void k_prefix_counts(FoldStatsPtrs st, int n, const CanvasCount* cc) 
 __global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
     st->pv_count = cc->valid_count;
 }
+__global__ void k_chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc) {
+    st->pv_count = prev ? prev->pv_count + prev->cnt2 : cc->valid_count;
+}
 
 // src/image.cpp:134-162 then src/image.cpp:70-83: crop of both sides over the
 // Area3 box (invalid pixels zeroed) and their gray levels.
@@ -591,10 +594,10 @@ __global__ void k_count_update(CanvasCount* cc, const FoldStats* st) {
 }
 
 // K8 — 8-bit RGBA output (src/image.cpp:52-65): alpha = valid.
-__global__ void k_quantize(Canvas cv, uchar4* __restrict__ out) {
-    int x = blockIdx.x * blockDim.x + threadIdx.x;
-    int y = blockIdx.y;
-    if (x >= cv.w) return;
+__global__ void k_quantize(Canvas cv, Rect r, uchar4* __restrict__ out) {
+    int x = r.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    int y = r.y0 + blockIdx.y;
+    if (x >= r.x1()) return;
     size_t p = (size_t)y * cv.w + x;
     uchar4 o = make_uchar4(0, 0, 0, 0);
     if (cv.valid[p]) {
@@ -649,6 +652,9 @@ void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cuda
 }
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t s) {
     k_snapshot_count<<<1, 1, 0, s>>>(st, cc);
+}
+void chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc, cudaStream_t s) {
+    k_chain_count<<<1, 1, 0, s>>>(st, prev, cc);
 }
 void check_box(FoldStats* st, const Rect& planned, cudaStream_t s) {
     k_check_box<<<1, 1, 0, s>>>(st, planned);
@@ -722,7 +728,10 @@ void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
 void quantize(const Canvas& cv, uchar4* out, cudaStream_t s) {
-    k_quantize<<<row_grid(cv.w, cv.h), 256, 0, s>>>(cv, out);
+    quantize_rect(cv, Rect{0, 0, cv.w, cv.h}, out, s);
+}
+void quantize_rect(const Canvas& cv, const Rect& r, uchar4* out, cudaStream_t s) {
+    if (r.w > 0 && r.h > 0) k_quantize<<<row_grid(r.w, r.h), 256, 0, s>>>(cv, r, out);
 }
 void export_float(const Canvas& cv, float* out, uint8_t* vout, cudaStream_t s) {
     k_export_float<<<row_grid(cv.w, cv.h), 256, 0, s>>>(cv, out, vout);

@@ -37,9 +37,17 @@ struct fs_plan_s {
     // stream; crop_from_views[k]: fold k's L crop can be read from the views.
     bool dag = false;
     std::vector<cudaStream_t> branch;
-    std::vector<cudaEvent_t> ev_branch, ev_compose;
-    cudaEvent_t ev_pro = nullptr;
+    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt;
+    cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<char> crop_from_views;
+    // final_rects[k]: canvas rectangles no fold after k writes (k = 0: the
+    // placement of view 0); quantised and read back as soon as fold k composed.
+    std::vector<std::vector<Rect>> final_rects;
+    // graph with the host copies inside (execute_host), keyed by the pointers
+    cudaGraph_t hgraph = nullptr;
+    cudaGraphExec_t hexec = nullptr;
+    std::vector<const void*> hkey;
 };
 
 namespace {
@@ -76,18 +84,48 @@ PanoViews views_before(const fs_plan_s* p, int k) {
     return pv;
 }
 
-// Enqueue one full execution on stream s (captured into the graph).  With
-// dag, each fold's partition / crop / pyramid / flow / distance transforms
-// run on its own branch stream as soon as their inputs exist, and only the
-// blend + compose of the folds form an ordered chain on s.
-int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag) {
+// Host buffers of one execute_host call (nullptr members: device-resident).
+struct HostIO {
+    const uint8_t* const* views = nullptr;
+    uint8_t* out = nullptr;
+};
+
+// Enqueue one full execution on stream s (captured into a graph).
+//
+// serial (dag = false; fs_plan_profile and n > kMaxDagViews): the folds one
+// after another on s, the 8-bit panorama quantised at the end.
+//
+// dag: fold k's partition, crop, pyramid, flow and distance transforms run on
+// its own branch stream as soon as views 0..k exist (and, when its L crop
+// needs the composed panorama, after fold k-1's compose); only the blend +
+// compose of the folds form an ordered chain on s.  A fold's |pano valid| is
+// chained from the previous fold's partition counts.  Each canvas rectangle
+// is quantised (and, with io->out, copied to the host) on the d2h stream as
+// soon as the last fold that writes it composed.  With io->views, the views
+// are copied in fold order on the h2d stream and each fold starts when its
+// views have landed — host transfers overlap the folds.
+int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullptr) {
     int launches = 0;
     const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
+    const bool hin = io && io->views, hout = io && io->out;
+    if (dag) {
+        FS_CK(cudaEventRecord(p->ev_start, s));
+        if (hin) {
+            FS_CK(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
+            for (int k = 0; k < p->n; ++k) {
+                FS_CK(cudaMemcpyAsync(p->views[k], io->views[k],
+                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
+                                      cudaMemcpyDefault, p->h2d));
+                FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
+            }
+        }
+    }
     {
         ProfScope ps("clear", (double)p->cw * p->chh, s);
         FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
     }
     init_count(p->cc, s);
+    if (hin) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[0], 0));
     {
         ProfScope ps("place", 21.0 * p->rects[0].area(), s);  // view 4 in, rgb 16 + valid 1 out
         launch::place_view(p->cv, view_of(p, 0), p->cc, s);
@@ -102,65 +140,161 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag) {
             launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr);
             launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
         }
-    } else {
-        // prologue: every fold's partition from the union of the earlier views
-        std::vector<FoldStats*> sts;
-        for (int k = 1; k < p->n; ++k) {
-            launches += fold_enqueue_pre(p->folds[k - 1], views_before(p, k), view_of(p, k), s);
-            sts.push_back(p->folds[k - 1].st);
+        {
+            ProfScope ps("quantize", 21.0 * p->cw * p->chh, s);  // rgb 16 + valid 1 in, rgba8 out
+            launch::quantize(p->cv, p->out, s);
         }
-        launch::prefix_counts(sts.data(), (int)sts.size(), p->cc, s);
+        launches += 1;
+        FS_CK(cudaGetLastError());
+        return launches;
+    }
+    FS_CK(cudaEventRecord(p->ev_place, s));
+    // the read-back chain: quantise (and copy) every rectangle once final
+    auto emit_final = [&](int k, cudaEvent_t after) {
+        if (p->final_rects[k].empty()) return;
+        FS_CK(cudaStreamWaitEvent(p->d2h, after, 0));
+        for (const Rect& r : p->final_rects[k]) {
+            launch::quantize_rect(p->cv, r, p->out, p->d2h);
+            ++launches;
+            if (!hout) continue;
+            const size_t pitch = (size_t)p->cw * 4;
+            const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
+            if (r.w == p->cw)
+                FS_CK(cudaMemcpyAsync(io->out + off, reinterpret_cast<const uint8_t*>(p->out) + off,
+                                      pitch * r.h, cudaMemcpyDefault, p->d2h));
+            else
+                FS_CK(cudaMemcpy2DAsync(io->out + off, pitch,
+                                        reinterpret_cast<const uint8_t*>(p->out) + off, pitch,
+                                        (size_t)r.w * 4, r.h, cudaMemcpyDefault, p->d2h));
+        }
+    };
+    emit_final(0, p->ev_place);
+    for (int k = 1; k < p->n; ++k) {
+        FoldWS<ViewU8>& f = p->folds[k - 1];
+        ViewU8 v = view_of(p, k);
+        cudaStream_t b = p->branch[k - 1];
+        FS_CK(cudaStreamWaitEvent(b, hin ? p->ev_h2d[k] : p->ev_start, 0));
+        const PanoViews pv = views_before(p, k);
+        launches += fold_enqueue_pre(f, pv, v, b);
+        FS_CK(cudaStreamWaitEvent(b, k == 1 ? p->ev_place : p->ev_cnt[k - 1], 0));
+        launch::chain_count(f.st, k == 1 ? nullptr : p->folds[k - 2].st, p->cc, b);
         ++launches;
-        FS_CK(cudaEventRecord(p->ev_pro, s));
-        for (int k = 1; k < p->n; ++k) {
-            FoldWS<ViewU8>& f = p->folds[k - 1];
-            ViewU8 v = view_of(p, k);
-            cudaStream_t b = p->branch[k - 1];
-            FS_CK(cudaStreamWaitEvent(b, p->ev_pro, 0));
-            const PanoViews pv = views_before(p, k);
-            if (p->crop_from_views[k]) {
-                launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr);
-            } else {  // an earlier Area3 box overlaps: L is the composed panorama
-                FS_CK(cudaStreamWaitEvent(b, p->ev_compose[k - 1], 0));
-                launches += fold_enqueue_flow_edt(f, pv, plane, v, 3, p->fp, b, nullptr, nullptr);
-            }
-            FS_CK(cudaEventRecord(p->ev_branch[k], b));
-            FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
-            launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
-            FS_CK(cudaEventRecord(p->ev_compose[k], s));
+        FS_CK(cudaEventRecord(p->ev_cnt[k], b));
+        if (p->crop_from_views[k]) {
+            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr);
+        } else {  // an earlier Area3 box overlaps: L is the composed panorama
+            FS_CK(cudaStreamWaitEvent(b, p->ev_compose[k - 1], 0));
+            launches += fold_enqueue_flow_edt(f, pv, plane, v, 3, p->fp, b, nullptr, nullptr);
         }
+        FS_CK(cudaEventRecord(p->ev_branch[k], b));
+        FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
+        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
+        FS_CK(cudaEventRecord(p->ev_compose[k], s));
+        emit_final(k, p->ev_compose[k]);
     }
-    {
-        ProfScope ps("quantize", 21.0 * p->cw * p->chh, s);  // rgb 16 + valid 1 in, rgba8 out
-        launch::quantize(p->cv, p->out, s);
-    }
-    launches += 1;
+    FS_CK(cudaEventRecord(p->ev_out, p->d2h));
+    FS_CK(cudaStreamWaitEvent(s, p->ev_out, 0));
     FS_CK(cudaGetLastError());
     return launches;
 }
 
-void build_graph(fs_plan_s* p) {
-    if (p->exec) return;
+void capture(fs_plan_s* p, const HostIO* io, cudaGraph_t* graph, cudaGraphExec_t* exec) {
     FS_CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
     int launches = 0;
     try {
-        launches = enqueue_all(p, p->cap, p->dag);
+        launches = enqueue_all(p, p->cap, p->dag, io);
     } catch (...) {
-        cudaGraph_t g;
+        cudaGraph_t g = nullptr;
         cudaStreamEndCapture(p->cap, &g);
         if (g) cudaGraphDestroy(g);
         throw;
     }
-    FS_CK(cudaStreamEndCapture(p->cap, &p->graph));
-    FS_CK(cudaGraphInstantiate(&p->exec, p->graph, 0));
+    FS_CK(cudaStreamEndCapture(p->cap, graph));
+    FS_CK(cudaGraphInstantiate(exec, *graph, 0));
     p->launches = launches;
+}
+
+void build_graph(fs_plan_s* p) {
+    if (!p->exec) capture(p, nullptr, &p->graph, &p->exec);
 }
 
 void drop_graph(fs_plan_s* p) {
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->graph) cudaGraphDestroy(p->graph);
+    if (p->hexec) cudaGraphExecDestroy(p->hexec);
+    if (p->hgraph) cudaGraphDestroy(p->hgraph);
     p->exec = nullptr;
     p->graph = nullptr;
+    p->hexec = nullptr;
+    p->hgraph = nullptr;
+    p->hkey.clear();
+}
+
+// Page-locked (or device) memory can be read by a graph's copy nodes
+// asynchronously; pageable host memory cannot.
+bool async_copyable(const void* ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type != cudaMemoryTypeUnregistered;
+}
+
+// Canvas rectangles final after fold k (k = 0: after view 0 is placed): the
+// canvas is cut into cells along every view edge; a cell is final after the
+// last fold whose view covers it (fold m writes only inside view m's rect).
+void plan_final_rects(fs_plan_s* p) {
+    std::vector<int> xs{0, p->cw}, ys{0, p->chh};
+    for (const Rect& r : p->rects) {
+        xs.push_back(r.x0);
+        xs.push_back(r.x1());
+        ys.push_back(r.y0);
+        ys.push_back(r.y1());
+    }
+    std::sort(xs.begin(), xs.end());
+    xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
+    std::sort(ys.begin(), ys.end());
+    ys.erase(std::unique(ys.begin(), ys.end()), ys.end());
+    p->final_rects.assign(p->n, {});
+    std::vector<std::vector<Rect>> open(p->n);  // runs of the previous row band
+    for (size_t j = 0; j + 1 < ys.size(); ++j) {
+        const int y0 = ys[j], y1 = ys[j + 1];
+        std::vector<std::vector<Rect>> cur(p->n);
+        for (size_t i = 0; i + 1 < xs.size();) {
+            auto last_of = [&](size_t c) {
+                int last = 0;
+                for (int k = 0; k < p->n; ++k)
+                    if (p->rects[k].contains(xs[c], y0)) last = k;
+                return last;
+            };
+            const int k = last_of(i);
+            size_t e = i + 1;
+            while (e + 1 < xs.size() && last_of(e) == k) ++e;
+            cur[k].push_back(Rect{xs[i], y0, xs[e] - xs[i], y1 - y0});
+            i = e;
+        }
+        for (int k = 0; k < p->n; ++k) {  // extend matching runs of the band above
+            std::vector<Rect> next;
+            for (Rect r : cur[k]) {
+                bool merged = false;
+                for (Rect& o : open[k])
+                    if (o.x0 == r.x0 && o.w == r.w && o.y1() == r.y0) {
+                        o.h += r.h;
+                        next.push_back(o);
+                        o.w = 0;
+                        merged = true;
+                        break;
+                    }
+                if (!merged) next.push_back(r);
+            }
+            for (const Rect& o : open[k])
+                if (o.w > 0) p->final_rects[k].push_back(o);
+            open[k] = next;
+        }
+    }
+    for (int k = 0; k < p->n; ++k)
+        for (const Rect& o : open[k]) p->final_rects[k].push_back(o);
 }
 
 // Area3 boxes of every fold from the view masks: a validity-only fold on the
@@ -297,11 +431,19 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             p->ev_branch.assign(n, nullptr);
             p->ev_compose.assign(n, nullptr);
             for (auto& b : p->branch) FS_CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+            p->ev_h2d.assign(n, nullptr);
+            p->ev_cnt.assign(n, nullptr);
             for (int k = 0; k < n; ++k) {
                 FS_CK(cudaEventCreateWithFlags(&p->ev_branch[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_compose[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_cnt[k], cudaEventDisableTiming));
             }
-            FS_CK(cudaEventCreateWithFlags(&p->ev_pro, cudaEventDisableTiming));
+            for (cudaEvent_t* e : {&p->ev_start, &p->ev_place, &p->ev_out})
+                FS_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            FS_CK(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
+            FS_CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+            plan_final_rects(p);
         }
         p->pano_bbox.assign(n, Rect{});
         Rect pb = p->rects[0];
@@ -383,21 +525,48 @@ fs_status fs_plan_execute_host(fs_plan p, const uint8_t* const* views_rgba, uint
     return plan_guard([&] {
         FS_CK(cudaSetDevice(p->device));
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        if (views_rgba)
-            for (int k = 0; k < p->n; ++k)
-                FS_CK(cudaMemcpyAsync(p->views[k], views_rgba[k],
-                                      (size_t)p->rects[k].w * p->rects[k].h * 4, cudaMemcpyDefault,
-                                      s));
+        // transfers inside the graph, overlapping the folds, when the host
+        // buffers allow asynchronous copies
+        bool overlap = p->dag && (views_rgba || out_rgba);
+        if (overlap && views_rgba)
+            for (int k = 0; k < p->n; ++k) overlap = overlap && async_copyable(views_rgba[k]);
+        if (overlap && out_rgba) overlap = async_copyable(out_rgba);
+        std::vector<const void*> key;
+        if (overlap) {
+            for (int k = 0; views_rgba && k < p->n; ++k) key.push_back(views_rgba[k]);
+            key.push_back(views_rgba ? (const void*)1 : nullptr);
+            key.push_back(out_rgba);
+        }
         for (int attempt = 0; attempt < 2; ++attempt) {
-            build_graph(p);
-            FS_CK(cudaGraphLaunch(p->exec, s));
-            if (out_rgba)
-                FS_CK(cudaMemcpyAsync(out_rgba, p->out, (size_t)p->cw * p->chh * 4,
-                                      cudaMemcpyDefault, s));
+            if (overlap) {
+                if (p->hexec && p->hkey != key) {
+                    cudaGraphExecDestroy(p->hexec);
+                    cudaGraphDestroy(p->hgraph);
+                    p->hexec = nullptr;
+                    p->hgraph = nullptr;
+                }
+                if (!p->hexec) {
+                    HostIO io{views_rgba, out_rgba};
+                    capture(p, &io, &p->hgraph, &p->hexec);
+                    p->hkey = key;
+                }
+                FS_CK(cudaGraphLaunch(p->hexec, s));
+            } else {
+                if (views_rgba)
+                    for (int k = 0; k < p->n; ++k)
+                        FS_CK(cudaMemcpyAsync(p->views[k], views_rgba[k],
+                                              (size_t)p->rects[k].w * p->rects[k].h * 4,
+                                              cudaMemcpyDefault, s));
+                build_graph(p);
+                FS_CK(cudaGraphLaunch(p->exec, s));
+                if (out_rgba)
+                    FS_CK(cudaMemcpyAsync(out_rgba, p->out, (size_t)p->cw * p->chh * 4,
+                                          cudaMemcpyDefault, s));
+            }
             FS_CK(cudaStreamSynchronize(s));
             fs_status c = fs_plan_check(p);
             if (c == FS_OK) return;
-            if (attempt == 1 || p->exec) raise(c, last_error_slot());
+            if (attempt == 1 || p->exec || p->hexec) raise(c, last_error_slot());
         }
     });
 }
@@ -456,7 +625,14 @@ void fs_plan_destroy(fs_plan p) {
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_compose)
         if (e) cudaEventDestroy(e);
-    if (p->ev_pro) cudaEventDestroy(p->ev_pro);
+    for (auto e : p->ev_h2d)
+        if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_cnt)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {p->ev_start, p->ev_place, p->ev_out})
+        if (e) cudaEventDestroy(e);
+    if (p->h2d) cudaStreamDestroy(p->h2d);
+    if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->arena) cudaFree(p->arena);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;

@@ -397,6 +397,54 @@ def test_plan_matches_oracle(fs, oracle):
     plan2.close()
 
 
+def _grid_layout(seed=3):
+    """2x2 views with a band across the middle: canvas rectangles become
+    final after different folds, in both directions."""
+    W, H = 420, 300
+    scene = S.rgb_scene(H, W, seed)
+    offs = [(0, 0), (180, 0), (0, 130), (180, 130), (0, 100)]
+    sizes = [(240, 170), (240, 170), (240, 170), (240, 170), (420, 100)]
+    views = [S.rgba(scene[y:y + h, x:x + w]) for (x, y), (w, h) in zip(offs, sizes)]
+    return S.Layout("grid", W, H, views, offs, 3)
+
+
+@pytest.mark.parametrize("which", ["panorama", "grid"])
+def test_plan_host_overlap_matches_sync_path(fs, which):
+    """execute_host with page-locked buffers runs the graph whose copies
+    overlap the folds (per-view H2D, per-rectangle quantise + D2H); it must
+    reproduce the pageable (copy, graph, copy) path and the device path."""
+    import torch
+    lay = S.small_panorama(seed=2) if which == "panorama" else _grid_layout()
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=3))
+    ref = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    plan.execute_host(lay.views, ref)  # pageable numpy: synchronous copies
+    pin = [torch.from_numpy(v).pin_memory() for v in lay.views]
+    out = torch.full((lay.canvas_h, lay.canvas_w, 4), 7, dtype=torch.uint8).pin_memory()
+    for _ in range(2):  # capture, then replay
+        out.fill_(7)
+        plan.execute_ptrs([t.data_ptr() for t in pin], out.data_ptr())
+        assert np.array_equal(out.numpy(), ref)
+    # new host buffers: the graph is re-captured for the new pointers
+    pin2 = [t.clone().pin_memory() for t in pin]
+    out2 = torch.zeros_like(out).pin_memory()
+    plan.execute_ptrs([t.data_ptr() for t in pin2], out2.data_ptr())
+    assert np.array_equal(out2.numpy(), ref)
+    # device-resident execution reads the same panorama from the output buffer
+    plan.execute(0)
+    torch.cuda.synchronize()
+
+    class _Dev:
+        __cuda_array_interface__ = {"shape": ref.shape, "typestr": "|u1", "version": 3,
+                                    "data": (plan.output_buffer(), False), "strides": None}
+    dev = torch.as_tensor(_Dev(), device="cuda").cpu().numpy()
+    assert np.array_equal(dev, ref)
+    # output only (views already resident): the in-graph read-back alone
+    out.fill_(7)
+    plan.execute_host(None, out.numpy())
+    assert np.array_equal(out.numpy(), ref)
+    plan.close()
+
+
 # ---------------------------------------------------------------- golden vectors (made by the reference)
 def test_gpu_matches_golden_vectors(fs):
     import os
