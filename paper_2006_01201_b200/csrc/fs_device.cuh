@@ -117,8 +117,6 @@ struct LkDir {
     uint8_t* okout;   // written by the first iteration of a level only
     float4* coef;     // level-constant (c/det, b/det, a/det, ok): written by the
                       // first iteration, read by the later ones (nullptr: unused)
-    const float* dtin;  // It of this iteration (written by prep / the previous sweep)
-    float* dtout;       // It of the next iteration (nullptr: level's last iteration)
 };
 struct LkArgs {
     LkDir d[2];

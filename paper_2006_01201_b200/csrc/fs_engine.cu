@@ -113,7 +113,6 @@ void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
         for (int q = 0; q < 2; ++q) {
             fb[d][q] = a.take<float2>(n);
             ok[d][q] = a.take<uint8_t>(n);
-            dt[d][q] = a.take<float>(n);
         }
         coef[d] = a.take<float4>(n);
     }
@@ -141,7 +140,7 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
          "lk_iter_L6", "lk_iter_L7"},
         {"lk_first", "lk_first_L1", "lk_first_L2", "lk_first_L3", "lk_first_L4",
          "lk_first_L5", "lk_first_L6", "lk_first_L7"}};
-    int fcur = 0, okcur = 0, dcur = 0;
+    int fcur = 0, okcur = 0;
     for (int l = ws.depth - 1; l >= 0; --l) {
         const Level L = ws.lv[l];
         const double npx = (double)L.w * L.h * ws.ndir;
@@ -172,38 +171,33 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             a.d[d].okin = ws.ok[d][okcur];
             a.d[d].fout = ws.fb[d][fcur ^ 1];
             a.d[d].okout = ws.ok[d][okcur ^ 1];
-            a.d[d].dtout = ws.dt[d][dcur];
         }
         {
-            // F 4 + T 4 + flow 8 + ok 1 + It 4 out, + the coarser flow/ok 9/4
-            ProfScope ps("lk_prep", (21.0 + (a.mode == 2 ? 2.25 : 0.0)) * npx, s);
+            // flow 8 + ok 1 out, + the coarser flow/ok 9/4
+            ProfScope ps("lk_prep", (9.0 + (a.mode == 2 ? 2.25 : 0.0)) * npx, s);
             FS_CK(launch::lk_prep(a, s));
         }
         ++launches;
         fcur ^= 1;
         okcur ^= 1;
         for (int it = 0; it < p.iterations_per_level; ++it) {
-            const bool full = it == 0, last = it + 1 == p.iterations_per_level;
+            const bool full = it == 0;
             for (int d = 0; d < ws.ndir; ++d) {
                 a.d[d].fin = ws.fb[d][fcur];
                 a.d[d].okin = ws.ok[d][okcur];
                 a.d[d].fout = ws.fb[d][fcur ^ 1];
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
-                a.d[d].dtin = ws.dt[d][dcur];
-                a.d[d].dtout = last ? nullptr : ws.dt[d][dcur ^ 1];
             }
             {
-                // per pixel and direction: F 4 + It 4 + flow 8 in, flow 8 out;
-                //  first iteration: ok 1 in/out + coef 16 out; later: coef 16 in;
-                //  not the level's last: F 4 + T 4 in, It 4 out for the next one
-                double per = 24.0 + (full ? 2.0 + (a.d[0].coef ? 16.0 : 0.0) : 16.0) +
-                             (last ? 0.0 : 12.0);
+                // per pixel and direction: F 4 + T 4 (It gather) + flow 8 in,
+                //  flow 8 out; first iteration: ok 1 in/out + coef 16 out;
+                //  later: coef 16 in
+                double per = 24.0 + (full ? 2.0 + (a.d[0].coef ? 16.0 : 0.0) : 16.0);
                 ProfScope ps(kSweepNames[full][std::min(l, 7)], per * npx, s);
                 FS_CK(launch::lk_sweep(a, full, s));
             }
             ++launches;
             fcur ^= 1;
-            if (!last) dcur ^= 1;
             if (full) okcur ^= 1;  // ever_ok is final after a level's first iteration
         }
         int P = p.smoothing_passes;

@@ -74,7 +74,6 @@ struct FlowWS {
     float2* fb[2][2] = {};       // [dir][pingpong] level flow
     uint8_t* ok[2][2] = {};
     float4* coef[2] = {};        // [dir] level-constant inverse structure tensor
-    float* dt[2][2] = {};        // [dir][pingpong] It
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
 // Enqueue the whole coarse-to-fine flow on stream s.  ndir = 1: from=g0,

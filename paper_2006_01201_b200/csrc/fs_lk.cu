@@ -39,8 +39,8 @@ namespace fs {
 template <bool FULL>
 struct LkCfg {
     static constexpr int NQ = FULL ? 5 : 2;  // window sums carried
-    static constexpr int NB = FULL ? 4 : 8;  // rows per staged batch
-    static constexpr int S = FULL ? 4 : 8;   // outputs per horizontal run
+    static constexpr int NB = 4;  // rows per staged batch
+    static constexpr int S = 4;   // outputs per horizontal run
 };
 
 constexpr int LK_IW = 128;  // producer threads = input columns per CTA
@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(256) k_lk_prep(LkArgs a) {
     const size_t o = (size_t)y * a.w + x;
     D.fout[o] = f;
     D.okout[o] = ok;
-    D.dtout[o] = lk_it(D.T, D.F, a.w, a.h, x, y, f);
 }
 
 // ---- producer: sweep rows, stage vertical window sums ----------------------
@@ -123,13 +122,20 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, floa
     double V[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) V[q] = 0.0;
+    // the current flow of the batch's pixels, loaded one batch ahead: It is
+    // gathered here, at every window pixel (src/flow.cpp:248-249)
+    float2 fl[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+        fl[b] = D.fin[(size_t)clampi(ystart + b, 0, h - 1) * w + xc];
     for (int i = 0; i < nbat; ++i) {
         const int buf = i & 1;
         const int ybase = ystart + i * NB;
-        float gxs[NB], gys[NB], dts[NB];
+        float gxs[NB], gys[NB], fcs[NB], tap[NB][4];
+        double tfx[NB], tfy[NB];
         bool in[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {  // coalesced, independent loads of the batch
+        for (int b = 0; b < NB; ++b) {  // independent loads of the batch
             const int y = ybase + b;
             in[b] = xin && y >= 0 && y < h && y < yend;
             const int yy = clampi(y, 0, h - 1);
@@ -137,7 +143,27 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, floa
             gxs[b] = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));  // src/flow.cpp:230-235
             gys[b] = 0.5f * (__ldg(D.F + (size_t)min(yy + 1, h - 1) * w + xc) -
                              __ldg(D.F + (size_t)max(yy - 1, 0) * w + xc));
-            dts[b] = __ldg(D.dtin + (size_t)yy * w + xc);
+            fcs[b] = __ldg(Frow + xc);
+            LevelTap t = level_tap(w, h, (double)((float)xc + fl[b].x), (double)((float)yy + fl[b].y));
+            tfx[b] = t.fx;
+            tfy[b] = t.fy;
+            tap[b][0] = __ldg(D.T + (size_t)t.y0 * w + t.x0);
+            tap[b][1] = __ldg(D.T + (size_t)t.y0 * w + t.x1);
+            tap[b][2] = __ldg(D.T + (size_t)t.y1 * w + t.x0);
+            tap[b][3] = __ldg(D.T + (size_t)t.y1 * w + t.x1);
+        }
+        if (i + 1 < nbat) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                fl[b] = D.fin[(size_t)clampi(ybase + NB + b, 0, h - 1) * w + xc];
+        }
+        float dts[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            LevelTap t;
+            t.fx = tfx[b];
+            t.fy = tfy[b];
+            dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - fcs[b];
         }
         if (i >= 2) bar_sync(3 + buf);  // consumers released this buffer
         double* st = stage + (size_t)buf * lk_stage_doubles<FULL>();
@@ -174,7 +200,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                                            int x0, int y0, int ystart, int yo_end, int nbat) {
     using Cfg = LkCfg<FULL>;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ, S = Cfg::S;
-    const int r = a.r, w = a.w, h = a.h;
+    const int r = a.r, w = a.w;
     const int IWP = lk_iwp(LK_IW);
     const int nruns = (a.tw + S - 1) / S;
     const int t = threadIdx.x - LK_IW;
@@ -257,14 +283,6 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                 }
                 fo[o] = f;
                 D.fout[oi] = f;
-            }
-            if (D.dtout) {  // It of the next iteration at the updated flow
-#pragma unroll
-                for (int o = 0; o < S; ++o) {
-                    if (o >= nout) break;
-                    const int xo = x0 + cs + o;
-                    D.dtout[(size_t)yo * w + xo] = lk_it(D.T, D.F, w, h, xo, yo, fo[o]);
-                }
             }
         }
         if (i + 2 < nbat) bar_arrive(3 + buf);  // buffer free for batch i + 2
