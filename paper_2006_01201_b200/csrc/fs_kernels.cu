@@ -188,68 +188,84 @@ constexpr int SM_TX = 32, SM_TY = 16;
 __constant__ double kInvSmall[10] = {0.0,       1.0,       1.0 / 2, 1.0 / 3, 1.0 / 4,
                                      1.0 / 5,   1.0 / 6,   1.0 / 7, 1.0 / 8, 1.0 / 9};
 
-__global__ void __launch_bounds__(SM_TX* SM_TY) k_smooth(SmoothArgs a) {
-    __shared__ float2 src[SM_TY + 4][SM_TX + 4];
-    __shared__ float2 p1[SM_TY + 2][SM_TX + 2];
+// One 3x3 mean (src/flow.cpp:175-200): the in-image neighbours summed in
+// double in the reference's row-major order, then (float)(sum / n).  INNER
+// blocks lie (with their halo) inside the level, so every neighbour counts
+// and n = 9.
+template <bool INNER, int TW>
+__device__ __forceinline__ float2 box3(const float2 (*tile)[TW], int ly, int lx, int gx, int gy,
+                                       int w, int h) {
+    double ax = 0.0, ay = 0.0;
+    int n = 0;
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+        for (int di = -1; di <= 1; ++di) {
+            if (!INNER) {
+                const int xx = gx + di, yy = gy + dj;
+                if (xx < 0 || xx >= w || yy < 0 || yy >= h) continue;
+            }
+            const float2 v = tile[ly + dj][lx + di];
+            ax += v.x;
+            ay += v.y;
+            ++n;
+        }
+    if (INNER) n = 9;
+    return make_float2(div_to_float(ax, n, kInvSmall[n]), div_to_float(ay, n, kInvSmall[n]));
+}
+
+template <bool INNER>
+__device__ __forceinline__ void smooth_tile(const SmoothArgs& a, float2 (*src)[SM_TX + 4],
+                                            float2 (*p1)[SM_TX + 2]) {
     const int d = blockIdx.z;
-    const float2* fin = d ? a.fin[1] : a.fin[0];
     const int w = a.w, h = a.h;
     const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
-    const int halo = a.passes == 2 ? 2 : 1;
-    for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 4) * (SM_TX + 4);
-         t += SM_TX * SM_TY) {
-        int ly = t / (SM_TX + 4), lx = t - ly * (SM_TX + 4);
-        int gx = bx - 2 + lx, gy = by - 2 + ly;
-        src[ly][lx] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? fin[(size_t)gy * w + gx]
-                                                               : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    if (halo == 2) {
-        for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 2) * (SM_TX + 2);
-             t += SM_TX * SM_TY) {
-            int ly = t / (SM_TX + 2), lx = t - ly * (SM_TX + 2);
-            int gx = bx - 1 + lx, gy = by - 1 + ly;
+    const int tid = threadIdx.y * SM_TX + threadIdx.x;
+    const bool two = a.passes == 2;
+    if (two) {
+        for (int t = tid; t < (SM_TY + 2) * (SM_TX + 2); t += SM_TX * SM_TY) {
+            const int ly = t / (SM_TX + 2), lx = t - ly * (SM_TX + 2);
+            const int gx = bx - 1 + lx, gy = by - 1 + ly;
             float2 v = make_float2(0.f, 0.f);
-            if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-                double ax = 0.0, ay = 0.0;
-                int n = 0;
-                for (int dj = -1; dj <= 1; ++dj)
-                    for (int di = -1; di <= 1; ++di) {
-                        int xx = gx + di, yy = gy + dj;
-                        if (xx < 0 || xx >= w || yy < 0 || yy >= h) continue;
-                        float2 s = src[ly + 1 + dj][lx + 1 + di];
-                        ax += s.x;
-                        ay += s.y;
-                        ++n;
-                    }
-                v = make_float2(div_to_float(ax, n, kInvSmall[n]),
-                                div_to_float(ay, n, kInvSmall[n]));
-            }
+            if (INNER || (gx >= 0 && gx < w && gy >= 0 && gy < h))
+                v = box3<INNER, SM_TX + 4>(src, ly + 1, lx + 1, gx, gy, w, h);
             p1[ly][lx] = v;
         }
         __syncthreads();
     }
     const int gx = bx + threadIdx.x, gy = by + threadIdx.y;
     if (gx >= w || gy >= h) return;
-    double ax = 0.0, ay = 0.0;
-    int n = 0;
-    for (int dj = -1; dj <= 1; ++dj)
-        for (int di = -1; di <= 1; ++di) {
-            int xx = gx + di, yy = gy + dj;
-            if (xx < 0 || xx >= w || yy < 0 || yy >= h) continue;
-            float2 s = halo == 2 ? p1[threadIdx.y + 1 + dj][threadIdx.x + 1 + di]
-                                 : src[threadIdx.y + 2 + dj][threadIdx.x + 2 + di];
-            ax += s.x;
-            ay += s.y;
-            ++n;
-        }
-    float vx = div_to_float(ax, n, kInvSmall[n]), vy = div_to_float(ay, n, kInvSmall[n]);
-    size_t o = (size_t)gy * w + gx;
+    const float2 v = two ? box3<INNER, SM_TX + 2>(p1, threadIdx.y + 1, threadIdx.x + 1, gx, gy, w, h)
+                         : box3<INNER, SM_TX + 4>(src, threadIdx.y + 2, threadIdx.x + 2, gx, gy, w, h);
+    float vx = v.x, vy = v.y;
+    const size_t o = (size_t)gy * w + gx;
     if (a.final_cap > 0.f) {
         final_cap(a.final_cap, vx, vy);
         (d ? a.valid_out[1] : a.valid_out[0])[o] = (d ? a.ok[1] : a.ok[0])[o];
     }
     (d ? a.fout[1] : a.fout[0])[o] = make_float2(vx, vy);
+}
+
+__global__ void __launch_bounds__(SM_TX* SM_TY, 3) k_smooth(SmoothArgs a) {
+    __shared__ float2 src[SM_TY + 4][SM_TX + 4];
+    __shared__ float2 p1[SM_TY + 2][SM_TX + 2];
+    const int d = blockIdx.z;
+    const float2* fin = d ? a.fin[1] : a.fin[0];
+    const int w = a.w, h = a.h;
+    const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
+    for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 4) * (SM_TX + 4);
+         t += SM_TX * SM_TY) {
+        const int ly = t / (SM_TX + 4), lx = t - ly * (SM_TX + 4);
+        const int gx = bx - 2 + lx, gy = by - 2 + ly;
+        float2 v = make_float2(0.f, 0.f);
+        if (gx >= 0 && gx < w && gy >= 0 && gy < h) v = fin[(size_t)gy * w + gx];
+        src[ly][lx] = v;
+    }
+    __syncthreads();
+    if (bx >= 2 && by >= 2 && bx + SM_TX + 2 <= w && by + SM_TY + 2 <= h)
+        smooth_tile<true>(a, src, p1);
+    else
+        smooth_tile<false>(a, src, p1);
 }
 
 // Level-0 finalisation when smoothing_passes == 0 (src/flow.cpp:300-313).
@@ -510,6 +526,7 @@ __device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, d
         out[0] = out[1] = out[2] = 0.f;
         return;
     }
+    const double inv = 1.0 / wsum;  // one division for the channels
     for (int c = 0; c < ch; ++c) {
         double acc = 0.0;
 #pragma unroll
@@ -517,7 +534,7 @@ __device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, d
             float pv = c == 0 ? px[k].x : (c == 1 ? px[k].y : px[k].z);
             if (v[k]) acc += t.ws[k] * pv;
         }
-        out[c] = (float)(acc / wsum);
+        out[c] = div_to_float(acc, wsum, inv);
     }
 }
 

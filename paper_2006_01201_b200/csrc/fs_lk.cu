@@ -47,8 +47,13 @@ constexpr int LK_IW = 128;  // producer threads = input columns per CTA
 constexpr int LK_THREADS = 2 * LK_IW;
 
 __host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
+// Ring of the last 2r+1 rows per column, so the row leaving the window is
+// subtracted exactly: FULL keeps (Ix, Iy, It) as floats (five products are
+// re-formed), later iterations keep the two double products themselves.
+template <bool FULL>
 __host__ __device__ inline size_t lk_ring_bytes(int r) {
-    return ((size_t)(2 * r + 1) * LK_IW * 3 * sizeof(float) + 15) & ~size_t(15);
+    const size_t per = FULL ? 3 * sizeof(float) : 2 * sizeof(double);
+    return ((size_t)(2 * r + 1) * LK_IW * per + 15) & ~size_t(15);
 }
 template <bool FULL>
 __host__ __device__ inline size_t lk_stage_doubles() {
@@ -56,7 +61,7 @@ __host__ __device__ inline size_t lk_stage_doubles() {
 }
 template <bool FULL>
 __host__ inline size_t lk_smem_bytes(int r) {
-    return lk_ring_bytes(r) + 2 * lk_stage_doubles<FULL>() * sizeof(double);
+    return lk_ring_bytes<FULL>(r) + 2 * lk_stage_doubles<FULL>() * sizeof(double);
 }
 
 __device__ __forceinline__ void bar_sync(int id) {
@@ -66,15 +71,25 @@ __device__ __forceinline__ void bar_arrive(int id) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
 }
 
-// src/flow.cpp:248-249: It = sample_level(to, i + dx, j + dy) - from(i, j)
-__device__ __forceinline__ float lk_it(const float* __restrict__ T, const float* __restrict__ F,
-                                       int w, int h, int x, int y, float2 f) {
-    LevelTap t = level_tap(w, h, (double)((float)x + f.x), (double)((float)y + f.y));
-    float warped = level_combine(t, __ldg(T + (size_t)t.y0 * w + t.x0),
-                                 __ldg(T + (size_t)t.y0 * w + t.x1),
-                                 __ldg(T + (size_t)t.y1 * w + t.x0),
-                                 __ldg(T + (size_t)t.y1 * w + t.x1));
-    return warped - __ldg(F + (size_t)y * w + x);
+// level_tap (fs_math.cuh) of the float position (i + dx, j + dy) of
+// src/flow.cpp:248: the clamp bounds are integers, so clamping, flooring and
+// x - floor(x) are exact in float — same taps and fractions as in double.
+struct TapF {
+    int off, dx, dy;  // T offset of (x0, y0); +x / +y tap steps
+    float fx, fy;
+};
+__device__ __forceinline__ TapF level_tap_f(int w, int h, float px, float py) {
+    const float wm = (float)(w - 1), hm = (float)(h - 1);
+    px = px < 0.f ? 0.f : (wm < px ? wm : px);
+    py = py < 0.f ? 0.f : (hm < py ? hm : py);
+    const int x0 = (int)px, y0 = (int)py;
+    TapF t;
+    t.off = y0 * w + x0;
+    t.dx = min(x0 + 1, w - 1) - x0;
+    t.dy = (min(y0 + 1, h - 1) - y0) * w;
+    t.fx = px - (float)x0;
+    t.fy = py - (float)y0;
+    return t;
 }
 
 // ---- per-level start: flow, ever_ok and It ---------------------------------
@@ -100,8 +115,15 @@ __global__ void __launch_bounds__(256) k_lk_prep(LkArgs a) {
 }
 
 // ---- producer: sweep rows, stage vertical window sums ----------------------
+// Per column, `from` walks down in registers: rows y-1, y (fu, f0) carried
+// from the previous batch, rows y+1.. loaded one batch ahead (fn).  The
+// horizontal neighbours F(x -/+ 1, y) are the neighbouring threads' centre
+// values (their columns are clamp(x -/+ 1), src/flow.cpp:230-235); only the
+// warp's edge lanes load them.  It = to(p + d) - from(p) (src/flow.cpp:248-249)
+// is gathered at every window pixel from the current flow (loaded one batch
+// ahead).  All indices are 32-bit (levels hold < 2^31 pixels).
 template <bool FULL>
-__device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, float* ring,
+__device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void* ringv,
                                            double* stage, int x0, int ystart, int yend, int nbat) {
     using Cfg = LkCfg<FULL>;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ;
@@ -111,82 +133,90 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, floa
     const int x = x0 - r + c;
     const bool xin = x >= 0 && x < w;
     const int xc = clampi(x, 0, w - 1);
-    const int xl = clampi(x - 1, 0, w - 1), xr = clampi(x + 1, 0, w - 1);
+    const int dxl = clampi(x - 1, 0, w - 1) - xc, dxr = clampi(x + 1, 0, w - 1) - xc;
     const int cc = c + (c >> 3);
+    const float* __restrict__ Fc = D.F + xc;
+    const float2* __restrict__ Uc = D.fin + xc;
+    const float* __restrict__ T = D.T;
+    float* ringf = static_cast<float*>(ringv);
+    double2* ringd = static_cast<double2*>(ringv);
     for (int k = 0; k < K; ++k) {
-        float* rs = ring + ((size_t)k * LK_IW + c) * 3;
-        rs[0] = 0.f;
-        rs[1] = 0.f;
-        rs[2] = 0.f;
+        if (FULL) {
+            float* rs = ringf + (k * LK_IW + c) * 3;
+            rs[0] = rs[1] = rs[2] = 0.f;
+        } else {
+            ringd[k * LK_IW + c] = make_double2(0.0, 0.0);
+        }
     }
     double V[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) V[q] = 0.0;
-    // the current flow of the batch's pixels, loaded one batch ahead: It is
-    // gathered here, at every window pixel (src/flow.cpp:248-249)
+    auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
     float2 fl[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-        fl[b] = D.fin[(size_t)clampi(ystart + b, 0, h - 1) * w + xc];
+    for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
+    int slot = 0;
     for (int i = 0; i < nbat; ++i) {
         const int buf = i & 1;
         const int ybase = ystart + i * NB;
-        float gxs[NB], gys[NB], fcs[NB], tap[NB][4];
-        double tfx[NB], tfy[NB];
+        float gxs[NB], gys[NB], dts[NB], tap[NB][4], tfx[NB], tfy[NB], ctr[NB];
         bool in[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {  // independent loads of the batch
             const int y = ybase + b;
             in[b] = xin && y >= 0 && y < h && y < yend;
             const int yy = clampi(y, 0, h - 1);
-            const float* Frow = D.F + (size_t)yy * w;
-            gxs[b] = 0.5f * (__ldg(Frow + xr) - __ldg(Frow + xl));  // src/flow.cpp:230-235
-            gys[b] = 0.5f * (__ldg(D.F + (size_t)min(yy + 1, h - 1) * w + xc) -
-                             __ldg(D.F + (size_t)max(yy - 1, 0) * w + xc));
-            fcs[b] = __ldg(Frow + xc);
-            LevelTap t = level_tap(w, h, (double)((float)xc + fl[b].x), (double)((float)yy + fl[b].y));
+            const float* Fr = Fc + yy * w;
+            gxs[b] = 0.5f * (__ldg(Fr + dxr) - __ldg(Fr + dxl));  // src/flow.cpp:230-235
+            gys[b] = 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
+            ctr[b] = __ldg(Fr);
+            const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
             tfx[b] = t.fx;
             tfy[b] = t.fy;
-            tap[b][0] = __ldg(D.T + (size_t)t.y0 * w + t.x0);
-            tap[b][1] = __ldg(D.T + (size_t)t.y0 * w + t.x1);
-            tap[b][2] = __ldg(D.T + (size_t)t.y1 * w + t.x0);
-            tap[b][3] = __ldg(D.T + (size_t)t.y1 * w + t.x1);
+            const float* p = T + t.off;
+            tap[b][0] = __ldg(p);
+            tap[b][1] = __ldg(p + t.dx);
+            tap[b][2] = __ldg(p + t.dy);
+            tap[b][3] = __ldg(p + (t.dy + t.dx));
         }
         if (i + 1 < nbat) {
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
-                fl[b] = D.fin[(size_t)clampi(ybase + NB + b, 0, h - 1) * w + xc];
+            for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + NB + b)];
         }
-        float dts[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             LevelTap t;
             t.fx = tfx[b];
             t.fy = tfy[b];
-            dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - fcs[b];
+            dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - ctr[b];
         }
         if (i >= 2) bar_sync(3 + buf);  // consumers released this buffer
         double* st = stage + (size_t)buf * lk_stage_doubles<FULL>();
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-            const float gx = in[b] ? gxs[b] : 0.f;
-            const float gy = in[b] ? gys[b] : 0.f;
-            const float dt = in[b] ? dts[b] : 0.f;
-            const int slot = (ybase + b - ystart) % K;
-            float* rs = ring + ((size_t)slot * LK_IW + c) * 3;
-            const double ogx = rs[0], ogy = rs[1], odt = rs[2];
-            rs[0] = gx;
-            rs[1] = gy;
-            rs[2] = dt;
-            const double ix = gx, iy = gy, tt = dt;
+            const double ix = in[b] ? gxs[b] : 0.f, iy = in[b] ? gys[b] : 0.f;
+            const double tt = in[b] ? dts[b] : 0.f;
             if (FULL) {
+                float* rs = ringf + (slot * LK_IW + c) * 3;
+                const double ogx = rs[0], ogy = rs[1], odt = rs[2];
+                rs[0] = (float)ix;
+                rs[1] = (float)iy;
+                rs[2] = (float)tt;
                 V[0] = (V[0] + ix * ix) - ogx * ogx;
                 V[1] = (V[1] + ix * iy) - ogx * ogy;
                 V[2] = (V[2] + iy * iy) - ogy * ogy;
+                V[3] = (V[3] + ix * tt) - ogx * odt;
+                V[4] = (V[4] + iy * tt) - ogy * odt;
+            } else {
+                double2* rp = ringd + (slot * LK_IW + c);
+                const double2 o = *rp;
+                const double px = ix * tt, py = iy * tt;
+                *rp = make_double2(px, py);
+                V[0] = (V[0] + px) - o.x;
+                V[1] = (V[1] + py) - o.y;
             }
-            V[NQ - 2] = (V[NQ - 2] + ix * tt) - ogx * odt;
-            V[NQ - 1] = (V[NQ - 1] + iy * tt) - ogy * odt;
-            double* vb = st + (size_t)b * NQ * IWP + cc;
+            slot = slot + 1 == K ? 0 : slot + 1;
+            double* vb = st + b * NQ * IWP + cc;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) vb[q * IWP] = V[q];
         }
@@ -218,7 +248,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
         if (active) {
 #pragma unroll
             for (int o = 0; o < S; ++o) {
-                const size_t oi = (size_t)yo * w + min(x0 + cs + o, w - 1);
+                const int oi = yo * w + min(x0 + cs + o, w - 1);
                 fo[o] = D.fin[oi];
                 if (FULL)
                     okv[o] = D.okin[oi];
@@ -259,7 +289,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                     for (int q = 0; q < NQ; ++q)
                         s[q] = (s[q] + vb[q * IWP + ia]) - vb[q * IWP + ib];
                 }
-                const size_t oi = (size_t)yo * w + (x0 + cs + o);
+                const int oi = yo * w + (x0 + cs + o);
                 float2 f = fo[o];
                 if (FULL) {
                     uint8_t ok = okv[o];
@@ -292,8 +322,8 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
 template <bool FULL>
 __global__ void __launch_bounds__(LK_THREADS, 2) k_lk_sweep(LkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float* ring = reinterpret_cast<float*>(smem);
-    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes(a.r));
+    void* ring = smem;
+    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes<FULL>(a.r));
     const LkDir& D = a.d[blockIdx.z];
     const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
     const int yo_end = min(y0 + a.th, a.h);

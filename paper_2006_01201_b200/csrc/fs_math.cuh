@@ -104,13 +104,21 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
     return true;
 }
 
-// (float)(acc / n) for a small positive integer n, as the reference rounds it
-// (double division, then float conversion), without a double division in
-// the common case: q = acc * (1/n) is within 1 ulp of the correctly rounded
-// quotient, so both convert to the same float unless q sits within a few ulp
-// of a float rounding boundary (the midpoint between two floats, low 29
-// mantissa bits == 2^28) — only then is the exact division taken.
-FS_HD float div_to_float(double acc, int n, double inv_n) {
+// (float)(acc / n) for a positive divisor n (a small integer count or a
+// bilinear weight sum), as the reference rounds it (double division, then
+// float conversion), without a double division in the common case:
+// q = acc * (1/n) is within 2 ulp of the correctly rounded quotient, so both
+// convert to the same float unless q sits within a few ulp of a float
+// rounding boundary (the midpoint between two floats, low 29 mantissa bits
+// == 2^28) — only then is the exact division taken.
+#ifdef __CUDA_ARCH__
+// kept out of line so the rare exact division is a branch, not a predicated
+// instruction sequence every thread issues
+__device__ __noinline__ double exact_div(double a, double b) { return a / b; }
+#else
+inline double exact_div(double a, double b) { return a / b; }
+#endif
+FS_HD float div_to_float(double acc, double n, double inv_n) {
     double q = acc * inv_n;
 #ifdef __CUDA_ARCH__
     long long bits = __double_as_longlong(q);
@@ -121,7 +129,7 @@ FS_HD float div_to_float(double acc, int n, double inv_n) {
     long long low = bits & ((1LL << 29) - 1);
     long long dist = low - (1LL << 28);
     if (dist < 0) dist = -dist;
-    if (dist <= 8) q = acc / n;
+    if (dist <= 8) q = exact_div(acc, n);
     return static_cast<float>(q);
 }
 
@@ -164,9 +172,12 @@ FS_HD void softmax_weights(double blend_l, double blend_r, double mag_rtol, doub
     double flow_r = 1.0 + coef * mag_ltor;
     double arg_l = k * blend_l * flow_l;
     double arg_r = k * blend_r * flow_r;
-    double m = arg_l < arg_r ? arg_r : arg_l;  // std::max
-    double el = exp(arg_l - m);
-    double er = exp(arg_r - m);
+    // std::max, then exp(arg - m): the larger argument gives exp(0) == 1
+    // exactly, so only the other exponential is evaluated
+    const bool r_max = arg_l < arg_r;
+    const double m = r_max ? arg_r : arg_l;
+    double el = r_max ? exp(arg_l - m) : 1.0;
+    double er = r_max ? 1.0 : exp(arg_r - m);
     sl = el / (el + er);
     sr = er / (el + er);
 }
