@@ -32,6 +32,8 @@
 // iterations form only the two mismatch sums and update by -(M^-1 b).
 // Products are exact in double (float x float) and all window sums are double,
 // agreeing with the reference's double prefix tables to ~1e-12 relative.
+#include <type_traits>
+
 #include "fs_device.cuh"
 
 namespace fs {
@@ -161,24 +163,35 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
         const int ybase = ystart + i * NB;
         float gxs[NB], gys[NB], dts[NB], tap[NB][4], tfx[NB], tfy[NB], ctr[NB];
         bool in[NB];
+        // batches whose rows (and rows -1, +1) lie inside the level and the
+        // band need no row clamps or row tests
+        auto loads = [&](auto inner_t) {
+            constexpr bool INNER = decltype(inner_t)::value;
+            const float* Fb = Fc + (INNER ? ybase * w : 0);
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {  // independent loads of the batch
-            const int y = ybase + b;
-            in[b] = xin && y >= 0 && y < h && y < yend;
-            const int yy = clampi(y, 0, h - 1);
-            const float* Fr = Fc + yy * w;
-            gxs[b] = 0.5f * (__ldg(Fr + dxr) - __ldg(Fr + dxl));  // src/flow.cpp:230-235
-            gys[b] = 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
-            ctr[b] = __ldg(Fr);
-            const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
-            tfx[b] = t.fx;
-            tfy[b] = t.fy;
-            const float* p = T + t.off;
-            tap[b][0] = __ldg(p);
-            tap[b][1] = __ldg(p + t.dx);
-            tap[b][2] = __ldg(p + t.dy);
-            tap[b][3] = __ldg(p + (t.dy + t.dx));
-        }
+            for (int b = 0; b < NB; ++b) {  // independent loads of the batch
+                const int y = ybase + b;
+                in[b] = INNER ? xin : (xin && y >= 0 && y < h && y < yend);
+                const int yy = INNER ? y : clampi(y, 0, h - 1);
+                const float* Fr = INNER ? Fb + b * w : Fc + yy * w;
+                gxs[b] = 0.5f * (__ldg(Fr + dxr) - __ldg(Fr + dxl));  // src/flow.cpp:230-235
+                gys[b] = INNER ? 0.5f * (__ldg(Fr + w) - __ldg(Fr - w))
+                               : 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
+                ctr[b] = __ldg(Fr);
+                const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
+                tfx[b] = t.fx;
+                tfy[b] = t.fy;
+                const float* p = T + t.off;
+                tap[b][0] = __ldg(p);
+                tap[b][1] = __ldg(p + t.dx);
+                tap[b][2] = __ldg(p + t.dy);
+                tap[b][3] = __ldg(p + (t.dy + t.dx));
+            }
+        };
+        if (ybase >= 1 && ybase + NB <= h - 1 && ybase + NB <= yend)
+            loads(std::true_type{});
+        else
+            loads(std::false_type{});
         if (i + 1 < nbat) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + NB + b)];
