@@ -324,7 +324,8 @@ def main():
             traffic = json.load(f).get("lk_iter_dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"kernel": "k_lk_iter (fused LK iteration, both directions)", "bound": "hbm",
+    roofline = {"kernel": "k_lk_sweep<false> (LK later iteration, level 0, both directions)",
+                "bound": "hbm",
                 "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": round(lk["bytes"] / lk["launches"]),
