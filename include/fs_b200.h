@@ -192,6 +192,12 @@ typedef struct {
     double ms;
     double bytes;
 } fs_kernel_stat;
+/* Schedule diagnostics: one execution of the DAG (with the host copies when
+ * views/out are given) launched stream by stream with timing events at its
+ * schedule points; writes a
+ * JSON object {"label": ms since start} into json (cap bytes). */
+fs_status fs_plan_timeline(fs_plan plan, const uint8_t* const* views_rgba, uint8_t* out_rgba,
+                           void* stream, char* json, int cap);
 fs_status fs_plan_profile(fs_plan plan, void* stream, fs_kernel_stat* out, int max_out,
                           int* n_out, double* total_ms);
 void fs_plan_destroy(fs_plan plan);

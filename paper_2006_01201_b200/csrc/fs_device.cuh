@@ -76,20 +76,39 @@ struct PanoPlane {
 // earlier fold blended holds the value of the first view that covered it
 // (Area2 copies R, src/blender.cpp:69-71).  Lets a fold's partition, distance
 // transforms and (when its Area3 box is disjoint from every earlier one) its
-// L crop run without waiting for the earlier folds.
+// L crop run without waiting for the earlier folds.  `owner` holds, per
+// canvas pixel, the index of the first view covering it (0xFF: none; views
+// are claimed in fold order as they arrive), so the union test is one byte.
 constexpr int kMaxDagViews = 16;
 struct PanoViews {
     int n;
     ViewU8 v[kMaxDagViews];
+    const uint8_t* owner;
+    int w;
     __device__ __forceinline__ bool valid_at(int x, int y) const {
-        for (int m = 0; m < n; ++m)
-            if (v[m].valid_at(x, y)) return true;
-        return false;
+        return owner[(size_t)y * w + x] < n;
     }
     __device__ __forceinline__ float4 value_at(int x, int y) const {
-        for (int m = 0; m < n; ++m)
-            if (v[m].valid_at(x, y)) return v[m].value_at(x, y);
-        return make_float4(0.f, 0.f, 0.f, 0.f);
+        const int m = owner[(size_t)y * w + x];
+        return m < n ? v[m].value_at(x, y) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+};
+
+// L-crop source of a fold whose Area3 box meets earlier folds' boxes: a pixel
+// covered by two or more views before fold k was blended by the last of them,
+// so its value is the composed canvas (final once that fold composed — the
+// fold waits for the compose of the last earlier fold whose box meets its
+// own); every other valid pixel still holds its first covering view's value.
+struct PanoHybrid {
+    PanoViews pv;
+    PanoPlane plane;
+    __device__ __forceinline__ bool valid_at(int x, int y) const { return pv.valid_at(x, y); }
+    __device__ __forceinline__ float4 value_at(int x, int y) const {
+        const int m0 = pv.owner[(size_t)y * pv.w + x];
+        if (m0 >= pv.n) return make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int m = m0 + 1; m < pv.n; ++m)
+            if (pv.v[m].valid_at(x, y)) return plane.value_at(x, y);
+        return pv.v[m0].value_at(x, y);
     }
 };
 
@@ -192,6 +211,8 @@ namespace launch {
 void init();     // one-time kernel attributes (call before any graph capture)
 void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
+// owner[p] = k where view k is valid and no earlier view claimed p
+void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t);
 template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
 template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
 // pv_count of fold k = |view 0 valid| + sum of the Area2 counts of folds < k

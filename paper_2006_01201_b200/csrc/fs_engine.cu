@@ -425,8 +425,8 @@ template int fold_enqueue_pre<ViewF4, PanoPlane>(FoldWS<ViewF4>&, const PanoPlan
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoViews>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoViews&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
-template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoPlane>(
-    FoldWS<ViewU8>&, const PanoViews&, const PanoPlane&, const ViewU8&, int,
+template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoHybrid>(
+    FoldWS<ViewU8>&, const PanoViews&, const PanoHybrid&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoPlane, PanoPlane>(
     FoldWS<ViewU8>&, const PanoPlane&, const PanoPlane&, const ViewU8&, int,

@@ -606,6 +606,14 @@ __global__ void k_union_valid(Canvas cv, V view) {
     if (view.valid_at(x, y)) cv.valid[(size_t)y * cv.w + x] = 1;
 }
 
+__global__ void k_claim_owner(uint8_t* __restrict__ owner, int w, ViewU8 view, int k) {
+    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = view.rect.y0 + blockIdx.y;
+    if (x >= view.rect.x1()) return;
+    uint8_t* o = owner + (size_t)y * w + x;
+    if (*o == 0xFF && view.valid_at(x, y)) *o = (uint8_t)k;
+}
+
 __global__ void k_count_update(CanvasCount* cc, const FoldStats* st) {
     cc->valid_count += st->cnt2;
 }
@@ -744,6 +752,9 @@ template <class V>
 void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
+void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t s) {
+    k_claim_owner<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(owner, w, view, k);
+}
 void quantize(const Canvas& cv, uchar4* out, cudaStream_t s) {
     quantize_rect(cv, Rect{0, 0, cv.w, cv.h}, out, s);
 }
@@ -767,6 +778,8 @@ template void partition<ViewF4, PanoPlane>(const PanoPlane&, const ViewF4&, Fold
 template void crop_gray<ViewU8, PanoPlane>(const PanoPlane&, const ViewU8&, const Rect&, int,
                                            float*, float*, cudaStream_t);
 template void crop_gray<ViewU8, PanoViews>(const PanoViews&, const ViewU8&, const Rect&, int,
+                                           float*, float*, cudaStream_t);
+template void crop_gray<ViewU8, PanoHybrid>(const PanoHybrid&, const ViewU8&, const Rect&, int,
                                            float*, float*, cudaStream_t);
 template void crop_gray<ViewF4, PanoPlane>(const PanoPlane&, const ViewF4&, const Rect&, int,
                                            float*, float*, cudaStream_t);

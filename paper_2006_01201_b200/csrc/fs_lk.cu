@@ -308,9 +308,10 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                     uint8_t ok = okv[o];
                     const double A = s[0], B = s[1], Cc = s[2];
                     float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (lk_solve(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y)) {
+                    double inv_det;
+                    if (lk_solve_inv(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y,
+                                     inv_det)) {
                         ok = 1;
-                        const double inv_det = 1.0 / (A * Cc - B * B);
                         coef = make_float4((float)(Cc * inv_det), (float)(B * inv_det),
                                            (float)(A * inv_det), 1.f);
                     }

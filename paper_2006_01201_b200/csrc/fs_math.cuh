@@ -104,6 +104,7 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
     return true;
 }
 
+
 // (float)(acc / n) for a positive divisor n (a small integer count or a
 // bilinear weight sum), as the reference rounds it (double division, then
 // float conversion), without a double division in the common case:
@@ -131,6 +132,31 @@ FS_HD float div_to_float(double acc, double n, double inv_n) {
     if (dist < 0) dist = -dist;
     if (dist <= 8) q = exact_div(acc, n);
     return static_cast<float>(q);
+}
+
+// lk_solve with one division: inv_det = 1/det is returned (the level's stored
+// inverse tensor needs it) and (float)(num / det) is formed by div_to_float —
+// the flow update only sees the quotient rounded to float, so the result is
+// identical to lk_solve's.
+FS_HD bool lk_solve_inv(double a, double b, double c, double bx, double by, double eig_thresh,
+                        float flow_cap, float& dx, float& dy, double& inv_det) {
+    double tr = a + c;
+    double det = a * c - b * b;
+    double disc = tr * tr - 4.0 * det;
+    if (disc < 0.0) disc = 0.0;  // std::max(0.0, x)
+    double lambda_min = 0.5 * (tr - sqrt(disc));
+    if (lambda_min < eig_thresh) return false;
+    inv_det = 1.0 / det;
+    float ndx = dx + -div_to_float(c * bx - b * by, det, inv_det);
+    float ndy = dy + -div_to_float(a * by - b * bx, det, inv_det);
+    float mag = sqrtf(ndx * ndx + ndy * ndy);
+    if (mag > flow_cap) {
+        ndx *= flow_cap / mag;
+        ndy *= flow_cap / mag;
+    }
+    dx = ndx;
+    dy = ndy;
+    return true;
 }
 
 // src/flow.cpp:300-311 — final magnitude cap.

@@ -4,6 +4,7 @@
 // (partition, crop+gray, pyramid, bidirectional LK, distance transforms,
 // Code 1 blend, composition, 8-bit quantisation) from the views in HBM.
 #include <algorithm>
+#include <cstdio>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -34,13 +35,15 @@ struct fs_plan_s {
     std::string err;
     // DAG schedule (n <= kMaxDagViews): per-fold branch streams for the
     // partition-independent work, an ordered blend/compose chain on the main
-    // stream; crop_from_views[k]: fold k's L crop can be read from the views.
+    // stream; crop_wait[k]: the last earlier fold whose Area3 box meets fold
+    // k's (0: none, the L crop is read from the views alone).
     bool dag = false;
     std::vector<cudaStream_t> branch;
-    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt;
+    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt, ev_own;
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    std::vector<char> crop_from_views;
+    cudaStream_t h2d = nullptr, d2h = nullptr, own = nullptr;
+    uint8_t* owner = nullptr;  // first covering view per canvas pixel (PanoViews)
+    std::vector<int> crop_wait;
     // final_rects[k]: canvas rectangles no fold after k writes (k = 0: the
     // placement of view 0); quantised and read back as soon as fold k composed.
     std::vector<std::vector<Rect>> final_rects;
@@ -48,6 +51,9 @@ struct fs_plan_s {
     cudaGraph_t hgraph = nullptr;
     cudaGraphExec_t hexec = nullptr;
     std::vector<const void*> hkey;
+    // timeline capture (fs_plan_timeline): timing events at schedule points
+    bool tl = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> tl_marks;
 };
 
 namespace {
@@ -81,6 +87,8 @@ PanoViews views_before(const fs_plan_s* p, int k) {
     PanoViews pv{};
     pv.n = k;
     for (int m = 0; m < k; ++m) pv.v[m] = view_of(p, m);
+    pv.owner = p->owner;
+    pv.w = p->cw;
     return pv;
 }
 
@@ -106,6 +114,22 @@ struct HostIO {
 // views have landed — host transfers overlap the folds.
 int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullptr) {
     int launches = 0;
+    auto mark = [&](const std::string& label, cudaStream_t st) -> cudaEvent_t {
+        if (!p->tl) return nullptr;
+        cudaEvent_t e;
+        FS_CK(cudaEventCreate(&e));
+        FS_CK(cudaEventRecord(e, st));
+        p->tl_marks.push_back({label, e});
+        return e;
+    };
+    auto tl_event = [&](const std::string& label) -> cudaEvent_t {
+        if (!p->tl) return nullptr;
+        cudaEvent_t e;
+        FS_CK(cudaEventCreate(&e));
+        p->tl_marks.push_back({label, e});
+        return e;
+    };
+    mark("t0", s);
     const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
     const bool hin = io && io->views, hout = io && io->out;
     if (dag) {
@@ -117,6 +141,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
                                       (size_t)p->rects[k].w * p->rects[k].h * 4,
                                       cudaMemcpyDefault, p->h2d));
                 FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
+                mark("h2d_" + std::to_string(k), p->h2d);
             }
         }
     }
@@ -149,6 +174,16 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         return launches;
     }
     FS_CK(cudaEventRecord(p->ev_place, s));
+    mark("place", s);
+    // the owner plane: views claimed in fold order as they land
+    FS_CK(cudaStreamWaitEvent(p->own, p->ev_start, 0));
+    FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
+    for (int k = 0; k + 1 < p->n; ++k) {
+        if (hin) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
+        launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own);
+        ++launches;
+        FS_CK(cudaEventRecord(p->ev_own[k], p->own));
+    }
     // the read-back chain: quantise (and copy) every rectangle once final
     auto emit_final = [&](int k, cudaEvent_t after) {
         if (p->final_rects[k].empty()) return;
@@ -167,6 +202,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
                                         reinterpret_cast<const uint8_t*>(p->out) + off, pitch,
                                         (size_t)r.w * 4, r.h, cudaMemcpyDefault, p->d2h));
         }
+        mark("readback_" + std::to_string(k), p->d2h);
     };
     emit_final(0, p->ev_place);
     for (int k = 1; k < p->n; ++k) {
@@ -174,26 +210,34 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         ViewU8 v = view_of(p, k);
         cudaStream_t b = p->branch[k - 1];
         FS_CK(cudaStreamWaitEvent(b, hin ? p->ev_h2d[k] : p->ev_start, 0));
+        FS_CK(cudaStreamWaitEvent(b, p->ev_own[k - 1], 0));  // views < k claimed
         const PanoViews pv = views_before(p, k);
+        const std::string fk = std::to_string(k);
+        mark("fold" + fk + "_start", b);
         launches += fold_enqueue_pre(f, pv, v, b);
         FS_CK(cudaStreamWaitEvent(b, k == 1 ? p->ev_place : p->ev_cnt[k - 1], 0));
         launch::chain_count(f.st, k == 1 ? nullptr : p->folds[k - 2].st, p->cc, b);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_cnt[k], b));
-        if (p->crop_from_views[k]) {
-            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr);
-        } else {  // an earlier Area3 box overlaps: L is the composed panorama
-            FS_CK(cudaStreamWaitEvent(b, p->ev_compose[k - 1], 0));
-            launches += fold_enqueue_flow_edt(f, pv, plane, v, 3, p->fp, b, nullptr, nullptr);
+        cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
+        if (p->crop_wait[k] == 0) {
+            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1);
+        } else {  // blended pixels inside the box: after that fold's compose
+            FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
+            launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1);
         }
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
+        mark("fold" + fk + "_edt_end", b);
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
+        mark("fold" + fk + "_blend_start", s);
         launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
+        mark("fold" + fk + "_compose_end", s);
         emit_final(k, p->ev_compose[k]);
     }
     FS_CK(cudaEventRecord(p->ev_out, p->d2h));
     FS_CK(cudaStreamWaitEvent(s, p->ev_out, 0));
+    mark("end", s);
     FS_CK(cudaGetLastError());
     return launches;
 }
@@ -210,7 +254,8 @@ void capture(fs_plan_s* p, const HostIO* io, cudaGraph_t* graph, cudaGraphExec_t
         throw;
     }
     FS_CK(cudaStreamEndCapture(p->cap, graph));
-    FS_CK(cudaGraphInstantiate(exec, *graph, 0));
+    // kernel nodes keep the priority of the stream they were captured on
+    FS_CK(cudaGraphInstantiateWithFlags(exec, *graph, cudaGraphInstantiateFlagUseNodePriority));
     p->launches = launches;
 }
 
@@ -375,6 +420,7 @@ void layout_plan(fs_plan_s* p, Arena& a, const std::vector<Rect>& boxes) {
     p->cv.h = p->chh;
     p->cv.ch = 3;
     p->cc = a.take<CanvasCount>(1);
+    p->owner = p->dag ? a.take<uint8_t>(nc) : nullptr;
     p->folds.resize(p->n - 1);
     for (int k = 1; k < p->n; ++k) {
         bool full = p->folds[k - 1].full_domain;
@@ -415,34 +461,45 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         std::vector<Rect> boxes = views_rgba ? boxes_from_masks(p, views_rgba) : boxes_from_rects(p);
         // DAG: fold k's L crop may come straight from the views when no earlier
         // fold's Area3 box overlaps its own (those pixels hold the first
-        // covering view's value); partitions and distance transforms always can.
+        // covering view's value); otherwise it waits only for the compose of
+        // the last earlier fold whose box meets its own.  Partitions and
+        // distance transforms never wait.
         p->dag = n <= kMaxDagViews;
-        p->crop_from_views.assign(n, 0);
-        for (int k = 1; k < n; ++k) {
-            bool disjoint = true;
+        p->crop_wait.assign(n, 0);
+        for (int k = 1; k < n; ++k)
             for (int m = 1; m < k; ++m) {
                 Rect i = rect_inter(boxes[m], boxes[k]);
-                if (i.w > 0 && i.h > 0) disjoint = false;
+                if (i.w > 0 && i.h > 0) p->crop_wait[k] = m;
             }
-            p->crop_from_views[k] = disjoint;
-        }
         if (p->dag) {
             p->branch.assign(n - 1, nullptr);
             p->ev_branch.assign(n, nullptr);
             p->ev_compose.assign(n, nullptr);
-            for (auto& b : p->branch) FS_CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+            // earlier folds' branches get higher priority: the ordered
+            // blend/compose chain needs them first, and their canvas
+            // rectangles can be read back while later folds still run
+            int least = 0, greatest = 0;
+            FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            const int levels = least - greatest + 1;
+            for (int k = 0; k < n - 1; ++k) {
+                const int prio = greatest + (n - 1 > 1 ? k * (levels - 1) / (n - 2) : 0);
+                FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, prio));
+            }
             p->ev_h2d.assign(n, nullptr);
             p->ev_cnt.assign(n, nullptr);
+            p->ev_own.assign(n, nullptr);
             for (int k = 0; k < n; ++k) {
                 FS_CK(cudaEventCreateWithFlags(&p->ev_branch[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_compose[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_cnt[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_own[k], cudaEventDisableTiming));
             }
             for (cudaEvent_t* e : {&p->ev_start, &p->ev_place, &p->ev_out})
                 FS_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
             FS_CK(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
             FS_CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+            FS_CK(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
             plan_final_rects(p);
         }
         p->pano_bbox.assign(n, Rect{});
@@ -571,6 +628,55 @@ fs_status fs_plan_execute_host(fs_plan p, const uint8_t* const* views_rgba, uint
     });
 }
 
+fs_status fs_plan_timeline(fs_plan p, const uint8_t* const* views_rgba, uint8_t* out_rgba,
+                           void* stream, char* json, int cap) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        if (!p->dag) raise(FS_ERR_UNSUPPORTED, "plan: timeline needs the DAG schedule");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        HostIO io{views_rgba, out_rgba};
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t e = nullptr;
+        const int saved = p->launches;
+        p->tl = true;
+        p->tl_marks.clear();
+        auto cleanup = [&] {
+            p->tl = false;
+            for (auto& m : p->tl_marks) cudaEventDestroy(m.second);
+            p->tl_marks.clear();
+            if (e) cudaGraphExecDestroy(e);
+            if (g) cudaGraphDestroy(g);
+            p->launches = saved;
+        };
+        try {
+            // the same stream schedule as the graph, launched directly (timing
+            // events are not available on graph event-record nodes)
+            enqueue_all(p, s, true, (views_rgba || out_rgba) ? &io : nullptr);
+            FS_CK(cudaStreamSynchronize(s));
+            for (auto& m : p->tl_marks) cudaEventDestroy(m.second);
+            p->tl_marks.clear();
+            enqueue_all(p, s, true, (views_rgba || out_rgba) ? &io : nullptr);
+            FS_CK(cudaStreamSynchronize(s));
+            std::string js = "{";
+            for (size_t i = 0; i < p->tl_marks.size(); ++i) {
+                float ms = 0.f;
+                FS_CK(cudaEventElapsedTime(&ms, p->tl_marks[0].second, p->tl_marks[i].second));
+                char item[128];
+                std::snprintf(item, sizeof item, "%s\"%s\": %.4f", i ? ", " : "",
+                              p->tl_marks[i].first.c_str(), ms);
+                js += item;
+            }
+            js += "}";
+            if ((int)js.size() + 1 > cap) raise(FS_ERR_CONTRACT, "plan: timeline buffer too small");
+            std::memcpy(json, js.c_str(), js.size() + 1);
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
 fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_out, int* n_out,
                           double* total_ms) {
     return plan_guard([&] {
@@ -629,6 +735,9 @@ void fs_plan_destroy(fs_plan p) {
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_cnt)
         if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_own)
+        if (e) cudaEventDestroy(e);
+    if (p->own) cudaStreamDestroy(p->own);
     for (cudaEvent_t e : {p->ev_start, p->ev_place, p->ev_out})
         if (e) cudaEventDestroy(e);
     if (p->h2d) cudaStreamDestroy(p->h2d);

@@ -1,0 +1,29 @@
+#!/usr/bin/env python
+"""DAG schedule timeline of one C2 execution (device-resident and with host
+transfers): python tools/timeline.py [c2]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2006_01201_b200 as fs  # noqa: E402
+from paper_2006_01201_b200 import synthetic as S  # noqa: E402
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    lay = {"c1": S.c1_pair, "c2": S.c2_panorama, "c3": S.c3_large_parallax, "c4": S.c4_ring}[cfg](0)
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=lay.levels))
+    plan.execute_host(lay.views, None)
+    pin = [torch.from_numpy(v).pin_memory() for v in lay.views]
+    out = torch.empty((lay.canvas_h, lay.canvas_w, 4), dtype=torch.uint8).pin_memory()
+    dev = plan.timeline()
+    host = plan.timeline([t.data_ptr() for t in pin], out.data_ptr())
+    print(json.dumps({"device": dev, "host": host}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
