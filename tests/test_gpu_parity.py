@@ -397,6 +397,49 @@ def test_plan_matches_oracle(fs, oracle):
     plan2.close()
 
 
+def _skip_wait_layout(seed=4):
+    """Fold 3's Area3 box meets fold 1's box but not fold 2's, while fold 2
+    writes Area2 pixels inside fold 3's box (view 2's alpha hides its left
+    part except a bottom tab): the DAG crops fold 3's L right after compose 1,
+    concurrently with fold 2, from the canvas where blended and from the first
+    covering view elsewhere."""
+    W, H = 600, 400
+    scene = S.rgb_scene(H, W, seed)
+    rects = [(0, 0, 100, 400), (50, 0, 200, 100), (0, 150, 600, 200), (60, 60, 440, 140)]
+    views = []
+    for x, y, w, h in rects:
+        views.append(S.rgba(scene[y:y + h, x:x + w]))
+    a2 = views[2][..., 3]
+    a2[:150, :100] = 0  # view 2 meets view 0 only at rows 300-350 (canvas)
+    return S.Layout("skip-wait", W, H, views, [(x, y) for x, y, _, _ in rects], 3)
+
+
+def test_plan_crop_waits_for_last_meeting_box(fs, oracle):
+    lay = _skip_wait_layout()
+    params = fs.FlowParams(levels=3)
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params,
+                   views_rgba=lay.views)
+    b1, b2, b3 = (plan.fold_info(k)[0] for k in (1, 2, 3))
+
+    def meets(a, b):
+        return (min(a[0] + a[2], b[0] + b[2]) > max(a[0], b[0]) and
+                min(a[1] + a[3], b[1] + b[3]) > max(a[1], b[1]))
+    assert meets(b3, b1) and not meets(b3, b2), (b1, b2, b3)
+    fv = lay.float_views()
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    out = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    for _ in range(2):
+        plan.execute_host(lay.views, out)
+        assert np.array_equal(out[..., 3] == 255, ov == 1)
+        q = np.rint(np.clip(od, 0, 1) * 255).astype(np.int32)
+        diff = np.abs(out[..., :3].astype(np.int32) - q)[ov == 1]
+        assert diff.max() <= 1 and np.mean(diff == 0) >= 0.999
+    tl = plan.timeline()  # the schedule diagnostics run on this layout too
+    assert tl["end"] >= tl["fold3_compose_end"] >= tl["fold3_flow_start"] > 0
+    plan.close()
+
+
 def _grid_layout(seed=3):
     """2x2 views with a band across the middle: canvas rectangles become
     final after different folds, in both directions."""
