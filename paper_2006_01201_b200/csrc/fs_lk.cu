@@ -366,7 +366,7 @@ void lk_init() {
 int lk_tile_rows(int w, int h, int r, int ndir) {
     const int tw = LK_IW - 2 * r;
     const int cols = (w + tw - 1) / tw;
-    for (int th : {64, 32}) {
+    for (int th : {128, 64, 32}) {
         long ctas = (long)cols * ((h + th - 1) / th) * ndir;
         if (ctas >= 148L * 3) return th;
     }
