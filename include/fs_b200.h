@@ -148,6 +148,16 @@ fs_status fs_warp_constituents(const float* l, const uint8_t* valid_l, const flo
                                uint8_t* out_valid_l, float* out_r, uint8_t* out_valid_r,
                                void* stream);
 
+/* misalignment_score (pipeline.hpp:81-83; src/pipeline.cpp:309-396): the
+ * seam metric of StitchReport.  l, r: w x h x ch canvases (valid_l unused,
+ * as in the reference), label/counts: their partition.  Defaults in the
+ * reference: patch_radius 8, stride 32.  FS_ERR_EMPTY_REGION when no patch
+ * is textured. */
+fs_status fs_misalignment_score(const float* l, const uint8_t* valid_l, const float* r,
+                                const uint8_t* valid_r, int w, int h, int ch,
+                                const uint8_t* label, const int64_t* counts, int patch_radius,
+                                int stride, double* out, void* stream);
+
 /* ---- pipeline fold (pipeline.hpp:63-67) ---- */
 /* stitch_placed: images[i] is dims[2i] x dims[2i+1] x ch at offsets[2i],
  * offsets[2i+1]; valids may be NULL or hold NULL entries (all valid).  The

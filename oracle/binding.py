@@ -35,6 +35,7 @@ _SIGS = {
     "softmax_weights": (None, [D, D, D, D, D, D, P]),
     "blend_pair": (I, [P, P, P, P, I, I, I, P, P, P, P, D, D, P, P]),
     "stitch_placed": (I, [I, P, P, P, P, I, I, I, I, I, I, D, I, D, D, P, P]),
+    "misalignment_score": (I, [P, P, P, P, I, I, I, P, P, I, I, P]),
 }
 
 
@@ -206,6 +207,20 @@ class Oracle:
         self._ok(self._fn("compute_blend")(_p(label), _p(np.ascontiguousarray(counts, np.int64)),
                                            w, h, _p(out)), "compute_blend")
         return out
+
+    def misalignment_score(self, L, vL, R, vR, label, counts, patch_radius=8, stride=32):
+        """proj/src/pipeline.cpp:309-396 -> float score."""
+        L = np.ascontiguousarray(L, np.float32)
+        R = np.ascontiguousarray(R, np.float32)
+        h, w = L.shape[:2]
+        ch = 1 if L.ndim == 2 else L.shape[2]
+        out = np.zeros(1, np.float64)
+        vL = None if vL is None else np.ascontiguousarray(vL, np.uint8)
+        self._ok(self._fn("misalignment_score")(
+            _p(L), _p(vL), _p(R), _p(np.ascontiguousarray(vR, np.uint8)), w, h, ch,
+            _p(np.ascontiguousarray(label, np.uint8)), _p(np.ascontiguousarray(counts, np.int64)),
+            patch_radius, stride, _p(out)), "misalignment_score")
+        return float(out[0])
 
     def softmax_weights(self, bl, br, mrl, mlr, k=10.0, coef=0.05):
         out = np.empty(2, np.float64)

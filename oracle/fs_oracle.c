@@ -699,3 +699,120 @@ int fso_stitch_placed(int n, const float* const* imgs, const uint8_t* const* val
     free(cflr); free(cfrl); free(cvalid);
     return st;
 }
+
+/* ---- misalignment_score (proj/src/pipeline.cpp:213-396) ---------------- */
+
+typedef struct {
+    double mean, var;
+} patch_stats_t;
+
+/* proj/src/pipeline.cpp:220-233 */
+static patch_stats_t patch_stats(const float* g, int w, int cx, int cy, int r) {
+    double sum = 0.0, sum2 = 0.0;
+    int n = (2 * r + 1) * (2 * r + 1);
+    for (int j = cy - r; j <= cy + r; ++j)
+        for (int i = cx - r; i <= cx + r; ++i) {
+            double v = g[(size_t)j * w + i];
+            sum += v;
+            sum2 += v * v;
+        }
+    patch_stats_t s;
+    s.mean = sum / n;
+    s.var = sum2 / n - s.mean * s.mean;
+    return s;
+}
+
+/* proj/src/pipeline.cpp:235-245 */
+static double patch_ncc(const float* a, int ax, int ay, const float* b, int bx, int by, int w,
+                        int r, patch_stats_t sa, patch_stats_t sb) {
+    if (sa.var <= 1e-12 || sb.var <= 1e-12) return -2.0;
+    double cov = 0.0;
+    int n = (2 * r + 1) * (2 * r + 1);
+    for (int dj = -r; dj <= r; ++dj)
+        for (int di = -r; di <= r; ++di)
+            cov += ((double)a[(size_t)(ay + dj) * w + ax + di] - sa.mean) *
+                   ((double)b[(size_t)(by + dj) * w + bx + di] - sb.mean);
+    cov /= n;
+    return cov / sqrt(sa.var * sb.var);
+}
+
+/* proj/src/pipeline.cpp:247-256 — fixed tie-break */
+static int better_candidate(double score, int dx, int dy, double best_score, int best_dx,
+                            int best_dy) {
+    if (score > best_score + 1e-12) return 1;
+    if (score < best_score - 1e-12) return 0;
+    long n2 = (long)dx * dx + (long)dy * dy;
+    long b2 = (long)best_dx * best_dx + (long)best_dy * best_dy;
+    if (n2 != b2) return n2 < b2;
+    if (dx != best_dx) return dx < best_dx;
+    return dy < best_dy;
+}
+
+/* proj/src/pipeline.cpp:309-396.  The footprint tests use the reference's
+ * prefix-count semantics (every pixel of the patch in Area3 / valid in R),
+ * evaluated directly. */
+int fso_misalignment_score(const float* l, const uint8_t* l_valid, const float* r,
+                           const uint8_t* r_valid, int w, int h, int ch, const uint8_t* label,
+                           const int64_t* counts, int patch_radius, int stride, double* out) {
+    (void)l_valid;
+    if (counts[3] == 0) return FSO_CONTRACT;
+    if (patch_radius < 1 || stride < 1) return FSO_CONTRACT;
+    size_t n = (size_t)w * h;
+    float* gl = (float*)malloc(n * sizeof(float));
+    float* gr = (float*)malloc(n * sizeof(float));
+    fso_to_gray(l, w, h, ch, gl);
+    fso_to_gray(r, w, h, ch, gr);
+    const int rr = patch_radius, search = 2 * patch_radius;
+    double total = 0.0;
+    long matched = 0;
+    for (int cy = rr; cy < h - rr; cy += stride) {
+        double row_total = 0.0;
+        long row_matched = 0;
+        for (int cx = rr; cx < w - rr; cx += stride) {
+            int full = 1;
+            for (int j = cy - rr; j <= cy + rr && full; ++j)
+                for (int i = cx - rr; i <= cx + rr; ++i)
+                    if (label[(size_t)j * w + i] != 3) {
+                        full = 0;
+                        break;
+                    }
+            if (!full) continue;
+            patch_stats_t sl = patch_stats(gl, w, cx, cy, rr);
+            if (sl.var < 1e-4) continue;
+            double best_score = -2.0;
+            int best_dx = 0, best_dy = 0, found = 0;
+            for (int dy = -search; dy <= search; ++dy)
+                for (int dx = -search; dx <= search; ++dx) {
+                    int bx = cx + dx, by = cy + dy;
+                    if (bx - rr < 0 || bx + rr >= w || by - rr < 0 || by + rr >= h) continue;
+                    int rv = 1;
+                    for (int j = by - rr; j <= by + rr && rv; ++j)
+                        for (int i = bx - rr; i <= bx + rr; ++i)
+                            if (!r_valid[(size_t)j * w + i]) {
+                                rv = 0;
+                                break;
+                            }
+                    if (!rv) continue;
+                    patch_stats_t sr = patch_stats(gr, w, bx, by, rr);
+                    double ncc = patch_ncc(gl, cx, cy, gr, bx, by, w, rr, sl, sr);
+                    if (ncc < -1.5) continue;
+                    found = 1;
+                    if (better_candidate(ncc, dx, dy, best_score, best_dx, best_dy)) {
+                        best_score = ncc;
+                        best_dx = dx;
+                        best_dy = dy;
+                    }
+                }
+            if (!found) continue;
+            row_total += sqrt((double)best_dx * best_dx + (double)best_dy * best_dy);
+            ++row_matched;
+        }
+        total += row_total;
+        matched += row_matched;
+    }
+    free(gl);
+    free(gr);
+    if (matched == 0) return FSO_EMPTY;
+    *out = total / (double)matched;
+    return FSO_OK;
+}

@@ -60,6 +60,14 @@ void fso_softmax_weights(double blend_l, double blend_r, double mag_rtol, double
 int fso_blend_pair(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr, int w,
                    int h, int ch, const float* flow_lr, const float* flow_rl, const double* b,
                    const uint8_t* label, double k, double coef, float* out, uint8_t* out_valid);
+/* misalignment_score (proj/src/pipeline.cpp:309-396, with patch_stats,
+ * patch_ncc and better_candidate at :215-256): mean shift norm of the best
+ * NCC match of every textured (2r+1)^2 patch fully inside Area3, searched
+ * over +-2r in R.  l, r: w*h*ch images (r_valid: R's validity; L's validity
+ * is not read), label/counts: the partition.  *out = the score. */
+int fso_misalignment_score(const float* l, const uint8_t* l_valid, const float* r,
+                           const uint8_t* r_valid, int w, int h, int ch, const uint8_t* label,
+                           const int64_t* counts, int patch_radius, int stride, double* out);
 /* Fold over n placed images (proj/src/pipeline.cpp:140-212 without the
  * misalignment metrics, which never touch the panorama).  imgs[i] is
  * dims[2i] x dims[2i+1] x ch, placed at offsets[2i], offsets[2i+1].

@@ -338,6 +338,16 @@ int fsref_stitch_placed(int n, const float* const* imgs, const uint8_t* const* v
                                      iters, eps, smoothing, k, coef, out, out_valid, nullptr);
 }
 
+// proj/src/pipeline.cpp:309-396
+int fsref_misalignment_score(const float* l, const uint8_t* l_valid, const float* r,
+                             const uint8_t* r_valid, int w, int h, int ch, const uint8_t* label,
+                             const int64_t* counts, int patch_radius, int stride, double* out) {
+    return guarded([&] {
+        *out = misalignment_score(make_image(l, l_valid, w, h, ch), make_image(r, r_valid, w, h, ch),
+                                  make_partition(label, counts, w, h), patch_radius, stride);
+    });
+}
+
 // The reference's own stitch_placed (proj/src/pipeline.cpp:140-212), metrics
 // included; used to pin that the metric-free fold above yields the same canvas.
 int fsref_stitch_placed_full(int n, const float* const* imgs, const uint8_t* const* valids,

@@ -90,6 +90,7 @@ SIGNATURES = {
     "fs_blend_pair": (I, [P, P, P, P, I, I, I, P, P, P, P, C.POINTER(BlendParams), P, P, P]),
     "fs_feather_blend": (I, [P, P, P, P, I, I, I, P, P, P, P, P]),
     "fs_warp_constituents": (I, [P, P, P, P, I, I, I, P, P, P, P, P, P, P, P, P]),
+    "fs_misalignment_score": (I, [P, P, P, P, I, I, I, P, P, I, I, P, P]),
     "fs_stitch_placed": (I, [I, PP, PP, P, P, I, I, I, C.POINTER(FlowParams),
                              C.POINTER(BlendParams), P, P, P, P]),
     "fs_plan_create": (I, [C.POINTER(P), I, I, P, P, I, I, C.POINTER(FlowParams),

@@ -25,7 +25,8 @@ __all__ = [
     "compute_partition", "crop_overlap", "place_on_canvas", "build_pyramid", "dense_pyr_lk",
     "bidirectional_flow", "flow_magnitude", "embed_flow", "distance_transform",
     "compute_blend", "softmax_weights", "blend_pair", "feather_blend", "warp_constituents",
-    "stitch_placed", "set_thread_count", "thread_count", "resolved_thread_count",
+    "misalignment_score", "stitch_placed", "set_thread_count", "thread_count",
+    "resolved_thread_count",
 ]
 
 
@@ -448,6 +449,21 @@ def warp_constituents(L: ImageBuf, R: ImageBuf, flow_ltor: FlowField, flow_rtol:
                                       _p(_u8(partition.label)), _p(ol), _p(ovl), _p(orr),
                                       _p(ovr), None))
     return ImageBuf(ol, ovl), ImageBuf(orr, ovr)
+
+
+def misalignment_score(L: ImageBuf, R: ImageBuf, partition: RegionPartition,
+                       patch_radius: int = 8, stride: int = 32) -> float:
+    """pipeline.hpp:81-83 — mean shift norm of the best NCC match of every
+    textured patch inside Area3 (src/pipeline.cpp:309-396)."""
+    if (L.width != R.width or L.height != R.height or L.width != partition.label.shape[1]
+            or L.height != partition.label.shape[0]):
+        raise ContractError("misalignment_score: dimension mismatch")
+    out = C.c_double()
+    _check(N.lib.fs_misalignment_score(_p(L.data), _p(L.valid), _p(R.data), _p(R.valid), L.width,
+                                       L.height, L.channels, _p(_u8(partition.label)),
+                                       _p(np.ascontiguousarray(partition.counts, np.int64)),
+                                       patch_radius, stride, C.byref(out), None))
+    return out.value
 
 
 # ---- pipeline fold (pipeline.hpp:63-67) ----

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "fs_api_kernels.cuh"
+#include "fs_metrics.cuh"
 #include "fs_engine.cuh"
 
 using namespace fs;
@@ -486,6 +487,38 @@ fs_status fs_feather_blend(const float* l, const uint8_t* valid_l, const float* 
 }
 
 // blender.hpp:42-46 / src/blender.cpp:137-163
+// pipeline.hpp:81-83 / src/pipeline.cpp:309-396
+fs_status fs_misalignment_score(const float* l, const uint8_t* valid_l, const float* r,
+                                const uint8_t* valid_r, int w, int h, int ch,
+                                const uint8_t* label, const int64_t* counts, int patch_radius,
+                                int stride, double* out, void* stream) {
+    (void)valid_l;  // the reference reads only R's validity (src/pipeline.cpp:338)
+    return guarded([&] {
+        check_dims(w, h);
+        check_ch(ch);
+        int64_t c[4];
+        read_counts(counts, c);
+        if (c[3] == 0) raise(FS_ERR_CONTRACT, "misalignment_score: Area3 is empty");
+        if (patch_radius < 1 || stride < 1)
+            raise(FS_ERR_CONTRACT, "misalignment_score: patch_radius and stride must be >= 1");
+        if (patch_radius > metrics::misalign_max_radius())
+            raise(FS_ERR_UNSUPPORTED, "misalignment_score: patch_radius above the kernel's maximum");
+        Stage st(stream);
+        const size_t n = (size_t)w * h;
+        const int ngx = w - 2 * patch_radius > 0 ? (w - 2 * patch_radius + stride - 1) / stride : 0;
+        const int ngy = h - 2 * patch_radius > 0 ? (h - 2 * patch_radius + stride - 1) / stride : 0;
+        int* res = st.tmp<int>(3 * (size_t)std::max(1, ngx * ngy));
+        double* dout = st.tmp<double>(2);
+        metrics::misalign(st.in(l, n * ch), st.in(r, n * ch), st.in(valid_r, n), st.in(label, n), w,
+                          h, ch, patch_radius, stride, res, dout, st.s);
+        double hout[2];
+        st.read(hout, dout, 2);
+        st.finish();
+        if (hout[1] == 0.0) raise(FS_ERR_EMPTY_REGION, "misalignment_score: no textured patches");
+        *out = hout[0];
+    });
+}
+
 fs_status fs_warp_constituents(const float* l, const uint8_t* valid_l, const float* r,
                                const uint8_t* valid_r, int w, int h, int ch,
                                const float* flow_ltor, const float* flow_rtol,

@@ -328,6 +328,54 @@ def test_feather_and_warp_constituents(fs, oracle):
     assert np.all(F.data[a3] >= lo[a3]) and np.all(F.data[a3] <= hi[a3])
 
 
+# ---------------------------------------------------------------- seam metric
+def _misalign_cases():
+    v = np.ones((120, 160), np.uint8)
+    tex = S.value_noise(120, 160, 13).astype(np.float32)
+    yield tex, v, tex, v, v, v, 16
+    yield tex, v, np.roll(tex, 4, axis=1), v, v, v, 16
+    yield tex, v, np.roll(tex, (4, 3), axis=(0, 1)), v, v, v, 16
+    rng = np.random.RandomState(5)
+    L = _rgb(90, 130, 7)
+    R = np.roll(L, (2, -3), axis=(0, 1))
+    vl = np.ones((90, 130), np.uint8)
+    vl[:, 100:] = 0
+    vr = np.ones((90, 130), np.uint8)
+    vr[:, :20] = 0
+    vr[rng.rand(90, 130) > 0.995] = 0
+    yield L, vl, R, vr, vl, vr, 16
+    yield L, vl, R, vr, vl, vr, 32  # the reference's default stride
+
+
+@pytest.mark.parametrize("case", list(range(5)))
+def test_misalignment_score_bit_exact(fs, oracle, case):
+    L, vl, R, vr, ml, mr, stride = list(_misalign_cases())[case]
+    part = fs.compute_partition(fs.Mask(ml), fs.Mask(mr))
+    got = fs.misalignment_score(_img(fs, L, vl), _img(fs, R, vr), part, 8, stride)
+    exp = oracle.misalignment_score(L, vl, R, vr, part.label, part.counts, 8, stride)
+    assert got == exp
+
+
+def test_misalignment_score_errors_and_seam_reduction(fs, oracle):
+    v = np.ones((120, 160), np.uint8)
+    flat = np.full((120, 160), 0.2, np.float32)
+    part = fs.compute_partition(fs.Mask(v), fs.Mask(v))
+    with pytest.raises(fs.EmptyRegionError):  # test_pipeline.cpp:191-194
+        fs.misalignment_score(_img(fs, flat), _img(fs, flat), part, 8, 16)
+    with pytest.raises(fs.ContractError):
+        fs.misalignment_score(_img(fs, flat), _img(fs, flat), part, 0, 16)
+    # acceptance.cpp:265-294: warped constituents score far below the raw pair
+    L, vl, R, vr, part, b, flr, frl = _overlap_case(fs, oracle, 160, 120, 3)
+    ones = np.ones(part.label.shape, np.uint8)
+    wl, wr = fs.warp_constituents(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
+                                  fs.FlowField(frl, ones), b, part)
+    before = fs.misalignment_score(_img(fs, L, vl), _img(fs, R, vr), part, 8, 16)
+    after = fs.misalignment_score(wl, wr, part, 8, 16)
+    assert before == oracle.misalignment_score(L, vl, R, vr, part.label, part.counts, 8, 16)
+    assert after == oracle.misalignment_score(wl.data, wl.valid, wr.data, wr.valid, part.label,
+                                              part.counts, 8, 16)
+
+
 # ---------------------------------------------------------------- fold
 def _fold_both(fs, oracle, lay, params):
     fv = lay.float_views()

@@ -273,3 +273,53 @@ def test_fold_identity_and_coverage(fso):
     exp = np.zeros((50, 120), np.uint8)
     exp[:40, :100] = 1
     assert np.array_equal(ov, exp)
+
+
+# ---------------------------------------------------------------- misalignment_score
+def _tex(h, w, seed, ch=1):
+    if ch == 1:
+        return S.value_noise(h, w, seed).astype(np.float32)
+    return np.stack([S.value_noise(h, w, seed + d) for d in (0, 101, 202)], -1).astype(np.float32)
+
+
+def _misalign_cases():
+    v = np.ones((120, 160), np.uint8)
+    tex = _tex(120, 160, 13)
+    yield "identical", tex, v, tex, v, v, v
+    yield "shift4", tex, v, np.roll(tex, 4, axis=1), v, v, v
+    yield "diag", tex, v, np.roll(tex, (4, 3), axis=(0, 1)), v, v, v
+    rng = np.random.RandomState(5)
+    L = _tex(90, 130, 7, 3)
+    R = np.roll(L, (2, -3), axis=(0, 1))
+    vl = np.ones((90, 130), np.uint8)
+    vl[:, 100:] = 0
+    vr = np.ones((90, 130), np.uint8)
+    vr[:, :20] = 0
+    vr[rng.rand(90, 130) > 0.995] = 0  # holes disqualify candidates
+    yield "rgb_partial", L, vl, R, vr, vl, vr
+
+
+@pytest.mark.parametrize("case", list(range(4)))
+def test_misalignment_restatement_kats_and_reference(fso, case):
+    name, L, vl, R, vr, ml, mr = list(_misalign_cases())[case]
+    lab, cnt = fso.compute_partition(ml, mr)
+    a = fso.misalignment_score(L, vl, R, vr, lab, cnt, 8, 16)
+    # test_pipeline.cpp:175-196: identical -> 0, 4 px -> ~4, (3, 4) -> ~5
+    expect = {"identical": 0.0, "shift4": 4.0, "diag": 5.0}.get(name)
+    if expect is not None:
+        assert abs(a - expect) <= (0.0 if expect == 0.0 else 0.5)
+    if ref_available():
+        assert a == reference().misalignment_score(L, vl, R, vr, lab, cnt, 8, 16)
+
+
+def test_misalignment_flat_and_contract(fso):
+    from oracle.binding import OracleError
+    v = np.ones((120, 160), np.uint8)
+    flat = np.full((120, 160), 0.2, np.float32)
+    lab, cnt = fso.compute_partition(v, v)
+    with pytest.raises(OracleError) as e:  # EmptyRegionError
+        fso.misalignment_score(flat, v, flat, v, lab, cnt, 8, 16)
+    assert e.value.status == 2
+    with pytest.raises(OracleError) as e:  # ContractError: stride
+        fso.misalignment_score(flat, v, flat, v, lab, cnt, 8, 0)
+    assert e.value.status == 1
