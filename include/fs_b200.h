@@ -68,6 +68,13 @@ typedef struct {
     double flow_seconds;  /* device time of the pair's flow stage */
     double blend_seconds; /* device time of blend field + blend + compose */
     int32_t crop_box[4];  /* x0, y0, w, h of the Area3 bounding box */
+    /* misalignment_score (pipeline.cpp:184-199) of the raw pair and of the
+     * flow-warped constituents, patch radius 8, stride 32; present flags
+     * (bit 0 before, bit 1 after) are clear where the reference's optional
+     * stays empty (no textured patch). */
+    int32_t misalignment_present;
+    double misalignment_before;
+    double misalignment_after;
 } fs_pair_stats;
 
 const char* fs_last_error(void);

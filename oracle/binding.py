@@ -269,6 +269,16 @@ class Oracle:
         self._ok(st, "stitch_placed")
         return out, ov
 
+    def last_report_misalignment(self, max_pairs: int = 64) -> np.ndarray:
+        """(before, after) per pair of the last stitch_placed(full=True)
+        report of the compiled reference; NaN where the optional is empty."""
+        buf = np.full((max_pairs, 2), np.nan)
+        fn = self.lib.fsref_last_report_misalignment
+        fn.restype = I
+        fn.argtypes = [P, I]
+        n = fn(_p(buf), max_pairs)
+        return buf[:n]
+
 
 _cache = {}
 

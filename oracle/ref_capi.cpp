@@ -7,6 +7,7 @@
 // function named in its comment and copies the result back.  Exceptions map to
 // the FSO_* status codes (proj/include/flowstitch/errors.hpp:10-37).
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -84,6 +85,11 @@ int guarded(F&& fn) {
     } catch (const ContractError&) {
         return FSO_CONTRACT;
     }
+}
+
+StitchReport& last_report() {
+    static StitchReport rep;
+    return rep;
 }
 
 void export_flow(const FlowField& f, float* vec, uint8_t* valid) {
@@ -361,7 +367,22 @@ int fsref_stitch_placed_full(int n, const float* const* imgs, const uint8_t* con
         auto [pano, rep] = stitch_placed(make_placed(n, imgs, valids, dims, offsets, ch), cw, chh,
                                          flow_params(levels, radius, iters, eps, smoothing), bp);
         export_image(pano, out, out_valid);
+        last_report() = rep;
     });
+}
+
+// The seam metrics of the last fsref_stitch_placed_full report: per pair
+// (misalignment_before, misalignment_after), NaN where the optional is empty.
+int fsref_last_report_misalignment(double* out, int max_pairs) {
+    const auto& pairs = last_report().pairs;
+    int n = 0;
+    for (const auto& p : pairs) {
+        if (n == max_pairs) break;
+        out[2 * n] = p.misalignment_before ? *p.misalignment_before : NAN;
+        out[2 * n + 1] = p.misalignment_after ? *p.misalignment_after : NAN;
+        ++n;
+    }
+    return n;
 }
 
 } // extern "C"

@@ -52,7 +52,9 @@ class BlendParams(C.Structure):
 class PairStats(C.Structure):
     _fields_ = [("overlap_pixels", C.c_int64), ("mean_flow_mag_ltor", C.c_double),
                 ("mean_flow_mag_rtol", C.c_double), ("flow_seconds", C.c_double),
-                ("blend_seconds", C.c_double), ("crop_box", C.c_int32 * 4)]
+                ("blend_seconds", C.c_double), ("crop_box", C.c_int32 * 4),
+                ("misalignment_present", C.c_int32), ("misalignment_before", C.c_double),
+                ("misalignment_after", C.c_double)]
 
 
 class KernelStat(C.Structure):

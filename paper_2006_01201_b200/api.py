@@ -207,6 +207,8 @@ class PairStats:
     flow_seconds: float = 0.0
     blend_seconds: float = 0.0
     crop_box: Tuple[int, int, int, int] = (0, 0, 0, 0)
+    misalignment_before: Optional[float] = None  # raw L vs R over the overlap
+    misalignment_after: Optional[float] = None   # flow-warped constituents
 
 
 @dataclass
@@ -471,8 +473,8 @@ def stitch_placed(placed: Sequence[PlacedImage], canvas_width: int, canvas_heigh
                   flow_params: FlowParams = None,
                   blend_params: BlendParams = None) -> Tuple[ImageBuf, StitchReport]:
     """pipeline.hpp:64-67 — left-to-right fold, the running panorama plays L.
-    Runs device-resident; the report carries per-pair device timings (the
-    reference's misalignment metrics are not part of this path)."""
+    Runs device-resident; the report carries per-pair device timings and the
+    reference's seam metrics (misalignment before / after, bit-identical)."""
     import time
     flow_params = flow_params or FlowParams()
     blend_params = blend_params or BlendParams()
@@ -498,5 +500,7 @@ def stitch_placed(placed: Sequence[PlacedImage], canvas_width: int, canvas_heigh
     for s in stats:
         rep.pairs.append(PairStats(int(s.overlap_pixels), s.mean_flow_mag_ltor,
                                    s.mean_flow_mag_rtol, s.flow_seconds, s.blend_seconds,
-                                   tuple(int(v) for v in s.crop_box)))
+                                   tuple(int(v) for v in s.crop_box),
+                                   s.misalignment_before if s.misalignment_present & 1 else None,
+                                   s.misalignment_after if s.misalignment_present & 2 else None))
     return ImageBuf(out, ov), rep

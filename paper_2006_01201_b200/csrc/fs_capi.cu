@@ -147,7 +147,7 @@ void full_edt(Stage& st, const M& m0, const M* m1, int w, int h, int* out0, int*
 extern "C" {
 
 const char* fs_last_error(void) { return last_error_slot().c_str(); }
-int fs_abi_version(void) { return 1; }
+int fs_abi_version(void) { return 2; }
 
 int fs_device_available(void) {
     try {
@@ -550,7 +550,8 @@ fs_status fs_warp_constituents(const float* l, const uint8_t* valid_l, const flo
     });
 }
 
-// pipeline.hpp:63-67 / src/pipeline.cpp:140-212 (the fold; metrics excluded)
+// pipeline.hpp:63-67 / src/pipeline.cpp:140-212 (the fold; with stats, the
+// report's seam metrics too)
 fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* const* valids,
                            const int* dims, const int* offsets, int ch, int canvas_w,
                            int canvas_h, const fs_flow_params* flow, const fs_blend_params* blend,
@@ -628,9 +629,25 @@ fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* con
                 f.replan_edt();
                 fold_enqueue_flow_edt(f, pano, pano, v, ch, *flow, st.s, ev[0], ev[1]);
             }
+            // seam metric of the raw pair, before the canvas is composed
+            // (src/pipeline.cpp:184-187)
+            double mis[2][2] = {{0, 0}, {0, 0}};
+            int* mres = nullptr;
+            double* mout = nullptr;
+            if (stats) {
+                mres = st.tmp<int>(3 * std::max<size_t>(1, metrics::fold_points(box, 8, 32)));
+                mout = st.tmp<double>(4);
+                metrics::misalign_fold(cv, v, box, nullptr, 8, 32, mres, mout, st.s);
+                f.wgray = st.tmp<float2>((size_t)box.w * box.h);
+                FS_CK(cudaMemsetAsync(f.wgray, 0xFF, sizeof(float2) * box.w * box.h, st.s));
+            }
             FS_CK(cudaEventRecord(ev[2], st.s));
             fold_enqueue_blend(f, cv, v, cc, *blend, st.s);
             FS_CK(cudaEventRecord(ev[3], st.s));
+            if (stats) {  // of the warped constituents (src/pipeline.cpp:192-199)
+                metrics::misalign_fold(cv, v, box, f.wgray, 8, 32, mres, mout + 2, st.s);
+                st.read(&mis[0][0], mout, 4);
+            }
             if (stats) {
                 api::mean_magnitude(f.fvec[0], (size_t)box.w * box.h, magscratch, st.s);
                 api::mean_magnitude(f.fvec[1], (size_t)box.w * box.h, magscratch + 257, st.s);
@@ -651,6 +668,9 @@ fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* con
                 ps.crop_box[1] = box.y0;
                 ps.crop_box[2] = box.w;
                 ps.crop_box[3] = box.h;
+                ps.misalignment_present = (mis[0][1] > 0 ? 1 : 0) | (mis[1][1] > 0 ? 2 : 0);
+                ps.misalignment_before = mis[0][1] > 0 ? mis[0][0] : 0.0;
+                ps.misalignment_after = mis[1][1] > 0 ? mis[1][0] : 0.0;
             }
             // grow the pano bbox by the placed rectangle
             int x0 = std::min(pb.x0, v.rect.x0), y0 = std::min(pb.y0, v.rect.y0);

@@ -234,7 +234,7 @@ template <class M>
 void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, cudaStream_t);
 template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
-                 const int*, const FoldStats*, double, double, float4*, cudaStream_t);
+                 const int*, const FoldStats*, double, double, float4*, float2*, cudaStream_t);
 template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);

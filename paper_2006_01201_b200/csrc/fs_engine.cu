@@ -402,7 +402,8 @@ int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCoun
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
         ProfScope ps("blend", 61.0 * f.box.area(), s);
         launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
-                            f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, s);
+                            f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, f.wgray,
+                            s);
     }
     {
         // view 4 + pano valid 1 in, rgb 16 + valid 1 out on the view; blended 16 in on Area3

@@ -109,6 +109,7 @@ struct FoldWS {
     uint8_t* fvalid[2] = {};
     EdtWS edt[2];
     float4* blended = nullptr;
+    float2* wgray = nullptr;  // (optional) gray of the warped constituents on Area3, box-indexed
     FoldStats* st = nullptr;
     void layout(Arena& a, const Rect& box, const Rect& pano_bbox, const Rect& view_rect,
                 const fs_flow_params& fp);

@@ -552,7 +552,7 @@ template <class V>
 __global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
                               const int* __restrict__ d2, const FoldStats* st, double k,
-                              double coef, float4* __restrict__ out) {
+                              double coef, float4* __restrict__ out, float2* __restrict__ wgray) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
@@ -579,6 +579,9 @@ __global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restr
         res[c] = (float)clampd(v, 0.0, 1.0);
     }
     out[o] = make_float4(res[0], res[1], res[2], 0.f);
+    if (wgray)  // gray of the warped constituents (warp_constituents, src/blender.cpp:150-158)
+        wgray[o] = cv.ch == 3 ? make_float2(gray3(cl[0], cl[1], cl[2]), gray3(cr[0], cr[1], cr[2]))
+                              : make_float2(cl[0], cr[0]);
 }
 
 template <class V>
@@ -738,9 +741,9 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, cudaStre
 template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
                  const float2* frl, const int* d1, const int* d2, const FoldStats* st, double k,
-                 double coef, float4* out, cudaStream_t s) {
+                 double coef, float4* out, float2* wgray, cudaStream_t s) {
     k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(cv, view, box, flr, frl, d1, d2, st,
-                                                             k, coef, out);
+                                                             k, coef, out, wgray);
 }
 template <class V>
 void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -798,10 +801,10 @@ template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
                              const FoldStats*, cudaStream_t);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, cudaStream_t);
+                                  double, float4*, float2*, cudaStream_t);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, cudaStream_t);
+                                  double, float4*, float2*, cudaStream_t);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

@@ -31,8 +31,9 @@ __device__ __forceinline__ bool better_candidate(double score, int dx, int dy, d
 
 template <class GL, class GR, class RV, class A3>
 __global__ void __launch_bounds__(MS_THREADS) k_misalign_point(GL gl, GR gr, RV rv, A3 a3, int w,
-                                                               int h, int rad, int stride,
-                                                               int ngx, int* __restrict__ res) {
+                                                               int h, int rad, int stride, int gx0,
+                                                               int gy0, int ngx,
+                                                               int* __restrict__ res) {
     extern __shared__ double sm[];
     const int P = 2 * rad + 1, NP = P * P, S = 2 * rad, RS = 2 * S + P, NW = 2 * S + 1;
     const int NC = NW * NW;
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_misalign_point(GL gl, GR gr, RV 
     uint8_t* rvb = reinterpret_cast<uint8_t*>(nc + NC);
     __shared__ double s_mean, s_var;
     const int t = threadIdx.x;
-    const int cx = rad + blockIdx.x * stride, cy = rad + blockIdx.y * stride;
+    const int cx = rad + (gx0 + (int)blockIdx.x) * stride, cy = rad + (gy0 + (int)blockIdx.y) * stride;
     int* out = res + 3 * (blockIdx.y * ngx + blockIdx.x);
     // the patch footprint must lie in Area3 (src/pipeline.cpp:367)
     int bad = 0;
@@ -185,6 +186,84 @@ size_t ms_smem(int rad) {
     return 8 * P * P + 9 * RS * RS + 8 * NW * NW;
 }
 
+// ---- sources of the fold's two calls (src/pipeline.cpp:184-199) ----------
+// L = the panorama before the fold, R = the placed view (place_on_canvas:
+// its data inside its rectangle, 0 outside), partition Area3 = both valid.
+__device__ __forceinline__ float gray_of(float4 v, int ch) {
+    return ch == 3 ? gray3(v.x, v.y, v.z) : v.x;
+}
+struct CanvasGray {
+    const float4* rgb;
+    int w, ch;
+    __device__ __forceinline__ float operator()(int x, int y) const {
+        return gray_of(rgb[(size_t)y * w + x], ch);
+    }
+};
+struct ViewGray {
+    ViewF4 v;
+    int ch;
+    __device__ __forceinline__ float operator()(int x, int y) const {
+        return v.rect.contains(x, y) ? gray_of(v.value_at(x, y), ch) : 0.f;
+    }
+};
+struct ViewValid {
+    ViewF4 v;
+    __device__ __forceinline__ bool operator()(int x, int y) const { return v.valid_at(x, y); }
+};
+struct FoldArea3 {
+    const uint8_t* pano_valid;
+    int w;
+    ViewF4 v;
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        return pano_valid[(size_t)y * w + x] && v.valid_at(x, y);
+    }
+};
+// warp_constituents (src/blender.cpp:137-163): on Area3 the warped colours
+// are the blend's two bilinear samples (their gray stored by k_blend_area3,
+// box-indexed); elsewhere the constituents are L and R unchanged.
+struct WarpGrayL {
+    const float2* wg;
+    Rect box;
+    __device__ __forceinline__ float operator()(int x, int y) const {
+        return box.contains(x, y) ? wg[(size_t)(y - box.y0) * box.w + (x - box.x0)].x : 0.f;
+    }
+};
+// Area3 of the fold read from the warp buffer (NaN-filled before the blend,
+// written on Area3 only): valid also after the canvas has been composed.
+struct WarpArea3 {
+    const float2* wg;
+    Rect box;
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        if (!box.contains(x, y)) return false;
+        const float v = wg[(size_t)(y - box.y0) * box.w + (x - box.x0)].x;
+        return v == v;
+    }
+};
+struct WarpGrayR {
+    const float2* wg;
+    Rect box;
+    WarpArea3 a3;
+    ViewGray vg;
+    __device__ __forceinline__ float operator()(int x, int y) const {
+        return a3(x, y) ? wg[(size_t)(y - box.y0) * box.w + (x - box.x0)].y : vg(x, y);
+    }
+};
+
+template <class GL, class GR, class RV, class A3>
+void launch_points(GL gl, GR gr, RV rv, A3 a3, int w, int h, int rad, int stride, int gx0,
+                   int gy0, int ngx, int ngy, int* res, cudaStream_t s) {
+    auto k = &k_misalign_point<GL, GR, RV, A3>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ms_smem(metrics::misalign_max_radius()));
+        configured = true;
+    }
+    if (ngx > 0 && ngy > 0)
+        k<<<dim3(ngx, ngy), MS_THREADS, ms_smem(rad), s>>>(gl, gr, rv, a3, w, h, rad, stride, gx0,
+                                                            gy0, ngx, res);
+}
+
 }  // namespace
 
 namespace metrics {
@@ -195,20 +274,42 @@ void misalign(const float* l, const float* r, const uint8_t* rvalid, const uint8
               int h, int ch, int rad, int stride, int* res, double* out, cudaStream_t s) {
     const int ngx = w - 2 * rad > 0 ? (w - 2 * rad + stride - 1) / stride : 0;
     const int ngy = h - 2 * rad > 0 ? (h - 2 * rad + stride - 1) / stride : 0;
-    static bool configured = false;
-    using K = decltype(&k_misalign_point<PlainGray, PlainGray, PlainValid, PlainArea3>);
-    K k = &k_misalign_point<PlainGray, PlainGray, PlainValid, PlainArea3>;
-    if (!configured) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)ms_smem(misalign_max_radius()));
-        configured = true;
-    }
-    if (ngx > 0 && ngy > 0)
-        k<<<dim3(ngx, ngy), MS_THREADS, ms_smem(rad), s>>>(PlainGray{l, w, ch}, PlainGray{r, w, ch},
-                                                            PlainValid{rvalid, w},
-                                                            PlainArea3{label, w}, w, h, rad,
-                                                            stride, ngx, res);
+    launch_points(PlainGray{l, w, ch}, PlainGray{r, w, ch}, PlainValid{rvalid, w},
+                  PlainArea3{label, w}, w, h, rad, stride, 0, 0, ngx, ngy, res, s);
     k_misalign_total<<<1, 1, 0, s>>>(res, ngx, ngy, out);
+}
+
+// Grid points whose footprint lies in the Area3 box: the others cannot have
+// their footprint in Area3 and add nothing (exact zeros) to the row sums.
+void fold_grid(const Rect& box, int rad, int stride, int& gx0, int& gy0, int& ngx, int& ngy) {
+    gx0 = (box.x0 + stride - 1) / stride;
+    gy0 = (box.y0 + stride - 1) / stride;
+    const int gx1 = box.x1() - 1 - 2 * rad >= 0 ? (box.x1() - 1 - 2 * rad) / stride : -1;
+    const int gy1 = box.y1() - 1 - 2 * rad >= 0 ? (box.y1() - 1 - 2 * rad) / stride : -1;
+    ngx = gx1 >= gx0 ? gx1 - gx0 + 1 : 0;
+    ngy = gy1 >= gy0 ? gy1 - gy0 + 1 : 0;
+}
+
+void misalign_fold(const Canvas& cv, const ViewF4& v, const Rect& box, const float2* wgray,
+                   int rad, int stride, int* res, double* out, cudaStream_t s) {
+    int gx0, gy0, ngx, ngy;
+    fold_grid(box, rad, stride, gx0, gy0, ngx, ngy);
+    const FoldArea3 a3{cv.valid, cv.w, v};
+    const ViewGray vg{v, cv.ch};
+    if (!wgray)
+        launch_points(CanvasGray{cv.rgb, cv.w, cv.ch}, vg, ViewValid{v}, a3, cv.w, cv.h, rad,
+                      stride, gx0, gy0, ngx, ngy, res, s);
+    else
+        launch_points(WarpGrayL{wgray, box}, WarpGrayR{wgray, box, WarpArea3{wgray, box}, vg},
+                      ViewValid{v}, WarpArea3{wgray, box}, cv.w, cv.h, rad, stride, gx0, gy0, ngx,
+                      ngy, res, s);
+    k_misalign_total<<<1, 1, 0, s>>>(res, ngx, ngy, out);
+}
+
+size_t fold_points(const Rect& box, int rad, int stride) {
+    int gx0, gy0, ngx, ngy;
+    fold_grid(box, rad, stride, gx0, gy0, ngx, ngy);
+    return (size_t)ngx * ngy;
 }
 
 }  // namespace metrics

@@ -85,6 +85,8 @@ std::pair<ImageBuf, StitchReport> stitch_placed(const std::vector<PlacedImage>& 
         ps.mean_flow_mag_rtol = s.mean_flow_mag_rtol;
         ps.flow_seconds = s.flow_seconds;
         ps.blend_seconds = s.blend_seconds;
+        if (s.misalignment_present & 1) ps.misalignment_before = s.misalignment_before;
+        if (s.misalignment_present & 2) ps.misalignment_after = s.misalignment_after;
         rep.pairs.push_back(ps);
     }
     rep.total_seconds =

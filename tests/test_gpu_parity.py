@@ -400,6 +400,31 @@ def test_stitch_placed_matches_oracle(fs, oracle, builder, kw):
     assert np.mean(np.abs(q_gpu - q_ref) <= 1) >= 0.999
 
 
+@pytest.mark.parametrize("builder", [S.small_strip, S.small_panorama])
+def test_stitch_report_seam_metrics_match_reference(fs, ref, builder):
+    """StitchReport.pairs[k].misalignment_before / after (pipeline.cpp:184-199)
+    against the compiled reference's own report.  The first pair's raw metric
+    reads only view 0 and view 1: bit-identical.  The others see panoramas
+    and warps built from flows that agree to ~1e-5 px: the best integer
+    shifts, hence the scores, agree (checked to 1e-9)."""
+    lay = builder(seed=3)
+    params = fs.FlowParams(levels=3)
+    fv = lay.float_views()
+    placed = [fs.PlacedImage(fs.ImageBuf(d, v), x, y) for (d, v), (x, y) in zip(fv, lay.offsets)]
+    pano, rep = fs.stitch_placed(placed, lay.canvas_w, lay.canvas_h, params)
+    ref.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets, lay.canvas_w,
+                      lay.canvas_h, params.astuple(), full=True)
+    exp = ref.last_report_misalignment()
+    assert len(exp) == len(rep.pairs)
+    got = np.array([[np.nan if p.misalignment_before is None else p.misalignment_before,
+                     np.nan if p.misalignment_after is None else p.misalignment_after]
+                    for p in rep.pairs])
+    assert np.array_equal(np.isnan(got), np.isnan(exp))
+    assert got[0, 0] == exp[0, 0]
+    ok = ~np.isnan(exp)
+    assert np.abs(got[ok] - exp[ok]).max() <= 1e-9, (got, exp)
+
+
 def test_stitch_errors(fs):
     img = fs.ImageBuf(_rgb(40, 40, 2), np.ones((40, 40), np.uint8))
     with pytest.raises(fs.EmptyRegionError):
