@@ -14,14 +14,18 @@ namespace flowstitch::b200 {
 // Device-resident version of flowstitch::stitch_placed
 // (proj/include/flowstitch/pipeline.hpp:64-67): the whole fold runs on the
 // GPU through fs_stitch_placed (include/fs_b200.h).  Same inputs, same
-// panorama and exceptions; the report carries overlap pixels, mean flow
-// magnitudes and device timings (the reference's misalignment metrics are
-// evaluation helpers, not part of the fold, and are left empty).  A distinct
-// name so it links next to the reference's pipeline.cpp.
+// panorama, report (overlap pixels, mean flow magnitudes, misalignment
+// before / after; timings are device times) and exceptions.  Distinct names
+// so they link next to the reference's pipeline.cpp.
 std::pair<ImageBuf, StitchReport> stitch_placed(const std::vector<PlacedImage>& placed,
                                                 int canvas_width, int canvas_height,
                                                 const FlowParams& flow_params,
                                                 const BlendParams& blend_params);
+
+// Device versions of the report helpers (pipeline.hpp:75-83), bit-identical.
+TranslationEstimate estimate_translation(const ImageBuf& A, const ImageBuf& B, int max_shift);
+double misalignment_score(const ImageBuf& L, const ImageBuf& R, const RegionPartition& partition,
+                          int patch_radius = 8, int stride = 32);
 
 }  // namespace flowstitch::b200
 

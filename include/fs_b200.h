@@ -165,6 +165,12 @@ fs_status fs_misalignment_score(const float* l, const uint8_t* valid_l, const fl
                                 const uint8_t* label, const int64_t* counts, int patch_radius,
                                 int stride, double* out, void* stream);
 
+/* estimate_translation (pipeline.hpp:69-77; src/pipeline.cpp:261-307):
+ * exhaustive integer-shift NCC of B against A (grayscale, ch == 1),
+ * |dx|, |dy| <= max_shift <= min(w, h) / 4. */
+fs_status fs_estimate_translation(const float* a, const float* b, int w, int h, int ch,
+                                  int max_shift, int* dx, int* dy, double* score, void* stream);
+
 /* ---- pipeline fold (pipeline.hpp:63-67) ---- */
 /* stitch_placed: images[i] is dims[2i] x dims[2i+1] x ch at offsets[2i],
  * offsets[2i+1]; valids may be NULL or hold NULL entries (all valid).  The

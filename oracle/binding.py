@@ -36,6 +36,7 @@ _SIGS = {
     "blend_pair": (I, [P, P, P, P, I, I, I, P, P, P, P, D, D, P, P]),
     "stitch_placed": (I, [I, P, P, P, P, I, I, I, I, I, I, D, I, D, D, P, P]),
     "misalignment_score": (I, [P, P, P, P, I, I, I, P, P, I, I, P]),
+    "estimate_translation": (I, [P, P, I, I, I, I, P, P, P]),
 }
 
 
@@ -221,6 +222,17 @@ class Oracle:
             _p(np.ascontiguousarray(label, np.uint8)), _p(np.ascontiguousarray(counts, np.int64)),
             patch_radius, stride, _p(out)), "misalignment_score")
         return float(out[0])
+
+    def estimate_translation(self, A, B, max_shift):
+        """proj/src/pipeline.cpp:261-307 -> (dx, dy, score)."""
+        A = np.ascontiguousarray(A, np.float32)
+        B = np.ascontiguousarray(B, np.float32)
+        h, w = A.shape[:2]
+        ch = 1 if A.ndim == 2 else A.shape[2]
+        dx, dy, sc = C.c_int(), C.c_int(), C.c_double()
+        self._ok(self._fn("estimate_translation")(_p(A), _p(B), w, h, ch, max_shift, C.byref(dx),
+                                                  C.byref(dy), C.byref(sc)), "estimate_translation")
+        return dx.value, dy.value, sc.value
 
     def softmax_weights(self, bl, br, mrl, mlr, k=10.0, coef=0.05):
         out = np.empty(2, np.float64)

@@ -816,3 +816,45 @@ int fso_misalignment_score(const float* l, const uint8_t* l_valid, const float* 
     *out = total / (double)matched;
     return FSO_OK;
 }
+
+/* proj/src/pipeline.cpp:261-307 */
+int fso_estimate_translation(const float* a, const float* b, int w, int h, int ch, int max_shift,
+                             int* out_dx, int* out_dy, double* out_score) {
+    if (ch != 1) return FSO_CONTRACT;
+    if (max_shift > imin(w, h) / 4) return FSO_CONTRACT;
+    double best_score = -2.0;
+    int best_dx = 0, best_dy = 0, any = 0;
+    for (int dy = -max_shift; dy <= max_shift; ++dy)
+        for (int dx = -max_shift; dx <= max_shift; ++dx) {
+            int x0 = imax(0, -dx), x1 = imin(w, w - dx);
+            int y0 = imax(0, -dy), y1 = imin(h, h - dy);
+            if (x1 <= x0 || y1 <= y0) continue;
+            long n = (long)(x1 - x0) * (y1 - y0);
+            double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+            for (int y = y0; y < y1; ++y)
+                for (int x = x0; x < x1; ++x) {
+                    double va = a[(size_t)y * w + x];
+                    double vb = b[(size_t)(y + dy) * w + x + dx];
+                    sa += va;
+                    sb += vb;
+                    saa += va * va;
+                    sbb += vb * vb;
+                    sab += va * vb;
+                }
+            double va = saa / n - (sa / n) * (sa / n);
+            double vb = sbb / n - (sb / n) * (sb / n);
+            if (va <= 1e-12 || vb <= 1e-12) continue;
+            double ncc = (sab / n - (sa / n) * (sb / n)) / sqrt(va * vb);
+            any = 1;
+            if (better_candidate(ncc, dx, dy, best_score, best_dx, best_dy)) {
+                best_dx = dx;
+                best_dy = dy;
+                best_score = ncc;
+            }
+        }
+    if (!any) return FSO_EMPTY;
+    *out_dx = best_dx;
+    *out_dy = best_dy;
+    *out_score = best_score;
+    return FSO_OK;
+}

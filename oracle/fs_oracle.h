@@ -68,6 +68,10 @@ int fso_blend_pair(const float* l, const uint8_t* vl, const float* r, const uint
 int fso_misalignment_score(const float* l, const uint8_t* l_valid, const float* r,
                            const uint8_t* r_valid, int w, int h, int ch, const uint8_t* label,
                            const int64_t* counts, int patch_radius, int stride, double* out);
+/* estimate_translation (proj/src/pipeline.cpp:261-307): exhaustive integer
+ * shift NCC search of B against A (grayscale, ch must be 1). */
+int fso_estimate_translation(const float* a, const float* b, int w, int h, int ch, int max_shift,
+                             int* dx, int* dy, double* score);
 /* Fold over n placed images (proj/src/pipeline.cpp:140-212 without the
  * misalignment metrics, which never touch the panorama).  imgs[i] is
  * dims[2i] x dims[2i+1] x ch, placed at offsets[2i], offsets[2i+1].

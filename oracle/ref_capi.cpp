@@ -354,6 +354,19 @@ int fsref_misalignment_score(const float* l, const uint8_t* l_valid, const float
     });
 }
 
+// proj/src/pipeline.cpp:261-307
+int fsref_estimate_translation(const float* a, const float* b, int w, int h, int ch, int max_shift,
+                               int* dx, int* dy, double* score) {
+    return guarded([&] {
+        TranslationEstimate t =
+            estimate_translation(make_image(a, nullptr, w, h, ch), make_image(b, nullptr, w, h, ch),
+                                 max_shift);
+        *dx = t.dx;
+        *dy = t.dy;
+        *score = t.score;
+    });
+}
+
 // The reference's own stitch_placed (proj/src/pipeline.cpp:140-212), metrics
 // included; used to pin that the metric-free fold above yields the same canvas.
 int fsref_stitch_placed_full(int n, const float* const* imgs, const uint8_t* const* valids,

@@ -93,6 +93,7 @@ SIGNATURES = {
     "fs_feather_blend": (I, [P, P, P, P, I, I, I, P, P, P, P, P]),
     "fs_warp_constituents": (I, [P, P, P, P, I, I, I, P, P, P, P, P, P, P, P, P]),
     "fs_misalignment_score": (I, [P, P, P, P, I, I, I, P, P, I, I, P, P]),
+    "fs_estimate_translation": (I, [P, P, I, I, I, I, P, P, P, P]),
     "fs_stitch_placed": (I, [I, PP, PP, P, P, I, I, I, C.POINTER(FlowParams),
                              C.POINTER(BlendParams), P, P, P, P]),
     "fs_plan_create": (I, [C.POINTER(P), I, I, P, P, I, I, C.POINTER(FlowParams),

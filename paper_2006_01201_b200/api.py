@@ -25,7 +25,7 @@ __all__ = [
     "compute_partition", "crop_overlap", "place_on_canvas", "build_pyramid", "dense_pyr_lk",
     "bidirectional_flow", "flow_magnitude", "embed_flow", "distance_transform",
     "compute_blend", "softmax_weights", "blend_pair", "feather_blend", "warp_constituents",
-    "misalignment_score", "stitch_placed", "set_thread_count", "thread_count",
+    "misalignment_score", "estimate_translation", "TranslationEstimate", "stitch_placed", "set_thread_count", "thread_count",
     "resolved_thread_count",
 ]
 
@@ -451,6 +451,26 @@ def warp_constituents(L: ImageBuf, R: ImageBuf, flow_ltor: FlowField, flow_rtol:
                                       _p(_u8(partition.label)), _p(ol), _p(ovl), _p(orr),
                                       _p(ovr), None))
     return ImageBuf(ol, ovl), ImageBuf(orr, ovr)
+
+
+@dataclass
+class TranslationEstimate:
+    """pipeline.hpp:69-73"""
+    dx: int = 0
+    dy: int = 0
+    score: float = 0.0
+
+
+def estimate_translation(A: ImageBuf, B: ImageBuf, max_shift: int) -> TranslationEstimate:
+    """pipeline.hpp:75-77 — exhaustive integer-shift NCC search (grayscale)."""
+    if A.channels != 1 or B.channels != 1:
+        raise ContractError("estimate_translation: grayscale inputs required")
+    if A.width != B.width or A.height != B.height:
+        raise ContractError("estimate_translation: dimension mismatch")
+    dx, dy, sc = C.c_int(), C.c_int(), C.c_double()
+    _check(N.lib.fs_estimate_translation(_p(A.data), _p(B.data), A.width, A.height, 1, max_shift,
+                                         C.byref(dx), C.byref(dy), C.byref(sc), None))
+    return TranslationEstimate(dx.value, dy.value, sc.value)
 
 
 def misalignment_score(L: ImageBuf, R: ImageBuf, partition: RegionPartition,

@@ -519,6 +519,30 @@ fs_status fs_misalignment_score(const float* l, const uint8_t* valid_l, const fl
     });
 }
 
+// pipeline.hpp:69-77 / src/pipeline.cpp:261-307
+fs_status fs_estimate_translation(const float* a, const float* b, int w, int h, int ch,
+                                  int max_shift, int* dx, int* dy, double* score, void* stream) {
+    return guarded([&] {
+        check_dims(w, h);
+        if (ch != 1) raise(FS_ERR_CONTRACT, "estimate_translation: grayscale inputs required");
+        if (max_shift > std::min(w, h) / 4)
+            raise(FS_ERR_CONTRACT, "estimate_translation: max_shift too large for the image size");
+        if (max_shift < 0) raise(FS_ERR_EMPTY_REGION, "estimate_translation: no texture");
+        Stage st(stream);
+        const size_t n = (size_t)w * h;
+        double* ncc = st.tmp<double>((size_t)(2 * max_shift + 1) * (2 * max_shift + 1));
+        double* dout = st.tmp<double>(4);
+        metrics::translation(st.in(a, n), st.in(b, n), w, h, max_shift, ncc, dout, st.s);
+        double hout[4];
+        st.read(hout, dout, 4);
+        st.finish();
+        if (hout[0] == 0.0) raise(FS_ERR_EMPTY_REGION, "estimate_translation: no texture");
+        *dx = (int)hout[1];
+        *dy = (int)hout[2];
+        *score = hout[3];
+    });
+}
+
 fs_status fs_warp_constituents(const float* l, const uint8_t* valid_l, const float* r,
                                const uint8_t* valid_r, int w, int h, int ch,
                                const float* flow_ltor, const float* flow_rtol,

@@ -158,6 +158,61 @@ __global__ void k_misalign_total(const int* __restrict__ res, int ngx, int ngy, 
     out[1] = (double)matched;
 }
 
+// estimate_translation (src/pipeline.cpp:261-307): one thread per shift sums
+// its overlap in the reference's row-major order; one thread then picks the
+// winner in the reference's (dy, dx) order.
+__global__ void k_translation_shift(const float* __restrict__ a, const float* __restrict__ b,
+                                    int w, int h, int ms, double* __restrict__ ncc) {
+    const int nw = 2 * ms + 1;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nw * nw) return;
+    const int dx = c % nw - ms, dy = c / nw - ms;
+    const int x0 = max(0, -dx), x1 = min(w, w - dx);
+    const int y0 = max(0, -dy), y1 = min(h, h - dy);
+    double v = -3.0;
+    if (x1 > x0 && y1 > y0) {
+        const long long n = (long long)(x1 - x0) * (y1 - y0);
+        double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+        for (int y = y0; y < y1; ++y) {
+            const float* ra = a + (size_t)y * w;
+            const float* rb = b + (size_t)(y + dy) * w + dx;
+            for (int x = x0; x < x1; ++x) {
+                const double va = __ldg(ra + x), vb = __ldg(rb + x);
+                sa += va;
+                sb += vb;
+                saa += va * va;
+                sbb += vb * vb;
+                sab += va * vb;
+            }
+        }
+        const double va = saa / n - (sa / n) * (sa / n);
+        const double vb = sbb / n - (sb / n) * (sb / n);
+        if (!(va <= 1e-12 || vb <= 1e-12)) v = (sab / n - (sa / n) * (sb / n)) / sqrt(va * vb);
+    }
+    ncc[c] = v;
+}
+
+__global__ void k_translation_pick(const double* __restrict__ ncc, int ms, double* out) {
+    const int nw = 2 * ms + 1;
+    double best = -2.0;
+    int bdx = 0, bdy = 0, any = 0;
+    for (int c = 0; c < nw * nw; ++c) {
+        const double v = ncc[c];
+        if (v < -2.5) continue;
+        any = 1;
+        const int dx = c % nw - ms, dy = c / nw - ms;
+        if (better_candidate(v, dx, dy, best, bdx, bdy)) {
+            best = v;
+            bdx = dx;
+            bdy = dy;
+        }
+    }
+    out[0] = any;
+    out[1] = bdx;
+    out[2] = bdy;
+    out[3] = best;
+}
+
 struct PlainGray {
     const float* img;
     int w, ch;
@@ -277,6 +332,13 @@ void misalign(const float* l, const float* r, const uint8_t* rvalid, const uint8
     launch_points(PlainGray{l, w, ch}, PlainGray{r, w, ch}, PlainValid{rvalid, w},
                   PlainArea3{label, w}, w, h, rad, stride, 0, 0, ngx, ngy, res, s);
     k_misalign_total<<<1, 1, 0, s>>>(res, ngx, ngy, out);
+}
+
+void translation(const float* a, const float* b, int w, int h, int max_shift, double* ncc,
+                 double* out, cudaStream_t s) {
+    const int nc = (2 * max_shift + 1) * (2 * max_shift + 1);
+    k_translation_shift<<<(nc + 127) / 128, 128, 0, s>>>(a, b, w, h, max_shift, ncc);
+    k_translation_pick<<<1, 1, 0, s>>>(ncc, max_shift, out);
 }
 
 // Grid points whose footprint lies in the Area3 box: the others cannot have

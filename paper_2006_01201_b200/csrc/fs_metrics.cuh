@@ -18,5 +18,8 @@ void misalign(const float* l, const float* r, const uint8_t* rvalid, const uint8
 void misalign_fold(const Canvas& cv, const ViewF4& v, const Rect& box, const float2* wgray,
                    int rad, int stride, int* res, double* out, cudaStream_t s);
 size_t fold_points(const Rect& box, int rad, int stride);  // res holds 3 ints per point
+// estimate_translation: ncc scratch (2m+1)^2 doubles; out = {any, dx, dy, score}
+void translation(const float* a, const float* b, int w, int h, int max_shift, double* ncc,
+                 double* out, cudaStream_t s);
 }  // namespace metrics
 }  // namespace fs

@@ -27,6 +27,65 @@ void read_png_size(const std::string& path, int&, int&) {
 
 namespace b200 {
 
+namespace {
+void rethrow(fs_status st) {
+    if (st == FS_OK) return;
+    std::string msg = fs_last_error();
+    if (st == FS_ERR_EMPTY_REGION) throw EmptyRegionError(msg);
+    if (st == FS_ERR_LAYOUT) throw LayoutError(msg);
+    if (st == FS_ERR_CONTRACT || st == FS_ERR_UNSUPPORTED) throw ContractError(msg);
+    throw std::runtime_error("flowstitch-b200: " + msg);
+}
+std::vector<uint8_t> valid_of(const ImageBuf& img) {
+    std::vector<uint8_t> v(static_cast<size_t>(img.width()) * img.height());
+    for (int j = 0; j < img.height(); ++j)
+        for (int i = 0; i < img.width(); ++i)
+            v[static_cast<size_t>(j) * img.width() + i] = img.valid(i, j) ? 1 : 0;
+    return v;
+}
+}  // namespace
+
+// pipeline.hpp:75-77
+TranslationEstimate estimate_translation(const ImageBuf& A, const ImageBuf& B, int max_shift) {
+    if (A.channels() != 1 || B.channels() != 1)
+        throw ContractError("estimate_translation: grayscale inputs required");
+    if (A.width() != B.width() || A.height() != B.height())
+        throw ContractError("estimate_translation: dimension mismatch");
+    TranslationEstimate t;
+    rethrow(fs_estimate_translation(A.data().data(), B.data().data(), A.width(), A.height(), 1,
+                                    max_shift, &t.dx, &t.dy, &t.score, nullptr));
+    return t;
+}
+
+// pipeline.hpp:81-83
+double misalignment_score(const ImageBuf& L, const ImageBuf& R, const RegionPartition& partition,
+                          int patch_radius, int stride) {
+    if (L.width() != R.width() || L.height() != R.height() || L.width() != partition.width ||
+        L.height() != partition.height)
+        throw ContractError("misalignment_score: dimension mismatch");
+    std::vector<uint8_t> label(partition.label.size());
+    for (size_t k = 0; k < label.size(); ++k) label[k] = static_cast<uint8_t>(partition.label[k]);
+    int64_t counts[4];
+    for (int r = 0; r < 4; ++r) counts[r] = partition.counts[r];
+    std::vector<uint8_t> vl = valid_of(L), vr = valid_of(R);
+    double out = 0.0;
+    if (L.channels() == R.channels()) {
+        rethrow(fs_misalignment_score(L.data().data(), vl.data(), R.data().data(), vr.data(),
+                                      L.width(), L.height(), L.channels(), label.data(), counts,
+                                      patch_radius, stride, &out, nullptr));
+        return out;
+    }
+    // mixed channel counts: both to gray first (the reference grays each)
+    const size_t n = static_cast<size_t>(L.width()) * L.height();
+    std::vector<float> gl(n), gr(n);
+    rethrow(fs_to_gray(L.data().data(), L.width(), L.height(), L.channels(), gl.data(), nullptr));
+    rethrow(fs_to_gray(R.data().data(), R.width(), R.height(), R.channels(), gr.data(), nullptr));
+    rethrow(fs_misalignment_score(gl.data(), vl.data(), gr.data(), vr.data(), L.width(),
+                                  L.height(), 1, label.data(), counts, patch_radius, stride, &out,
+                                  nullptr));
+    return out;
+}
+
 std::pair<ImageBuf, StitchReport> stitch_placed(const std::vector<PlacedImage>& placed,
                                                 int canvas_width, int canvas_height,
                                                 const FlowParams& flow_params,
@@ -67,13 +126,7 @@ std::pair<ImageBuf, StitchReport> stitch_placed(const std::vector<PlacedImage>& 
     fs_status st = fs_stitch_placed(n, imgs.data(), vptr.data(), dims.data(), offs.data(), ch,
                                     canvas_width, canvas_height, &fp, &bp, pano.data().data(),
                                     pv.data(), stats.data(), nullptr);
-    if (st != FS_OK) {
-        std::string msg = fs_last_error();
-        if (st == FS_ERR_EMPTY_REGION) throw EmptyRegionError(msg);
-        if (st == FS_ERR_LAYOUT) throw LayoutError(msg);
-        if (st == FS_ERR_CONTRACT || st == FS_ERR_UNSUPPORTED) throw ContractError(msg);
-        throw std::runtime_error("flowstitch-b200: " + msg);
-    }
+    rethrow(st);
     for (int j = 0; j < canvas_height; ++j)
         for (int i = 0; i < canvas_width; ++i)
             pano.set_valid(i, j, pv[static_cast<size_t>(j) * canvas_width + i] != 0);

@@ -21,6 +21,17 @@ def test_reference_acceptance_suite_on_b200():
     assert "0 criterion failure(s)" in r.stdout
 
 
+@pytest.mark.gpu
+def test_dropin_check_against_reference_pipeline():
+    exe = os.path.join(ROOT, "paper_2006_01201_b200", "shim", "dropin_check")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_check not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 check failure(s)" in r.stdout
+
+
 def test_dropin_library_exports_reference_api():
     lib = os.path.join(ROOT, "paper_2006_01201_b200", "shim", "libflowstitch_b200.so")
     if not os.path.exists(lib):
@@ -32,5 +43,6 @@ def test_dropin_library_exports_reference_api():
                 "flowstitch::blend_pair(", "flowstitch::crop_overlap(",
                 "flowstitch::compute_partition(", "flowstitch::place_on_canvas(",
                 "flowstitch::to_gray(", "flowstitch::build_pyramid(",
-                "flowstitch::b200::stitch_placed("]:
+                "flowstitch::b200::stitch_placed(", "flowstitch::b200::misalignment_score(",
+                "flowstitch::b200::estimate_translation("]:
         assert sym in out, sym

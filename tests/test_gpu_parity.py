@@ -376,6 +376,27 @@ def test_misalignment_score_errors_and_seam_reduction(fs, oracle):
                                               part.counts, 8, 16)
 
 
+def test_estimate_translation_matches_oracle(fs, oracle):
+    a = S.value_noise(64, 64, 8).astype(np.float32)
+    b = np.roll(a, (-3, 5), axis=(0, 1))
+    rng = np.random.RandomState(3)
+    c = (a + 0.01 * rng.rand(64, 64)).astype(np.float32)
+    d = S.value_noise(96, 150, 2).astype(np.float32)
+    e = np.roll(d, (7, -11), axis=(0, 1))
+    for A, B, m in ((a, b, 8), (a, a, 4), (a, c, 6), (b, a, 16), (d, e, 20)):
+        t = fs.estimate_translation(_img(fs, A), _img(fs, B), m)
+        assert (t.dx, t.dy, t.score) == oracle.estimate_translation(A, B, m)
+    t = fs.estimate_translation(_img(fs, a), _img(fs, b), 8)  # test_pipeline.cpp:151-158
+    assert (t.dx, t.dy) == (5, -3) and t.score > 0.99
+    flat = np.full((64, 64), 0.5, np.float32)
+    with pytest.raises(fs.EmptyRegionError):
+        fs.estimate_translation(_img(fs, flat), _img(fs, flat), 4)
+    with pytest.raises(fs.ContractError):
+        fs.estimate_translation(_img(fs, a), _img(fs, a), 40)
+    with pytest.raises(fs.ContractError):
+        fs.estimate_translation(_img(fs, _rgb(64, 64, 1)), _img(fs, _rgb(64, 64, 1)), 4)
+
+
 # ---------------------------------------------------------------- fold
 def _fold_both(fs, oracle, lay, params):
     fv = lay.float_views()

@@ -323,3 +323,27 @@ def test_misalignment_flat_and_contract(fso):
     with pytest.raises(OracleError) as e:  # ContractError: stride
         fso.misalignment_score(flat, v, flat, v, lab, cnt, 8, 0)
     assert e.value.status == 1
+
+
+# ---------------------------------------------------------------- estimate_translation
+def test_estimate_translation_kats_and_reference(fso):
+    from oracle.binding import OracleError
+    a = S.value_noise(64, 64, 8).astype(np.float32)
+    b = np.roll(a, (-3, 5), axis=(0, 1))  # b(x + 5, y - 3) = a(x, y)
+    got = fso.estimate_translation(a, b, 8)  # test_pipeline.cpp:151-158
+    assert got[:2] == (5, -3) and got[2] > 0.99
+    same = fso.estimate_translation(a, a, 4)
+    assert same[:2] == (0, 0) and abs(same[2] - 1.0) < 1e-12
+    with pytest.raises(OracleError) as e:  # constant images: no texture
+        fso.estimate_translation(np.full((64, 64), 0.5, np.float32),
+                                 np.full((64, 64), 0.5, np.float32), 4)
+    assert e.value.status == 2
+    with pytest.raises(OracleError) as e:  # max_shift too large
+        fso.estimate_translation(a, a, 40)
+    assert e.value.status == 1
+    if ref_available():
+        ref = reference()
+        rng = np.random.RandomState(3)
+        c = (a + 0.01 * rng.rand(64, 64)).astype(np.float32)
+        for A, B, m in ((a, b, 8), (a, a, 4), (a, c, 6), (b, a, 16)):
+            assert fso.estimate_translation(A, B, m) == ref.estimate_translation(A, B, m)
