@@ -361,16 +361,24 @@ void lk_init() {
     lk_configured = true;
 }
 
-// th shrinks on small levels so the grid still covers the SMs (a CTA's sweep
-// is a serial chain of th + 2r rows).
 int lk_tile_rows(int w, int h, int r, int ndir) {
+    // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x 2.  Pick th
+    // minimising waves x rows per CTA (wave quantisation vs. halo rows).
     const int tw = LK_IW - 2 * r;
-    const int cols = (w + tw - 1) / tw;
-    for (int th : {128, 64, 32}) {
-        long ctas = (long)cols * ((h + th - 1) / th) * ndir;
-        if (ctas >= 148L * 3) return th;
+    const long cols = (w + tw - 1) / tw;
+    const long slots = 148L * 2;
+    int best = 16;
+    long best_cost = -1;
+    for (int th = 16; th <= 256; th += 8) {
+        const long ctas = cols * ((h + th - 1) / th) * ndir;
+        const long cost = ((ctas + slots - 1) / slots) * (th + 2 * r);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = th;
+        }
+        if (th >= h) break;
     }
-    return 16;
+    return best;
 }
 
 cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
