@@ -214,29 +214,31 @@ __device__ __forceinline__ float2 box3(const float2 (*tile)[TW], int ly, int lx,
     return make_float2(div_to_float(ax, n, kInvSmall[n]), div_to_float(ay, n, kInvSmall[n]));
 }
 
+// Block of SM_TX x SM_TY threads, output tile SM_OX x SM_OY: the first pass
+// covers the tile plus a 1-pixel ring — exactly one position per thread.
+constexpr int SM_OX = SM_TX - 2, SM_OY = SM_TY - 2;
+
 template <bool INNER>
-__device__ __forceinline__ void smooth_tile(const SmoothArgs& a, float2 (*src)[SM_TX + 4],
-                                            float2 (*p1)[SM_TX + 2]) {
+__device__ __forceinline__ void smooth_tile(const SmoothArgs& a, float2 (*src)[SM_OX + 4],
+                                            float2 (*p1)[SM_TX]) {
     const int d = blockIdx.z;
     const int w = a.w, h = a.h;
-    const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
-    const int tid = threadIdx.y * SM_TX + threadIdx.x;
+    const int bx = blockIdx.x * SM_OX, by = blockIdx.y * SM_OY;
+    const int tx = threadIdx.x, ty = threadIdx.y;
     const bool two = a.passes == 2;
     if (two) {
-        for (int t = tid; t < (SM_TY + 2) * (SM_TX + 2); t += SM_TX * SM_TY) {
-            const int ly = t / (SM_TX + 2), lx = t - ly * (SM_TX + 2);
-            const int gx = bx - 1 + lx, gy = by - 1 + ly;
-            float2 v = make_float2(0.f, 0.f);
-            if (INNER || (gx >= 0 && gx < w && gy >= 0 && gy < h))
-                v = box3<INNER, SM_TX + 4>(src, ly + 1, lx + 1, gx, gy, w, h);
-            p1[ly][lx] = v;
-        }
+        const int gx = bx - 1 + tx, gy = by - 1 + ty;
+        float2 v = make_float2(0.f, 0.f);
+        if (INNER || (gx >= 0 && gx < w && gy >= 0 && gy < h))
+            v = box3<INNER, SM_OX + 4>(src, ty + 1, tx + 1, gx, gy, w, h);
+        p1[ty][tx] = v;
         __syncthreads();
     }
-    const int gx = bx + threadIdx.x, gy = by + threadIdx.y;
+    if (tx >= SM_OX || ty >= SM_OY) return;
+    const int gx = bx + tx, gy = by + ty;
     if (gx >= w || gy >= h) return;
-    const float2 v = two ? box3<INNER, SM_TX + 2>(p1, threadIdx.y + 1, threadIdx.x + 1, gx, gy, w, h)
-                         : box3<INNER, SM_TX + 4>(src, threadIdx.y + 2, threadIdx.x + 2, gx, gy, w, h);
+    const float2 v = two ? box3<INNER, SM_TX>(p1, ty + 1, tx + 1, gx, gy, w, h)
+                         : box3<INNER, SM_OX + 4>(src, ty + 2, tx + 2, gx, gy, w, h);
     float vx = v.x, vy = v.y;
     const size_t o = (size_t)gy * w + gx;
     if (a.final_cap > 0.f) {
@@ -247,22 +249,22 @@ __device__ __forceinline__ void smooth_tile(const SmoothArgs& a, float2 (*src)[S
 }
 
 __global__ void __launch_bounds__(SM_TX* SM_TY, 3) k_smooth(SmoothArgs a) {
-    __shared__ float2 src[SM_TY + 4][SM_TX + 4];
-    __shared__ float2 p1[SM_TY + 2][SM_TX + 2];
+    __shared__ float2 src[SM_OY + 4][SM_OX + 4];
+    __shared__ float2 p1[SM_TY][SM_TX];
     const int d = blockIdx.z;
     const float2* fin = d ? a.fin[1] : a.fin[0];
     const int w = a.w, h = a.h;
-    const int bx = blockIdx.x * SM_TX, by = blockIdx.y * SM_TY;
-    for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_TY + 4) * (SM_TX + 4);
+    const int bx = blockIdx.x * SM_OX, by = blockIdx.y * SM_OY;
+    for (int t = threadIdx.y * SM_TX + threadIdx.x; t < (SM_OY + 4) * (SM_OX + 4);
          t += SM_TX * SM_TY) {
-        const int ly = t / (SM_TX + 4), lx = t - ly * (SM_TX + 4);
+        const int ly = t / (SM_OX + 4), lx = t - ly * (SM_OX + 4);
         const int gx = bx - 2 + lx, gy = by - 2 + ly;
         float2 v = make_float2(0.f, 0.f);
         if (gx >= 0 && gx < w && gy >= 0 && gy < h) v = fin[(size_t)gy * w + gx];
         src[ly][lx] = v;
     }
     __syncthreads();
-    if (bx >= 2 && by >= 2 && bx + SM_TX + 2 <= w && by + SM_TY + 2 <= h)
+    if (bx >= 2 && by >= 2 && bx + SM_OX + 2 <= w && by + SM_OY + 2 <= h)
         smooth_tile<true>(a, src, p1);
     else
         smooth_tile<false>(a, src, p1);
@@ -702,7 +704,7 @@ void downsample(const float* in0, const float* in1, float* out0, float* out1, in
 void init() { lk_init(); }
 
 void smooth(const SmoothArgs& a, cudaStream_t s) {
-    dim3 g((a.w + SM_TX - 1) / SM_TX, (a.h + SM_TY - 1) / SM_TY, a.ndir);
+    dim3 g((a.w + SM_OX - 1) / SM_OX, (a.h + SM_OY - 1) / SM_OY, a.ndir);
     k_smooth<<<g, dim3(SM_TX, SM_TY), 0, s>>>(a);
 }
 void finalize_flow(const SmoothArgs& a, cudaStream_t s) {

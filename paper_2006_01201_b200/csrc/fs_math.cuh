@@ -105,39 +105,18 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
 }
 
 
-// (float)(acc / n) for a positive divisor n (a small integer count or a
-// bilinear weight sum), as the reference rounds it (double division, then
-// float conversion), without a double division in the common case:
-// q = acc * (1/n) is within 2 ulp of the correctly rounded quotient, so both
-// convert to the same float unless q sits within a few ulp of a float
-// rounding boundary (the midpoint between two floats, low 29 mantissa bits
-// == 2^28) — only then is the exact division taken.
-#ifdef __CUDA_ARCH__
-// kept out of line so the rare exact division is a branch, not a predicated
-// instruction sequence every thread issues
-__device__ __noinline__ double exact_div(double a, double b) { return a / b; }
-#else
-inline double exact_div(double a, double b) { return a / b; }
-#endif
+// (float)(acc / n), as the reference rounds it (double division, then float
+// conversion).  The device double division is IEEE round-to-nearest (a
+// reciprocal seed plus DFMA refinement, ~10 instructions; its slow path only
+// for extreme exponents), so no cheaper exact form exists.  inv_n is unused
+// (kept for the call sites' signature).
 FS_HD float div_to_float(double acc, double n, double inv_n) {
-    double q = acc * inv_n;
-#ifdef __CUDA_ARCH__
-    long long bits = __double_as_longlong(q);
-#else
-    long long bits;
-    memcpy(&bits, &q, sizeof bits);
-#endif
-    long long low = bits & ((1LL << 29) - 1);
-    long long dist = low - (1LL << 28);
-    if (dist < 0) dist = -dist;
-    if (dist <= 8) q = exact_div(acc, n);
-    return static_cast<float>(q);
+    (void)inv_n;
+    return static_cast<float>(acc / n);
 }
 
-// lk_solve with one division: inv_det = 1/det is returned (the level's stored
-// inverse tensor needs it) and (float)(num / det) is formed by div_to_float —
-// the flow update only sees the quotient rounded to float, so the result is
-// identical to lk_solve's.
+// lk_solve that also returns inv_det = 1/det (the level's stored inverse
+// structure tensor needs it); the update is lk_solve's.
 FS_HD bool lk_solve_inv(double a, double b, double c, double bx, double by, double eig_thresh,
                         float flow_cap, float& dx, float& dy, double& inv_det) {
     double tr = a + c;
