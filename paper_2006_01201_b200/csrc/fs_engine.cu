@@ -351,8 +351,18 @@ int fold_enqueue_pre(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s)
 template <class V, class P, class PC>
 int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
-                          cudaEvent_t ev_flow1) {
+                          cudaEvent_t ev_flow1, cudaStream_t es, cudaEvent_t ev_fork,
+                          cudaEvent_t ev_join, bool with_edt) {
     int launches = 0;
+    // the distance transforms need only the masks and the fold's counts: with
+    // a second stream they run concurrently with the flow
+    cudaStream_t se = s;
+    if (!with_edt) es = nullptr;
+    if (es) {
+        FS_CK(cudaEventRecord(ev_fork, s));
+        FS_CK(cudaStreamWaitEvent(es, ev_fork, 0));
+        se = es;
+    }
     launch::check_box(f.st, f.box, s);
     {
         // pano rgb 16 + valid 1 + view 4 in, two gray planes 8 out
@@ -361,8 +371,21 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
     }
     launches += 2;
     if (ev_flow0) FS_CK(cudaEventRecord(ev_flow0, s));
+    if (es) launches += fold_enqueue_edt(f, pano, view, se);
     launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s);
     if (ev_flow1) FS_CK(cudaEventRecord(ev_flow1, s));
+    if (es) {
+        FS_CK(cudaEventRecord(ev_join, es));
+        FS_CK(cudaStreamWaitEvent(s, ev_join, 0));
+    } else if (with_edt) {
+        launches += fold_enqueue_edt(f, pano, view, s);
+    }
+    FS_CK(cudaGetLastError());
+    return launches;
+}
+
+template <class V, class P>
+int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s) {
     EdtJob<FoldMask<V, P>> j[2];
     for (int m = 0; m < 2; ++m) {
         const EdtPlan& E = f.ep[m];
@@ -389,9 +412,7 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
         ProfScope ps("edt", bytes, s);
         launch::edt(j[0], j[1], f.st, s);
     }
-    launches += 3;
-    FS_CK(cudaGetLastError());
-    return launches;
+    return 3;
 }
 
 template <class V>
@@ -425,16 +446,22 @@ template int fold_enqueue_pre<ViewF4, PanoPlane>(FoldWS<ViewF4>&, const PanoPlan
                                                  cudaStream_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoViews>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoViews&, const ViewU8&, int,
-    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
+    cudaEvent_t, cudaEvent_t, bool);
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoHybrid>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoHybrid&, const ViewU8&, int,
-    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
+    cudaEvent_t, cudaEvent_t, bool);
 template int fold_enqueue_flow_edt<ViewU8, PanoPlane, PanoPlane>(
     FoldWS<ViewU8>&, const PanoPlane&, const PanoPlane&, const ViewU8&, int,
-    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
+    cudaEvent_t, cudaEvent_t, bool);
 template int fold_enqueue_flow_edt<ViewF4, PanoPlane, PanoPlane>(
     FoldWS<ViewF4>&, const PanoPlane&, const PanoPlane&, const ViewF4&, int,
-    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+    const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
+    cudaEvent_t, cudaEvent_t, bool);
+template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoViews&, const ViewU8&,
+                                                 cudaStream_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t);
 template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,

@@ -119,11 +119,17 @@ struct FoldWS {
 template <class V, class P>
 int fold_enqueue_pre(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
 // check box, crop+gray (L from crop_src), pyramid, flow (both directions),
-// distance transforms (seed masks from `pano`'s validity)
+// distance transforms (seed masks from `pano`'s validity).  With `es` (and
+// two events) the distance transforms run on es, concurrently with the flow,
+// and s waits for them at the end; with_edt = false leaves them to the caller.
 template <class V, class P, class PC>
 int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
-                          cudaEvent_t ev_flow1);
+                          cudaEvent_t ev_flow1, cudaStream_t es = nullptr,
+                          cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
+                          bool with_edt = true);
+template <class V, class P>
+int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
 // Code 1 blend on Area3 + composition of the view onto the canvas
 template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,

@@ -39,7 +39,8 @@ struct fs_plan_s {
     // k's (0: none, the L crop is read from the views alone).
     bool dag = false;
     std::vector<cudaStream_t> branch;
-    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt, ev_own;
+    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt, ev_own, ev_efork, ev_ejoin;
+    std::vector<cudaStream_t> edt_stream;  // per fold: the distance transforms
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr, own = nullptr;
     uint8_t* owner = nullptr;  // first covering view per canvas pixel (PanoViews)
@@ -220,11 +221,20 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         ++launches;
         FS_CK(cudaEventRecord(p->ev_cnt[k], b));
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
+        cudaStream_t es = p->edt_stream[k - 1];
         if (p->crop_wait[k] == 0) {
-            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1);
+            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1, es,
+                                              p->ev_efork[k], p->ev_ejoin[k]);
         } else {  // blended pixels inside the box: after that fold's compose
+            // (the distance transforms need only the masks: fork them first)
+            FS_CK(cudaEventRecord(p->ev_efork[k], b));
+            FS_CK(cudaStreamWaitEvent(es, p->ev_efork[k], 0));
+            launches += fold_enqueue_edt(f, pv, v, es);
+            FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
             FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
-            launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1);
+            launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1,
+                                              nullptr, nullptr, nullptr, false);
+            FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
         mark("fold" + fk + "_edt_end", b);
@@ -481,19 +491,25 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             int least = 0, greatest = 0;
             FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
             const int levels = least - greatest + 1;
+            p->edt_stream.assign(n - 1, nullptr);
             for (int k = 0; k < n - 1; ++k) {
                 const int prio = greatest + (n - 1 > 1 ? k * (levels - 1) / (n - 2) : 0);
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, prio));
+                FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking, prio));
             }
             p->ev_h2d.assign(n, nullptr);
             p->ev_cnt.assign(n, nullptr);
             p->ev_own.assign(n, nullptr);
+            p->ev_efork.assign(n, nullptr);
+            p->ev_ejoin.assign(n, nullptr);
             for (int k = 0; k < n; ++k) {
                 FS_CK(cudaEventCreateWithFlags(&p->ev_branch[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_compose[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_cnt[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_own[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_efork[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_ejoin[k], cudaEventDisableTiming));
             }
             for (cudaEvent_t* e : {&p->ev_start, &p->ev_place, &p->ev_out})
                 FS_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -737,6 +753,12 @@ void fs_plan_destroy(fs_plan p) {
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_own)
         if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_efork)
+        if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_ejoin)
+        if (e) cudaEventDestroy(e);
+    for (auto st : p->edt_stream)
+        if (st) cudaStreamDestroy(st);
     if (p->own) cudaStreamDestroy(p->own);
     for (cudaEvent_t e : {p->ev_start, p->ev_place, p->ev_out})
         if (e) cudaEventDestroy(e);
