@@ -491,6 +491,26 @@ def test_plan_matches_oracle(fs, oracle):
     plan2.close()
 
 
+def test_plan_serial_schedule_many_views(fs, oracle):
+    """More views than the DAG schedule takes (kMaxDagViews = 16): the plan
+    folds serially on one stream; same panorama as the restatement."""
+    lay = S.small_strip(seed=6, n=18, vw=90, vh=72, step=60, parallax=2)
+    params = fs.FlowParams(levels=2, window_radius=4, iterations_per_level=2)
+    fv = lay.float_views()
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params)
+    out = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    plan.execute_host(lay.views, out)
+    assert np.array_equal(out[..., 3] == 255, ov == 1)
+    q = np.rint(np.clip(od, 0, 1) * 255).astype(np.int32)
+    diff = np.abs(out[..., :3].astype(np.int32) - q)[ov == 1]
+    assert diff.max() <= 1 and np.mean(diff == 0) >= 0.999
+    with pytest.raises(fs.FlowstitchError):
+        plan.timeline()  # the diagnostics need the DAG schedule
+    plan.close()
+
+
 def _skip_wait_layout(seed=4):
     """Fold 3's Area3 box meets fold 1's box but not fold 2's, while fold 2
     writes Area2 pixels inside fold 3's box (view 2's alpha hides its left
