@@ -48,7 +48,10 @@ struct LkCfg {
 constexpr int LK_IW = 128;  // producer threads = input columns per CTA
 constexpr int LK_THREADS = 2 * LK_IW;
 
-__host__ __device__ inline int lk_iwp(int iw) { return iw + (iw >> 3) + 1; }
+// Staged sums: plane [q][batch row][column] with an odd row stride, so the
+// consumers (consecutive threads = consecutive batch rows, then runs) read
+// without bank conflicts and with plain column offsets.
+__host__ __device__ inline int lk_iwp(int iw) { return iw + 1; }
 // Ring of the last 2r+1 rows per column, so the row leaving the window is
 // subtracted exactly: FULL keeps (Ix, Iy, It) as floats (five products are
 // re-formed), later iterations keep the two double products themselves.
@@ -136,7 +139,6 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     const bool xin = x >= 0 && x < w;
     const int xc = clampi(x, 0, w - 1);
     const int dxl = clampi(x - 1, 0, w - 1) - xc, dxr = clampi(x + 1, 0, w - 1) - xc;
-    const int cc = c + (c >> 3);
     const float* __restrict__ Fc = D.F + xc;
     const float2* __restrict__ Uc = D.fin + xc;
     const float* __restrict__ T = D.T;
@@ -229,9 +231,9 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 V[1] = (V[1] + py) - o.y;
             }
             slot = slot + 1 == K ? 0 : slot + 1;
-            double* vb = st + b * NQ * IWP + cc;
+            double* vb = st + b * IWP + c;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) vb[q * IWP] = V[q];
+            for (int q = 0; q < NQ; ++q) vb[q * NB * IWP] = V[q];
         }
         bar_arrive(1 + buf);  // batch staged
     }
@@ -247,12 +249,12 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
     const int IWP = lk_iwp(LK_IW);
     const int nruns = (a.tw + S - 1) / S;
     const int t = threadIdx.x - LK_IW;
-    const int b = t / nruns, run = t - b * nruns;  // NB * nruns <= 128 by construction
+    const int b = t % NB, run = t / NB;  // NB * nruns <= 128 by construction
     const int cs = run * S;
     for (int i = 0; i < nbat; ++i) {
         const int buf = i & 1;
         const int yo = ystart + i * NB + b - r;
-        const bool active = t < NB * nruns && yo >= y0 && yo < yo_end && x0 + cs < w;
+        const bool active = run < nruns && yo >= y0 && yo < yo_end && x0 + cs < w;
         const int nout = active ? min(min(S, a.tw - cs), w - (x0 + cs)) : 0;
         // prefetch the run's own flow / ok / coefficients before waiting
         float2 fo[S];
@@ -271,36 +273,33 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
         }
         bar_sync(1 + buf);
         if (active) {
-            const double* vb =
-                stage + (size_t)buf * lk_stage_doubles<FULL>() + (size_t)b * NQ * IWP;
+            const double* vb = stage + (size_t)buf * lk_stage_doubles<FULL>() + b * IWP + cs;
+            const int QS = NB * IWP;  // plane stride
             double s[NQ], s2[NQ];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) s[q] = s2[q] = 0.0;
-            int k = cs;
-            for (; k + 1 <= cs + 2 * r; k += 2) {  // two accumulators, no single chain
-                const int ci = k + (k >> 3), cj = (k + 1) + ((k + 1) >> 3);
+            int k = 0;
+            for (; k + 1 <= 2 * r; k += 2) {  // two accumulators, no single chain
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    s[q] += vb[q * IWP + ci];
-                    s2[q] += vb[q * IWP + cj];
+                    s[q] += vb[q * QS + k];
+                    s2[q] += vb[q * QS + k + 1];
                 }
             }
-            if (k <= cs + 2 * r) {
-                const int ci = k + (k >> 3);
+            if (k <= 2 * r) {
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) s[q] += vb[q * IWP + ci];
+                for (int q = 0; q < NQ; ++q) s[q] += vb[q * QS + k];
             }
 #pragma unroll
             for (int q = 0; q < NQ; ++q) s[q] += s2[q];
+            const double* va = vb + 2 * r;  // column entering the window at o
 #pragma unroll
             for (int o = 0; o < S; ++o) {
                 if (o >= nout) break;
                 if (o > 0) {
-                    const int ca = cs + 2 * r + o, cb = cs + o - 1;
-                    const int ia = ca + (ca >> 3), ib = cb + (cb >> 3);
 #pragma unroll
                     for (int q = 0; q < NQ; ++q)
-                        s[q] = (s[q] + vb[q * IWP + ia]) - vb[q * IWP + ib];
+                        s[q] = (s[q] + va[q * QS + o]) - vb[q * QS + o - 1];
                 }
                 const int oi = yo * w + (x0 + cs + o);
                 float2 f = fo[o];
