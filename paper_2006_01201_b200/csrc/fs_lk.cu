@@ -41,8 +41,14 @@ namespace fs {
 template <bool FULL>
 struct LkCfg {
     static constexpr int NQ = FULL ? 5 : 2;  // window sums carried
-    static constexpr int NB = 4;  // rows per staged batch
-    static constexpr int S = 4;   // outputs per horizontal run
+#ifndef LK_NB_FULL
+#define LK_NB_FULL 4
+#define LK_S_FULL 4
+#define LK_NB_ITER 4
+#define LK_S_ITER 4
+#endif
+    static constexpr int NB = FULL ? LK_NB_FULL : LK_NB_ITER;  // rows per staged batch
+    static constexpr int S = FULL ? LK_S_FULL : LK_S_ITER;     // outputs per horizontal run
 };
 
 constexpr int LK_IW = 128;  // producer threads = input columns per CTA
