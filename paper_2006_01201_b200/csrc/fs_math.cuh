@@ -80,6 +80,20 @@ FS_HD float up_combine(const UpTap& t, float f00, float f10, float f01, float f1
     return static_cast<float>(2.0 * l);
 }
 
+// src/flow.cpp:300-311 — final magnitude cap (and the per-update cap of
+// src/flow.cpp:283-287, the same expression).  The square root is taken only
+// when the squared norm is within 2% of cap^2: below that sqrtf(s) < cap for
+// certain, so the outcome is exactly the reference's test.
+FS_HD void final_cap(float cap, float& x, float& y) {
+    const float s = x * x + y * y;
+    if (!(s > 0.98f * (cap * cap))) return;
+    float mag = sqrtf(s);
+    if (mag > cap) {
+        x *= cap / mag;
+        y *= cap / mag;
+    }
+}
+
 // src/flow.cpp:267-291 — the 2x2 structure-tensor solve of one pixel.
 // Returns true (and the updated flow) when lambda_min >= threshold.
 FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double eig_thresh,
@@ -94,11 +108,7 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
     double uy = -(a * by - b * bx) / det;
     float ndx = dx + static_cast<float>(ux);
     float ndy = dy + static_cast<float>(uy);
-    float mag = sqrtf(ndx * ndx + ndy * ndy);
-    if (mag > flow_cap) {
-        ndx *= flow_cap / mag;
-        ndy *= flow_cap / mag;
-    }
+    final_cap(flow_cap, ndx, ndy);  // src/flow.cpp:283-287
     dx = ndx;
     dy = ndy;
     return true;
@@ -128,24 +138,12 @@ FS_HD bool lk_solve_inv(double a, double b, double c, double bx, double by, doub
     inv_det = 1.0 / det;
     float ndx = dx + -div_to_float(c * bx - b * by, det, inv_det);
     float ndy = dy + -div_to_float(a * by - b * bx, det, inv_det);
-    float mag = sqrtf(ndx * ndx + ndy * ndy);
-    if (mag > flow_cap) {
-        ndx *= flow_cap / mag;
-        ndy *= flow_cap / mag;
-    }
+    final_cap(flow_cap, ndx, ndy);  // src/flow.cpp:283-287
     dx = ndx;
     dy = ndy;
     return true;
 }
 
-// src/flow.cpp:300-311 — final magnitude cap.
-FS_HD void final_cap(float cap, float& x, float& y) {
-    float mag = sqrtf(x * x + y * y);
-    if (mag > cap) {
-        x *= cap / mag;
-        y *= cap / mag;
-    }
-}
 
 // src/image.cpp:87-97 — clamp-to-edge bilinear corners and weights.
 struct BiTap {
