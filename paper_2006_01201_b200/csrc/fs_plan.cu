@@ -44,6 +44,7 @@ struct fs_plan_s {
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr, own = nullptr;
     uint8_t* owner = nullptr;  // first covering view per canvas pixel (PanoViews)
+    FoldStats* hstats = nullptr;  // page-locked copy of the folds' statistics (fs_plan_check)
     std::vector<int> crop_wait;
     // final_rects[k]: canvas rectangles no fold after k writes (k = 0: the
     // placement of view 0); quantised and read back as soon as fold k composed.
@@ -571,15 +572,18 @@ fs_status fs_plan_execute(fs_plan p, void* stream) {
 fs_status fs_plan_check(fs_plan p) {
     return plan_guard([&] {
         FS_CK(cudaSetDevice(p->device));
-        std::vector<FoldStats> hs(p->folds.size());
+        if (!p->hstats) FS_CK(cudaMallocHost(&p->hstats, sizeof(FoldStats) * p->folds.size()));
         for (size_t k = 0; k < p->folds.size(); ++k)
-            FS_CK(cudaMemcpy(&hs[k], p->folds[k].st, sizeof(FoldStats), cudaMemcpyDeviceToHost));
-        for (size_t k = 0; k < hs.size(); ++k)
+            FS_CK(cudaMemcpyAsync(&p->hstats[k], p->folds[k].st, sizeof(FoldStats),
+                                  cudaMemcpyDeviceToHost, p->cap));
+        FS_CK(cudaStreamSynchronize(p->cap));
+        const FoldStats* hs = p->hstats;
+        for (size_t k = 0; k < p->folds.size(); ++k)
             if (hs[k].box_mismatch)
                 raise(FS_ERR_CONTRACT, "plan: the views' masks no longer produce the planned "
                                        "overlap of fold #" + std::to_string(k + 1));
         bool widened = false;
-        for (size_t k = 0; k < hs.size(); ++k)
+        for (size_t k = 0; k < p->folds.size(); ++k)
             if (hs[k].edt_fail && !p->folds[k].full_domain) {
                 p->folds[k].full_domain = true;
                 p->folds[k].replan_edt();
@@ -765,6 +769,7 @@ void fs_plan_destroy(fs_plan p) {
     if (p->h2d) cudaStreamDestroy(p->h2d);
     if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->arena) cudaFree(p->arena);
+    if (p->hstats) cudaFreeHost(p->hstats);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;
 }
