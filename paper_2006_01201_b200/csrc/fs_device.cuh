@@ -215,8 +215,6 @@ template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t);
 template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
 template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
-// pv_count of fold k = |view 0 valid| + sum of the Area2 counts of folds < k
-void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cudaStream_t);
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
 // pv_count = prev->pv_count + prev->cnt2 (prev: the previous fold), or cc for fold 1
 void chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc, cudaStream_t);

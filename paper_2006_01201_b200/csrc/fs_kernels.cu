@@ -114,18 +114,6 @@ __global__ void k_check_box(FoldStats* st, Rect planned) {
     if (!ok) st->box_mismatch = 1;
 }
 
-// |pano valid| before each fold: view 0's count plus the Area2 pixels every
-// earlier fold added (the union of the masks, src/pipeline.cpp:201-204).
-struct FoldStatsPtrs {
-    FoldStats* p[64];
-};
-__global__ void k_prefix_counts(FoldStatsPtrs st, int n, const CanvasCount* cc) {
-    unsigned long long c = cc->valid_count;
-    for (int k = 0; k < n; ++k) {
-        st.p[k]->pv_count = c;
-        c += st.p[k]->cnt2;
-    }
-}
 __global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
     st->pv_count = cc->valid_count;
 }
@@ -674,11 +662,6 @@ template <class V, class P>
 void partition(const P& pano, const V& view, FoldStats* st, cudaStream_t s) {
     k_partition<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
         pano, view, st);
-}
-void prefix_counts(FoldStats* const* st, int nfolds, const CanvasCount* cc, cudaStream_t s) {
-    FoldStatsPtrs p{};
-    for (int k = 0; k < nfolds && k < 64; ++k) p.p[k] = st[k];
-    k_prefix_counts<<<1, 1, 0, s>>>(p, nfolds < 64 ? nfolds : 64, cc);
 }
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t s) {
     k_snapshot_count<<<1, 1, 0, s>>>(st, cc);

@@ -82,9 +82,10 @@ __device__ __forceinline__ void bar_arrive(int id) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
 }
 
-// level_tap (fs_math.cuh) of the float position (i + dx, j + dy) of
-// src/flow.cpp:248: the clamp bounds are integers, so clamping, flooring and
-// x - floor(x) are exact in float — same taps and fractions as in double.
+// sample_level's clamp and taps (src/flow.cpp:100-111) at the float position
+// (i + dx, j + dy) of src/flow.cpp:248: the clamp bounds are integers, so
+// clamping, flooring and x - floor(x) are exact in float — the same taps and
+// fractions as the reference's double evaluation.
 struct TapF {
     int off, dx, dy;  // T offset of (x0, y0); +x / +y tap steps
     float fx, fy;
@@ -314,7 +315,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                     const double A = s[0], B = s[1], Cc = s[2];
                     float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
                     double inv_det;
-                    if (lk_solve_inv(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y,
+                    if (lk_solve(A, B, Cc, s[3], s[4], a.eig_thresh, a.flow_cap, f.x, f.y,
                                      inv_det)) {
                         ok = 1;
                         coef = make_float4((float)(Cc * inv_det), (float)(B * inv_det),

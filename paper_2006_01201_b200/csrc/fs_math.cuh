@@ -32,23 +32,12 @@ FS_HD float binom_tap(int t) {
     return t == 0 ? 6.f / 16 : ((t == 1 || t == -1) ? 4.f / 16 : 1.f / 16);
 }
 
-// src/flow.cpp:100-111 — bilinear weights of sample_level after the clamp.
+// src/flow.cpp:100-111 — sample_level's bilinear fractions after the clamp
+// (the taps themselves: level_tap_f, fs_lk.cu).
 struct LevelTap {
     int x0, y0, x1, y1;
     double fx, fy;
 };
-FS_HD LevelTap level_tap(int w, int h, double x, double y) {
-    x = clampd(x, 0.0, static_cast<double>(w - 1));
-    y = clampd(y, 0.0, static_cast<double>(h - 1));
-    LevelTap t;
-    t.x0 = static_cast<int>(x);
-    t.y0 = static_cast<int>(y);
-    t.x1 = imin(t.x0 + 1, w - 1);
-    t.y1 = imin(t.y0 + 1, h - 1);
-    t.fx = x - t.x0;
-    t.fy = y - t.y0;
-    return t;
-}
 FS_HD float level_combine(const LevelTap& t, float v00, float v10, float v01, float v11) {
     return static_cast<float>((1 - t.fx) * (1 - t.fy) * v00 + t.fx * (1 - t.fy) * v10 +
                               (1 - t.fx) * t.fy * v01 + t.fx * t.fy * v11);
@@ -94,27 +83,6 @@ FS_HD void final_cap(float cap, float& x, float& y) {
     }
 }
 
-// src/flow.cpp:267-291 — the 2x2 structure-tensor solve of one pixel.
-// Returns true (and the updated flow) when lambda_min >= threshold.
-FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double eig_thresh,
-                    float flow_cap, float& dx, float& dy) {
-    double tr = a + c;
-    double det = a * c - b * b;
-    double disc = tr * tr - 4.0 * det;
-    if (disc < 0.0) disc = 0.0;  // std::max(0.0, x)
-    double lambda_min = 0.5 * (tr - sqrt(disc));
-    if (lambda_min < eig_thresh) return false;
-    double ux = -(c * bx - b * by) / det;
-    double uy = -(a * by - b * bx) / det;
-    float ndx = dx + static_cast<float>(ux);
-    float ndy = dy + static_cast<float>(uy);
-    final_cap(flow_cap, ndx, ndy);  // src/flow.cpp:283-287
-    dx = ndx;
-    dy = ndy;
-    return true;
-}
-
-
 // (float)(acc / n), as the reference rounds it (double division, then float
 // conversion).  The device double division is IEEE round-to-nearest (a
 // reciprocal seed plus DFMA refinement, ~10 instructions; its slow path only
@@ -125,9 +93,10 @@ FS_HD float div_to_float(double acc, double n, double inv_n) {
     return static_cast<float>(acc / n);
 }
 
-// lk_solve that also returns inv_det = 1/det (the level's stored inverse
-// structure tensor needs it); the update is lk_solve's.
-FS_HD bool lk_solve_inv(double a, double b, double c, double bx, double by, double eig_thresh,
+// src/flow.cpp:267-291 — the 2x2 structure-tensor solve of one pixel.
+// Returns true (and the updated flow) when lambda_min >= threshold, with
+// inv_det = 1/det (the level's stored inverse structure tensor needs it).
+FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double eig_thresh,
                         float flow_cap, float& dx, float& dy, double& inv_det) {
     double tr = a + c;
     double det = a * c - b * b;
