@@ -93,6 +93,8 @@ int pyramid_depth(int w, int h, int levels) {
 
 // ---------------------------------------------------------------------------
 void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
+    if ((long long)w_ * h_ >= (1LL << 31))
+        raise(FS_ERR_UNSUPPORTED, "flow: overlap crops of 2^31 pixels or more are not supported");
     w = w_;
     h = h_;
     ndir = ndir_;
