@@ -511,6 +511,57 @@ def test_plan_serial_schedule_many_views(fs, oracle):
     plan.close()
 
 
+def _far_seed_layout(seed=8):
+    """Area3 (x 3..500) whose only Area1 seeds are a 3-px hole at its left
+    end, while the panorama's bounding box (view 0's rectangle, alpha 0 for
+    x >= 500) reaches x = 1000: the bounded distance-transform domain is
+    clipped on the right and its exactness certificate fails, so the fold
+    must fall back to the full domain."""
+    W, H = 1000, 40
+    scene = S.rgb_scene(H, W, seed)
+    v0 = S.rgba(scene[:, :1000])
+    v0[:, 500:, 3] = 0
+    v1 = S.rgba(np.roll(scene, 2, axis=1)[:, :500])
+    v1[:, :3, 3] = 0
+    return S.Layout("far-seed", W, H, [v0, v1], [(0, 0), (0, 0)], 2)
+
+
+def test_edt_certificate_fallback(fs, oracle):
+    lay = _far_seed_layout()
+    params = fs.FlowParams(levels=2, window_radius=4, iterations_per_level=2)
+    fv = lay.float_views()
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    # device fold (re-runs the fold's transforms on the full domain at once)
+    placed = [fs.PlacedImage(fs.ImageBuf(d, v), x, y) for (d, v), (x, y) in zip(fv, lay.offsets)]
+    pano, _ = fs.stitch_placed(placed, lay.canvas_w, lay.canvas_h, params)
+    assert np.array_equal(pano.valid, ov)
+    assert np.abs(pano.data - od).max() <= 1e-5
+    # planned fold: the check widens the plan and execute_host runs again;
+    # same kernels as the device fold, so its 8-bit canvas is that fold's
+    # panorama quantised (src/image.cpp:60-61: lroundf(v * 255.0f))
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params,
+                   views_rgba=lay.views)
+    import torch
+    plan.execute(0)
+    torch.cuda.synchronize()
+    with pytest.raises(fs.ContractError, match="widened"):  # the certificate failed
+        plan.check()
+    plan.execute(0)
+    torch.cuda.synchronize()
+    plan.check()  # the widened plan is exact
+    out = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    v32 = np.clip(pano.data, 0, 1).astype(np.float32) * np.float32(255.0)
+    q_dev = np.floor(v32.astype(np.float64) + 0.5).astype(np.int32)
+    q_ref = np.rint(np.clip(od, 0, 1) * 255).astype(np.int32)
+    for _ in range(2):
+        plan.execute_host(lay.views, out)
+        assert np.array_equal(out[..., 3] == 255, ov == 1)
+        assert np.array_equal(out[..., :3].astype(np.int32)[ov == 1], q_dev[ov == 1])
+        assert np.abs(out[..., :3].astype(np.int32) - q_ref)[ov == 1].max() <= 1
+    plan.close()
+
+
 def _skip_wait_layout(seed=4):
     """Fold 3's Area3 box meets fold 1's box but not fold 2's, while fold 2
     writes Area2 pixels inside fold 3's box (view 2's alpha hides its left
