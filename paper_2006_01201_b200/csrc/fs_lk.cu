@@ -51,6 +51,12 @@ struct LkCfg {
     static constexpr int S = FULL ? LK_S_FULL : LK_S_ITER;     // outputs per horizontal run
 };
 
+#ifndef LK_MINB_FULL
+#define LK_MINB_FULL 2
+#endif
+#ifndef LK_MINB_ITER
+#define LK_MINB_ITER 3
+#endif
 constexpr int LK_IW = 128;  // producer threads = input columns per CTA
 constexpr int LK_THREADS = 2 * LK_IW;
 
@@ -340,7 +346,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(LK_THREADS, 2) k_lk_sweep(LkArgs a) {
+__global__ void __launch_bounds__(LK_THREADS, FULL ? LK_MINB_FULL : LK_MINB_ITER) k_lk_sweep(LkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     void* ring = smem;
     double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes<FULL>(a.r));
@@ -367,12 +373,12 @@ void lk_init() {
     lk_configured = true;
 }
 
-int lk_tile_rows(int w, int h, int r, int ndir) {
-    // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x 2.  Pick th
+int lk_tile_rows(int w, int h, int r, int ndir, int per_sm) {
+    // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x per_sm.  Pick th
     // minimising waves x rows per CTA (wave quantisation vs. halo rows).
     const int tw = LK_IW - 2 * r;
     const long cols = (w + tw - 1) / tw;
-    const long slots = 148L * 2;
+    const long slots = 148L * per_sm;
     int best = 16;
     long best_cost = -1;
     for (int th = 16; th <= 256; th += 8) {
@@ -399,7 +405,7 @@ cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
 cudaError_t lk_sweep(const LkArgs& a0, bool full, cudaStream_t s) {
     LkArgs a = a0;
     a.tw = LK_IW - 2 * a.r;
-    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir);
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, full ? LK_MINB_FULL : LK_MINB_ITER);
     lk_init();
     dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
     if (full)
