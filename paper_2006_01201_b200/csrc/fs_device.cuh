@@ -230,9 +230,16 @@ void smooth(const SmoothArgs&, cudaStream_t);
 void finalize_flow(const SmoothArgs&, cudaStream_t);
 template <class M>
 void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, cudaStream_t);
+// owner != nullptr: the panorama's validity before fold `fold` is owner < fold
 template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
-                 const int*, const FoldStats*, double, double, float4*, float2*, cudaStream_t);
+                 const int*, const FoldStats*, double, double, float4*, float2*,
+                 const uint8_t* owner, int fold, cudaStream_t);
+template <class V>
+void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t);
+template <class V>
+void compose_area3(const Canvas&, const V&, const Rect& box, const float4*, const uint8_t* owner,
+                   int fold, cudaStream_t);
 template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);

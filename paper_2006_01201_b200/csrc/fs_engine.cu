@@ -419,14 +419,20 @@ int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s)
 
 template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
-                       const fs_blend_params& bp, cudaStream_t s) {
+                       const fs_blend_params& bp, cudaStream_t s, const uint8_t* owner, int fold) {
     int launches = 0;
     {
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
         ProfScope ps("blend", 61.0 * f.box.area(), s);
         launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
                             f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, f.wgray,
-                            s);
+                            owner, fold, s);
+    }
+    if (owner) {  // Area3 only: the fold's Area2 was copied on its branch
+        ProfScope ps("compose", 21.0 * f.box.area(), s);  // owner 1 + view 4 + blended 16
+        launch::compose_area3(cv, view, f.box, f.blended, owner, fold, s);
+        FS_CK(cudaGetLastError());
+        return launches + 2;
     }
     {
         // view 4 + pano valid 1 in, rgb 16 + valid 1 out on the view; blended 16 in on Area3
@@ -465,8 +471,10 @@ template int fold_enqueue_flow_edt<ViewF4, PanoPlane, PanoPlane>(
 template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoViews&, const ViewU8&,
                                                  cudaStream_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
-                                        CanvasCount*, const fs_blend_params&, cudaStream_t);
+                                        CanvasCount*, const fs_blend_params&, cudaStream_t,
+                                        const uint8_t*, int);
 template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
-                                        CanvasCount*, const fs_blend_params&, cudaStream_t);
+                                        CanvasCount*, const fs_blend_params&, cudaStream_t,
+                                        const uint8_t*, int);
 
 }  // namespace fs

@@ -528,18 +528,34 @@ __device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, d
     }
 }
 
-struct CanvasSampler {
-    const float4* rgb;
+// The panorama's validity before a fold: the canvas valid plane (serial
+// folds), or the owner plane (owner < k: some earlier view covers the pixel)
+// when the folds' Area2 copies are written ahead of the ordered chain.
+struct PanoValidPlane {
     const uint8_t* valid;
     int w;
-    __device__ __forceinline__ bool valid_at(int x, int y) const {
+    __device__ __forceinline__ bool operator()(int x, int y) const {
         return valid[(size_t)y * w + x] != 0;
     }
+};
+struct PanoOwnerBefore {
+    const uint8_t* owner;
+    int w, k;
+    __device__ __forceinline__ bool operator()(int x, int y) const {
+        return owner[(size_t)y * w + x] < k;
+    }
+};
+template <class PV>
+struct CanvasSampler {
+    const float4* rgb;
+    PV pv;
+    int w;
+    __device__ __forceinline__ bool valid_at(int x, int y) const { return pv(x, y); }
     __device__ __forceinline__ float4 value_at(int x, int y) const { return rgb[(size_t)y * w + x]; }
 };
 
-template <class V>
-__global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restrict__ flr,
+template <class V, class PV>
+__global__ void k_blend_area3(Canvas cv, PV pv, V view, Rect box, const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
                               const int* __restrict__ d2, const FoldStats* st, double k,
                               double coef, float4* __restrict__ out, float2* __restrict__ wgray) {
@@ -547,15 +563,14 @@ __global__ void k_blend_area3(Canvas cv, V view, Rect box, const float2* __restr
     int j = blockIdx.y;
     if (i >= box.w) return;
     int x = box.x0 + i, y = box.y0 + j;
-    size_t p = (size_t)y * cv.w + x;
-    if (!(cv.valid[p] && view.valid_at(x, y))) return;  // not Area3
+    if (!(pv(x, y) && view.valid_at(x, y))) return;  // not Area3
     const bool have1 = (st->pv_count - st->cnt3) > 0, have2 = st->cnt2 > 0;
     size_t o = (size_t)j * box.w + i;
     double blend_r = eq1_area3(have1, have2, d1[o], d2[o]);
     double blend_l = 1.0 - blend_r;
     float2 rl = frl[o], lr = flr[o];
     float cl[3], cr[3];
-    CanvasSampler L{cv.rgb, cv.valid, cv.w};
+    CanvasSampler<PV> L{cv.rgb, pv, cv.w};
     bilinear_rgb(L, cv.w, cv.h, cv.ch, x + rl.x * (1.0 - blend_l), y + rl.y * (1.0 - blend_l), cl);
     bilinear_rgb(view, cv.w, cv.h, cv.ch, x + lr.x * (1.0 - blend_r), y + lr.y * (1.0 - blend_r),
                  cr);
@@ -588,6 +603,31 @@ __global__ void k_compose(Canvas cv, V view, Rect box, const float4* __restrict_
         cv.rgb[p] = view.value_at(x, y);
         cv.valid[p] = 1;
     }
+}
+
+// The compose split for the planned DAG: a fold's Area2 (the pixels its view
+// covers first, owner == k: a copy of the view, src/blender.cpp:69-71) is
+// written on the fold's branch as soon as the view is claimed; only its Area3
+// (the blended box) is written in the ordered chain.
+template <class V>
+__global__ void k_compose_area2(Canvas cv, V view, const uint8_t* __restrict__ owner, int k) {
+    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = view.rect.y0 + blockIdx.y;
+    if (x >= view.rect.x1()) return;
+    const size_t p = (size_t)y * cv.w + x;
+    if (owner[p] != k) return;
+    cv.rgb[p] = view.value_at(x, y);
+    cv.valid[p] = 1;
+}
+template <class V>
+__global__ void k_compose_area3(Canvas cv, V view, Rect box, const float4* __restrict__ blended,
+                                const uint8_t* __restrict__ owner, int k) {
+    const int x = box.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = box.y0 + blockIdx.y;
+    if (x >= box.x1()) return;
+    const size_t p = (size_t)y * cv.w + x;
+    if (owner[p] < k && view.valid_at(x, y))
+        cv.rgb[p] = blended[(size_t)(y - box.y0) * box.w + (x - box.x0)];
 }
 
 // validity-only fold step used by the planner: pano valid |= view valid
@@ -726,9 +766,26 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, cudaStre
 template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
                  const float2* frl, const int* d1, const int* d2, const FoldStats* st, double k,
-                 double coef, float4* out, float2* wgray, cudaStream_t s) {
-    k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(cv, view, box, flr, frl, d1, d2, st,
-                                                             k, coef, out, wgray);
+                 double coef, float4* out, float2* wgray, const uint8_t* owner, int fold,
+                 cudaStream_t s) {
+    if (owner)
+        k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
+            cv, PanoOwnerBefore{owner, cv.w, fold}, view, box, flr, frl, d1, d2, st, k, coef, out,
+            wgray);
+    else
+        k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
+            cv, PanoValidPlane{cv.valid, cv.w}, view, box, flr, frl, d1, d2, st, k, coef, out,
+            wgray);
+}
+template <class V>
+void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
+                   cudaStream_t s) {
+    k_compose_area2<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, owner, fold);
+}
+template <class V>
+void compose_area3(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
+                   const uint8_t* owner, int fold, cudaStream_t s) {
+    k_compose_area3<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, blended, owner, fold);
 }
 template <class V>
 void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -784,12 +841,18 @@ template void edt<PlaneMask>(const EdtJob<PlaneMask>&, const EdtJob<PlaneMask>&,
                              const FoldStats*, cudaStream_t);
 template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
                              const FoldStats*, cudaStream_t);
+template void compose_area2<ViewU8>(const Canvas&, const ViewU8&, const uint8_t*, int,
+                                    cudaStream_t);
+template void compose_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
+                                    const uint8_t*, int, cudaStream_t);
+template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
+                                    const uint8_t*, int, cudaStream_t);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, float2*, cudaStream_t);
+                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, float2*, cudaStream_t);
+                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

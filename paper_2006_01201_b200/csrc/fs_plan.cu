@@ -47,8 +47,21 @@ struct fs_plan_s {
     FoldStats* hstats = nullptr;  // page-locked copy of the folds' statistics (fs_plan_check)
     std::vector<int> crop_wait;
     // final_rects[k]: canvas rectangles no fold after k writes (k = 0: the
-    // placement of view 0); quantised and read back as soon as fold k composed.
+    // placement of view 0).  Split by fold k's Area3 box into reads that wait
+    // for fold k's compose in the chain (late) and reads that wait only for
+    // the Area2 copies / composes that can touch them (early).
     std::vector<std::vector<Rect>> final_rects;
+    struct Readback {
+        Rect r;
+        std::vector<int> a2;  // folds whose Area2 copy may write r
+        int compose = 0;      // last fold whose chain compose may write r (0: none)
+        bool place = false;   // view 0's placement may write r
+    };
+    std::vector<std::vector<Readback>> early, late;
+    std::vector<Rect> boxes;  // Area3 box of fold k (k >= 1)
+    std::vector<cudaEvent_t> ev_a2;  // fold k's Area2 copied
+    cudaStream_t d2h_early = nullptr;
+    cudaEvent_t ev_out_early = nullptr;
     // graph with the host copies inside (execute_host), keyed by the pointers
     cudaGraph_t hgraph = nullptr;
     cudaGraphExec_t hexec = nullptr;
@@ -180,33 +193,47 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     // the owner plane: views claimed in fold order as they land
     FS_CK(cudaStreamWaitEvent(p->own, p->ev_start, 0));
     FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
-    for (int k = 0; k + 1 < p->n; ++k) {
+    for (int k = 0; k < p->n; ++k) {
         if (hin) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
         launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_own[k], p->own));
     }
-    // the read-back chain: quantise (and copy) every rectangle once final
-    auto emit_final = [&](int k, cudaEvent_t after) {
-        if (p->final_rects[k].empty()) return;
-        FS_CK(cudaStreamWaitEvent(p->d2h, after, 0));
-        for (const Rect& r : p->final_rects[k]) {
-            launch::quantize_rect(p->cv, r, p->out, p->d2h);
-            ++launches;
-            if (!hout) continue;
-            const size_t pitch = (size_t)p->cw * 4;
-            const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
-            if (r.w == p->cw)
-                FS_CK(cudaMemcpyAsync(io->out + off, reinterpret_cast<const uint8_t*>(p->out) + off,
-                                      pitch * r.h, cudaMemcpyDefault, p->d2h));
-            else
-                FS_CK(cudaMemcpy2DAsync(io->out + off, pitch,
-                                        reinterpret_cast<const uint8_t*>(p->out) + off, pitch,
-                                        (size_t)r.w * 4, r.h, cudaMemcpyDefault, p->d2h));
+    // the read-backs: quantise (and copy) every rectangle once final
+    auto read_rect = [&](const Rect& r, cudaStream_t st) {
+        launch::quantize_rect(p->cv, r, p->out, st);
+        ++launches;
+        if (!hout) return;
+        const size_t pitch = (size_t)p->cw * 4;
+        const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
+        if (r.w == p->cw)
+            FS_CK(cudaMemcpyAsync(io->out + off, reinterpret_cast<const uint8_t*>(p->out) + off,
+                                  pitch * r.h, cudaMemcpyDefault, st));
+        else
+            FS_CK(cudaMemcpy2DAsync(io->out + off, pitch,
+                                    reinterpret_cast<const uint8_t*>(p->out) + off, pitch,
+                                    (size_t)r.w * 4, r.h, cudaMemcpyDefault, st));
+    };
+    // early reads of fold k: after the Area2 copies and composes that may
+    // write them (all recorded by the time fold k's branch copied its Area2)
+    auto emit_early = [&](int k) {
+        for (const auto& rb : p->early[k]) {
+            if (rb.place) FS_CK(cudaStreamWaitEvent(p->d2h_early, p->ev_place, 0));
+            for (int m : rb.a2) FS_CK(cudaStreamWaitEvent(p->d2h_early, p->ev_a2[m], 0));
+            if (rb.compose) FS_CK(cudaStreamWaitEvent(p->d2h_early, p->ev_compose[rb.compose], 0));
+            if (&rb == &p->early[k].front())
+                mark("readback_early_" + std::to_string(k) + "_ready", p->d2h_early);
+            read_rect(rb.r, p->d2h_early);
         }
+        if (!p->early[k].empty()) mark("readback_early_" + std::to_string(k), p->d2h_early);
+    };
+    auto emit_late = [&](int k) {
+        if (p->late[k].empty()) return;
+        FS_CK(cudaStreamWaitEvent(p->d2h, p->ev_compose[k], 0));
+        for (const auto& rb : p->late[k]) read_rect(rb.r, p->d2h);
         mark("readback_" + std::to_string(k), p->d2h);
     };
-    emit_final(0, p->ev_place);
+    emit_early(0);
     for (int k = 1; k < p->n; ++k) {
         FoldWS<ViewU8>& f = p->folds[k - 1];
         ViewU8 v = view_of(p, k);
@@ -221,6 +248,12 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         launch::chain_count(f.st, k == 1 ? nullptr : p->folds[k - 2].st, p->cc, b);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_cnt[k], b));
+        // the fold's Area2 (the pixels view k covers first) is a copy of the
+        // view: written now, off the ordered chain
+        FS_CK(cudaStreamWaitEvent(b, p->ev_own[k], 0));
+        launch::compose_area2(p->cv, v, p->owner, k, b);
+        ++launches;
+        FS_CK(cudaEventRecord(p->ev_a2[k], b));
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
         cudaStream_t es = p->edt_stream[k - 1];
         if (p->crop_wait[k] == 0) {
@@ -241,13 +274,17 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         mark("fold" + fk + "_edt_end", b);
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         mark("fold" + fk + "_blend_start", s);
-        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
+        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
         mark("fold" + fk + "_compose_end", s);
-        emit_final(k, p->ev_compose[k]);
     }
+    // early reads in fold order, then the chain's late reads in fold order
+    for (int k = 1; k < p->n; ++k) emit_early(k);
+    for (int k = 1; k < p->n; ++k) emit_late(k);
     FS_CK(cudaEventRecord(p->ev_out, p->d2h));
     FS_CK(cudaStreamWaitEvent(s, p->ev_out, 0));
+    FS_CK(cudaEventRecord(p->ev_out_early, p->d2h_early));
+    FS_CK(cudaStreamWaitEvent(s, p->ev_out_early, 0));
     mark("end", s);
     FS_CK(cudaGetLastError());
     return launches;
@@ -296,6 +333,7 @@ bool async_copyable(const void* ptr) {
     }
     return at.type != cudaMemoryTypeUnregistered;
 }
+
 
 // Canvas rectangles final after fold k (k = 0: after view 0 is placed): the
 // canvas is cut into cells along every view edge; a cell is final after the
@@ -351,6 +389,47 @@ void plan_final_rects(fs_plan_s* p) {
     }
     for (int k = 0; k < p->n; ++k)
         for (const Rect& o : open[k]) p->final_rects[k].push_back(o);
+}
+
+// Split of the final rectangles (see fs_plan_s::Readback).
+void plan_readbacks(fs_plan_s* p) {
+    plan_final_rects(p);
+    const int n = p->n;
+    p->early.assign(n, {});
+    p->late.assign(n, {});
+    auto meets = [](const Rect& a, const Rect& b) {
+        Rect i = rect_inter(a, b);
+        return i.w > 0 && i.h > 0;
+    };
+    for (int k = 0; k < n; ++k)
+        for (const Rect& R : p->final_rects[k]) {
+            if (k == 0) {
+                p->early[0].push_back({R, {}, 0, true});
+                continue;
+            }
+            const Rect& B = p->boxes[k];
+            const Rect in = rect_inter(R, B);
+            if (in.w > 0 && in.h > 0) p->late[k].push_back({in, {}, 0, false});
+            // R minus the box: the bands above and below, then left and right
+            std::vector<Rect> pieces;
+            if (in.w <= 0 || in.h <= 0) {
+                pieces.push_back(R);
+            } else {
+                pieces.push_back(Rect{R.x0, R.y0, R.w, in.y0 - R.y0});
+                pieces.push_back(Rect{R.x0, in.y1(), R.w, R.y1() - in.y1()});
+                pieces.push_back(Rect{R.x0, in.y0, in.x0 - R.x0, in.h});
+                pieces.push_back(Rect{in.x1(), in.y0, R.x1() - in.x1(), in.h});
+            }
+            for (const Rect& q : pieces) {
+                if (q.w <= 0 || q.h <= 0) continue;
+                fs_plan_s::Readback rb{q, {}, 0, meets(p->rects[0], q)};
+                for (int m = 1; m <= k; ++m)
+                    if (meets(p->rects[m], q)) rb.a2.push_back(m);
+                for (int m = 1; m < k; ++m)
+                    if (meets(p->boxes[m], q)) rb.compose = m;
+                p->early[k].push_back(rb);
+            }
+        }
 }
 
 // Area3 boxes of every fold from the view masks: a validity-only fold on the
@@ -501,6 +580,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             p->ev_h2d.assign(n, nullptr);
             p->ev_cnt.assign(n, nullptr);
             p->ev_own.assign(n, nullptr);
+            p->ev_a2.assign(n, nullptr);
             p->ev_efork.assign(n, nullptr);
             p->ev_ejoin.assign(n, nullptr);
             for (int k = 0; k < n; ++k) {
@@ -509,15 +589,18 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
                 FS_CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_cnt[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_own[k], cudaEventDisableTiming));
+                FS_CK(cudaEventCreateWithFlags(&p->ev_a2[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_efork[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_ejoin[k], cudaEventDisableTiming));
             }
-            for (cudaEvent_t* e : {&p->ev_start, &p->ev_place, &p->ev_out})
+            for (cudaEvent_t* e : {&p->ev_start, &p->ev_place, &p->ev_out, &p->ev_out_early})
                 FS_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
             FS_CK(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
             FS_CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+            FS_CK(cudaStreamCreateWithFlags(&p->d2h_early, cudaStreamNonBlocking));
             FS_CK(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
-            plan_final_rects(p);
+            p->boxes = boxes;
+            plan_readbacks(p);
         }
         p->pano_bbox.assign(n, Rect{});
         Rect pb = p->rects[0];
@@ -764,7 +847,10 @@ void fs_plan_destroy(fs_plan p) {
     for (auto st : p->edt_stream)
         if (st) cudaStreamDestroy(st);
     if (p->own) cudaStreamDestroy(p->own);
-    for (cudaEvent_t e : {p->ev_start, p->ev_place, p->ev_out})
+    for (auto e : p->ev_a2)
+        if (e) cudaEventDestroy(e);
+    if (p->d2h_early) cudaStreamDestroy(p->d2h_early);
+    for (cudaEvent_t e : {p->ev_start, p->ev_place, p->ev_out, p->ev_out_early})
         if (e) cudaEventDestroy(e);
     if (p->h2d) cudaStreamDestroy(p->h2d);
     if (p->d2h) cudaStreamDestroy(p->d2h);
