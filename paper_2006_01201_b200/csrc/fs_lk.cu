@@ -373,15 +373,18 @@ void lk_init() {
     lk_configured = true;
 }
 
+#ifndef LK_TH_MIN
+#define LK_TH_MIN 16  // smallest tile height (smaller: faster alone, slower in the DAG)
+#endif
 int lk_tile_rows(int w, int h, int r, int ndir, int per_sm) {
     // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x per_sm.  Pick th
     // minimising waves x rows per CTA (wave quantisation vs. halo rows).
     const int tw = LK_IW - 2 * r;
     const long cols = (w + tw - 1) / tw;
     const long slots = 148L * per_sm;
-    int best = 16;
+    int best = LK_TH_MIN;
     long best_cost = -1;
-    for (int th = 16; th <= 256; th += 8) {
+    for (int th = LK_TH_MIN; th <= 256; th += (th < 32 ? 4 : 8)) {
         const long ctas = cols * ((h + th - 1) / th) * ndir;
         const long cost = ((ctas + slots - 1) / slots) * (th + 2 * r);
         if (best_cost < 0 || cost < best_cost) {
