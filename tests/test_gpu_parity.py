@@ -511,6 +511,70 @@ def test_plan_serial_schedule_many_views(fs, oracle):
     plan.close()
 
 
+def _random_layout(seed):
+    """A random fold: 2-6 views of random sizes placed so that each overlaps
+    the union of the earlier ones, some with alpha holes; random canvas."""
+    rng = np.random.RandomState(seed)
+    W, H = int(rng.randint(220, 420)), int(rng.randint(140, 300))
+    scene = S.rgb_scene(H, W, seed + 100)
+    n = int(rng.randint(2, 7))
+    offs, views = [], []
+    covered = np.zeros((H, W), bool)
+    for k in range(n):
+        for _ in range(100):
+            w, h = int(rng.randint(60, W // 2 + 60)), int(rng.randint(50, H))
+            w, h = min(w, W), min(h, H)
+            x, y = int(rng.randint(0, W - w + 1)), int(rng.randint(0, H - h + 1))
+            if k == 0 or covered[y:y + h, x:x + w].sum() >= 400:
+                break
+        else:
+            break
+        v = S.rgba(np.roll(scene, (int(rng.randint(-2, 3)), int(rng.randint(-3, 4))),
+                           axis=(0, 1))[y:y + h, x:x + w])
+        if rng.rand() < 0.4:  # an alpha hole
+            hx, hy = int(rng.randint(0, w)), int(rng.randint(0, h))
+            v[hy:hy + int(rng.randint(3, 30)), hx:hx + int(rng.randint(3, 30)), 3] = 0
+        valid = v[..., 3] >= 128
+        if k > 0 and (covered[y:y + h, x:x + w] & valid).sum() == 0:
+            break
+        covered[y:y + h, x:x + w] |= valid
+        views.append(v)
+        offs.append((x, y))
+    return S.Layout("random%d" % seed, W, H, views, offs, 3)
+
+
+@pytest.mark.parametrize("seed", list(range(20)))
+def test_plan_random_layouts(fs, oracle, seed):
+    """Random layouts through the planned DAG (owner plane, early Area2
+    copies, hybrid crops, split read-backs): the planned 8-bit canvas equals
+    the device fold's panorama quantised, and the fold matches the
+    restatement."""
+    lay = _random_layout(seed)
+    if len(lay.views) < 2:
+        pytest.skip("degenerate layout")
+    params = fs.FlowParams(levels=2, window_radius=4, iterations_per_level=2)
+    fv = lay.float_views()
+    od, ov = oracle.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                  lay.canvas_w, lay.canvas_h, params.astuple())
+    placed = [fs.PlacedImage(fs.ImageBuf(d, v), x, y) for (d, v), (x, y) in zip(fv, lay.offsets)]
+    pano, _ = fs.stitch_placed(placed, lay.canvas_w, lay.canvas_h, params)
+    assert np.array_equal(pano.valid, ov)
+    assert np.abs(pano.data - od).max() <= 1e-4
+    v32 = np.clip(pano.data, 0, 1).astype(np.float32) * np.float32(255.0)
+    q_dev = np.floor(v32.astype(np.float64) + 0.5).astype(np.int32)
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params,
+                   views_rgba=lay.views)
+    import torch
+    pin = [torch.from_numpy(v).pin_memory() for v in lay.views]
+    out = torch.zeros((lay.canvas_h, lay.canvas_w, 4), dtype=torch.uint8).pin_memory()
+    for _ in range(2):  # page-locked: the graph with the transfers inside
+        plan.execute_ptrs([t.data_ptr() for t in pin], out.data_ptr())
+        o = out.numpy()
+        assert np.array_equal(o[..., 3] == 255, ov == 1)
+        assert np.array_equal(o[..., :3].astype(np.int32)[ov == 1], q_dev[ov == 1])
+    plan.close()
+
+
 def _far_seed_layout(seed=8):
     """Area3 (x 3..500) whose only Area1 seeds are a 3-px hole at its left
     end, while the panorama's bounding box (view 0's rectangle, alpha 0 for
