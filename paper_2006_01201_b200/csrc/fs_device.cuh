@@ -213,7 +213,9 @@ void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 // owner[p] = k where view k is valid and no earlier view claimed p
 void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t);
-template <class V> void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t);
+// out != nullptr: also the RGBA8 value of every valid pixel written
+template <class V>
+void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t, uchar4* out = nullptr);
 template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
 // pv_count = prev->pv_count + prev->cnt2 (prev: the previous fold), or cc for fold 1
@@ -236,10 +238,11 @@ void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const floa
                  const int*, const FoldStats*, double, double, float4*, float2*,
                  const uint8_t* owner, int fold, cudaStream_t);
 template <class V>
-void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t);
+void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
+                   uchar4* out = nullptr);
 template <class V>
 void compose_area3(const Canvas&, const V&, const Rect& box, const float4*, const uint8_t* owner,
-                   int fold, cudaStream_t);
+                   int fold, cudaStream_t, uchar4* out = nullptr);
 template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);

@@ -132,12 +132,12 @@ template <class V, class P>
 int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
 // Code 1 blend on Area3 + composition of the view onto the canvas
 // (owner != nullptr: the planned DAG — the panorama's validity is owner <
-// fold and only the Area3 box is written; the fold's Area2 copy is the
-// caller's, launch::compose_area2)
+// fold and only the Area3 box is written, with its RGBA8 values into `out`;
+// the fold's Area2 copy is the caller's, launch::compose_area2)
 template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
                        const fs_blend_params& bp, cudaStream_t s, const uint8_t* owner = nullptr,
-                       int fold = 0);
+                       int fold = 0, uchar4* out = nullptr);
 
 void init_stats(FoldStats* st, cudaStream_t s);
 void init_count(CanvasCount* cc, cudaStream_t s);

@@ -22,8 +22,19 @@ namespace fs {
 // block issues one atomic per statistic (thousands, not millions).
 constexpr int PART_ROWS = 8;
 
+// K8 (src/image.cpp:52-65) of one valid pixel: RGBA8, alpha 255
+__device__ __forceinline__ uchar4 quantize_px(float4 v, int ch) {
+    const uint8_t r = quantize8(v.x);
+    return ch == 3 ? make_uchar4(r, quantize8(v.y), quantize8(v.z), 255)
+                   : make_uchar4(r, r, r, 255);
+}
+
+// out != nullptr (the planned DAG): the RGBA8 canvas is written by each
+// pixel's writers directly (place, Area2 copy, Area3 compose) — the last
+// writer of a pixel leaves its final 8-bit value.
 template <class V>
-__global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCount* count) {
+__global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCount* count,
+                                                    uchar4* __restrict__ out) {
     __shared__ int red[8];
     const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
@@ -33,8 +44,10 @@ __global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCou
         for (int y = ya; y < yb; ++y) {
             size_t p = (size_t)y * cv.w + x;
             bool v = view.valid_at(x, y);
-            cv.rgb[p] = view.value_at(x, y);
+            const float4 val = view.value_at(x, y);
+            cv.rgb[p] = val;
             cv.valid[p] = v ? 1 : 0;
+            if (out && v) out[p] = quantize_px(val, cv.ch);
             n += v;
         }
     n = __reduce_add_sync(0xffffffffu, n);
@@ -610,24 +623,31 @@ __global__ void k_compose(Canvas cv, V view, Rect box, const float4* __restrict_
 // written on the fold's branch as soon as the view is claimed; only its Area3
 // (the blended box) is written in the ordered chain.
 template <class V>
-__global__ void k_compose_area2(Canvas cv, V view, const uint8_t* __restrict__ owner, int k) {
+__global__ void k_compose_area2(Canvas cv, V view, const uint8_t* __restrict__ owner, int k,
+                                uchar4* __restrict__ out) {
     const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int y = view.rect.y0 + blockIdx.y;
     if (x >= view.rect.x1()) return;
     const size_t p = (size_t)y * cv.w + x;
     if (owner[p] != k) return;
-    cv.rgb[p] = view.value_at(x, y);
+    const float4 v = view.value_at(x, y);
+    cv.rgb[p] = v;
     cv.valid[p] = 1;
+    if (out) out[p] = quantize_px(v, cv.ch);
 }
 template <class V>
 __global__ void k_compose_area3(Canvas cv, V view, Rect box, const float4* __restrict__ blended,
-                                const uint8_t* __restrict__ owner, int k) {
+                                const uint8_t* __restrict__ owner, int k,
+                                uchar4* __restrict__ out) {
     const int x = box.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int y = box.y0 + blockIdx.y;
     if (x >= box.x1()) return;
     const size_t p = (size_t)y * cv.w + x;
-    if (owner[p] < k && view.valid_at(x, y))
-        cv.rgb[p] = blended[(size_t)(y - box.y0) * box.w + (x - box.x0)];
+    if (owner[p] < k && view.valid_at(x, y)) {
+        const float4 v = blended[(size_t)(y - box.y0) * box.w + (x - box.x0)];
+        cv.rgb[p] = v;
+        if (out) out[p] = quantize_px(v, cv.ch);
+    }
 }
 
 // validity-only fold step used by the planner: pano valid |= view valid
@@ -694,9 +714,9 @@ namespace launch {
 static inline dim3 row_grid(int w, int h, int bx = 256) { return dim3((w + bx - 1) / bx, h); }
 
 template <class V>
-void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s) {
+void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s, uchar4* out) {
     k_place_view<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
-        cv, view, count);
+        cv, view, count, out);
 }
 template <class V, class P>
 void partition(const P& pano, const V& view, FoldStats* st, cudaStream_t s) {
@@ -779,13 +799,14 @@ void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2*
 }
 template <class V>
 void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
-                   cudaStream_t s) {
-    k_compose_area2<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, owner, fold);
+                   cudaStream_t s, uchar4* out) {
+    k_compose_area2<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, owner, fold, out);
 }
 template <class V>
 void compose_area3(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
-                   const uint8_t* owner, int fold, cudaStream_t s) {
-    k_compose_area3<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, blended, owner, fold);
+                   const uint8_t* owner, int fold, cudaStream_t s, uchar4* out) {
+    k_compose_area3<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, blended, owner, fold,
+                                                          out);
 }
 template <class V>
 void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -812,8 +833,10 @@ void export_float(const Canvas& cv, float* out, uint8_t* vout, cudaStream_t s) {
 
 // explicit instantiations
 template void union_valid<ViewU8>(const Canvas&, const ViewU8&, cudaStream_t);
-template void place_view<ViewU8>(const Canvas&, const ViewU8&, CanvasCount*, cudaStream_t);
-template void place_view<ViewF4>(const Canvas&, const ViewF4&, CanvasCount*, cudaStream_t);
+template void place_view<ViewU8>(const Canvas&, const ViewU8&, CanvasCount*, cudaStream_t,
+                                 uchar4*);
+template void place_view<ViewF4>(const Canvas&, const ViewF4&, CanvasCount*, cudaStream_t,
+                                 uchar4*);
 template void partition<ViewU8, PanoPlane>(const PanoPlane&, const ViewU8&, FoldStats*,
                                            cudaStream_t);
 template void partition<ViewU8, PanoViews>(const PanoViews&, const ViewU8&, FoldStats*,
@@ -842,11 +865,11 @@ template void edt<PlaneMask>(const EdtJob<PlaneMask>&, const EdtJob<PlaneMask>&,
 template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
                              const FoldStats*, cudaStream_t);
 template void compose_area2<ViewU8>(const Canvas&, const ViewU8&, const uint8_t*, int,
-                                    cudaStream_t);
+                                    cudaStream_t, uchar4*);
 template void compose_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
-                                    const uint8_t*, int, cudaStream_t);
+                                    const uint8_t*, int, cudaStream_t, uchar4*);
 template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
-                                    const uint8_t*, int, cudaStream_t);
+                                    const uint8_t*, int, cudaStream_t, uchar4*);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, const FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t);

@@ -166,9 +166,10 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     }
     init_count(p->cc, s);
     if (hin) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[0], 0));
+    if (dag) FS_CK(cudaMemsetAsync(p->out, 0, (size_t)p->cw * p->chh * 4, s));
     {
         ProfScope ps("place", 21.0 * p->rects[0].area(), s);  // view 4 in, rgb 16 + valid 1 out
-        launch::place_view(p->cv, view_of(p, 0), p->cc, s);
+        launch::place_view(p->cv, view_of(p, 0), p->cc, s, dag ? p->out : nullptr);
     }
     launches += 2;
     if (!dag) {
@@ -200,9 +201,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaEventRecord(p->ev_own[k], p->own));
     }
     // the read-backs: quantise (and copy) every rectangle once final
+    // (the RGBA8 canvas is written by each pixel's writers: copies only)
     auto read_rect = [&](const Rect& r, cudaStream_t st) {
-        launch::quantize_rect(p->cv, r, p->out, st);
-        ++launches;
         if (!hout) return;
         const size_t pitch = (size_t)p->cw * 4;
         const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
@@ -251,7 +251,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         // the fold's Area2 (the pixels view k covers first) is a copy of the
         // view: written now, off the ordered chain
         FS_CK(cudaStreamWaitEvent(b, p->ev_own[k], 0));
-        launch::compose_area2(p->cv, v, p->owner, k, b);
+        launch::compose_area2(p->cv, v, p->owner, k, b, p->out);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_a2[k], b));
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
@@ -274,7 +274,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         mark("fold" + fk + "_edt_end", b);
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         mark("fold" + fk + "_blend_start", s);
-        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k);
+        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
         mark("fold" + fk + "_compose_end", s);
     }
