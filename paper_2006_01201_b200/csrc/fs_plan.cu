@@ -598,7 +598,8 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             FS_CK(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
             FS_CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
             FS_CK(cudaStreamCreateWithFlags(&p->d2h_early, cudaStreamNonBlocking));
-            FS_CK(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
+            // the claims gate every fold's branch: highest priority
+            FS_CK(cudaStreamCreateWithPriority(&p->own, cudaStreamNonBlocking, greatest));
             p->boxes = boxes;
             plan_readbacks(p);
         }
