@@ -278,9 +278,14 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
         mark("fold" + fk + "_compose_end", s);
     }
-    // early reads in fold order, then the chain's late reads in fold order
-    for (int k = 1; k < p->n; ++k) emit_early(k);
-    for (int k = 1; k < p->n; ++k) emit_late(k);
+    // Copies leave the device in submission order (one D2H engine), so they
+    // are submitted by expected readiness: a fold's early reads when its view
+    // has arrived, its late reads about a fold later (after its flow)
+    for (int k = 1; k < p->n; ++k) {
+        emit_early(k);
+        if (k >= 2) emit_late(k - 1);
+    }
+    emit_late(p->n - 1);
     FS_CK(cudaEventRecord(p->ev_out, p->d2h));
     FS_CK(cudaStreamWaitEvent(s, p->ev_out, 0));
     FS_CK(cudaEventRecord(p->ev_out_early, p->d2h_early));
