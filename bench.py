@@ -48,6 +48,10 @@ def parse_args():
     ap.add_argument("--config", choices=["c2", "c1", "c3", "c4"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", choices=["none", "seams"], default="none",
+                    help="seams: ONE panorama whose overlap pairs are sharded over the GPUs "
+                         "(strong scaling, strips gathered to rank 0 over NCCL P2P); "
+                         "none: one independent panorama per GPU (weak scaling)")
     ap.add_argument("--kernel-only", action="store_true",
                     help="only warmup + timed steps (for ncu launch lists)")
     return ap.parse_args()
@@ -217,11 +221,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2006_01201_b200 as fs
 
-    lay = make_layout(args.config, rank)
+    sharded = args.shard == "seams"
+    lay = make_layout(args.config, 0 if sharded else rank)
     params = fs.FlowParams(levels=lay.levels)
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params, device=local)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
+    sp = None
+    if sharded:
+        from paper_2006_01201_b200.shard import ShardedPlan, TorchDistTransport
+        if ws > 1:
+            dist.barrier()  # communicator up before the first point-to-point batch
+        sp = ShardedPlan(plan, ws, rank, transport=TorchDistTransport() if ws > 1 else None)
 
     # pinned host views + output canvas (the end-to-end call's buffers)
     host_views = [torch.from_numpy(v).pin_memory() for v in lay.views]
@@ -231,6 +242,29 @@ def main():
     d2h_bytes = host_out.numel()
     # first execution: uploads the views, validates the plan's EDT domains
     plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
+    shard_mode = None
+    if sp is not None:
+        if ws > 1:
+            shard_mode = sp.run()  # certified sharded, or unsharded on rank 0 from now on
+        else:
+            sp.execute(sptr)
+            torch.cuda.synchronize()
+            shard_mode = "sharded" if sp.status() == 0 else "unsharded"
+            if shard_mode == "unsharded":
+                sp.unsharded = True
+
+    def run_step(host=False):
+        if sp is not None and not sp.unsharded:
+            if host:
+                sp.execute(sptr, view_ptrs, host_out.data_ptr())
+            else:
+                sp.execute(sptr)
+        elif sp is not None and rank != 0:
+            return  # unsharded fallback: rank 0 folds the panorama alone
+        elif host:
+            plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
+        else:
+            plan.execute(sptr)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -239,7 +273,7 @@ def main():
             dist.barrier()
 
     for _ in range(args.warmup):
-        plan.execute(sptr)
+        run_step()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -252,20 +286,27 @@ def main():
         for a, b in ev:
             flush.zero_()
             a.record(stream)
-            plan.execute(sptr)
+            run_step()
             b.record(stream)
         torch.cuda.synchronize()
         barrier()
         wall = time.perf_counter() - wall0
-    plan.check()
+    if sp is not None and not sp.unsharded:
+        if sp.status() != 0:
+            raise RuntimeError("sharded execution not certified: " + fs._native.last_error())
+    elif rank == 0 or sp is None:
+        plan.check()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(step_ms)
     if ws > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * lay.canvas_mpx / (ms / 1e3)
+    units = 1 if sharded else ws  # panoramas per step over the job
+    value = units * lay.canvas_mpx / (ms / 1e3)
     launches = plan.launch_count
+    if sp is not None and not sp.unsharded:
+        launches = sp.launch_count
 
     if args.kernel_only:
         if rank == 0:
@@ -284,7 +325,7 @@ def main():
         barrier()
         for a, b in ee:
             a.record(stream)
-            plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
+            run_step(host=True)
             b.record(stream)
         torch.cuda.synchronize()
         e_ms = statistics.mean(a.elapsed_time(b) for a, b in ee)
@@ -292,8 +333,8 @@ def main():
             t = torch.tensor([e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": round(ws * lay.canvas_mpx / (e_ms / 1e3), 2), "unit": UNIT,
-               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+        e2e = {"value": round(units * lay.canvas_mpx / (e_ms / 1e3), 2), "unit": UNIT,
+               "h2d_bytes_per_step": h2d_bytes * ws, "d2h_bytes_per_step": d2h_bytes * units,
                "s_per_panorama": round(e_ms / 1e3, 5), "ms_per_step": round(e_ms, 4)}
 
     # ---- per-kernel roofline: event-timed launches on the launching stream
@@ -355,13 +396,19 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "f32/f64", "data": "synthetic",
             "config": {"workload": workload_name(lay, args.config),
                        "canvas": [lay.canvas_w, lay.canvas_h],
                        "views": [list(d) for d in lay.dims], "folds": len(lay.views) - 1,
                        "flow_params": list(params.astuple()), "blend_params": [10.0, 0.05],
-                       "parallelism": "dp%d (one independent panorama per GPU)" % ws,
+                       "parallelism": ("seam-sharded over %d GPU(s): folds on ranks %s, "
+                                       "stages %s, %d strip transfers (NCCL P2P), %s"
+                                       % (ws, sp.schedule.fold_rank, sp.schedule.stage,
+                                          len(sp.schedule.xfers), shard_mode)
+                                       if sharded else
+                                       "dp%d (one independent panorama per GPU)" % ws),
                        "l2": "inputs larger than L2 (views %d MB + canvas %d MB) and L2 "
                              "flushed (256 MB write) between timed steps"
                              % (h2d_bytes >> 20, (lay.canvas_w * lay.canvas_h * 21) >> 20),

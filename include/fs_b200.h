@@ -42,7 +42,9 @@ typedef enum {
     FS_ERR_OOM = 5,          /* device allocation failed */
     FS_ERR_UNSUPPORTED = 6,  /* parameter outside what the kernels implement */
     FS_ERR_IO = 7,           /* IoError (errors.hpp:16-20) */
-    FS_ERR_FORMAT = 8        /* FormatError (errors.hpp:22-26) */
+    FS_ERR_FORMAT = 8,       /* FormatError (errors.hpp:22-26) */
+    FS_ERR_SHARD_REACH = 9   /* a sharded fold read canvas pixels its GPU does not hold final:
+                                the result is not certified, execute unsharded */
 } fs_status;
 
 /* FlowParams (flow.hpp:36-44); defaults 4 / 8 / 3 / 1e-4 / 2. */
@@ -224,6 +226,49 @@ fs_status fs_plan_timeline(fs_plan plan, const uint8_t* const* views_rgba, uint8
 fs_status fs_plan_profile(fs_plan plan, void* stream, fs_kernel_stat* out, int max_out,
                           int* n_out, double* total_ms);
 void fs_plan_destroy(fs_plan plan);
+
+/* ---- seam sharding of one plan over GPUs ----
+ * Folds are assigned to ranks (one process per GPU, each holding the same
+ * plan); every rank computes the partitions and first-cover copies of all
+ * views and the flow, distance transforms and blend of its own folds.  A
+ * fold's Area3 "strip" (fold k's blended box, box_w*box_h float4) moves
+ * between ranks only where another fold's L crop needs it (Area3 boxes that
+ * meet) and to rank 0, the canvas GPU, which composes all strips in fold
+ * order and holds the RGBA8 panorama.  The execution is a sequence of
+ * segments; after segment s every transfer with stage s is done (by the
+ * caller: NCCL send/recv of the strip buffers, or device copies).  Blend taps
+ * that land outside what the rank holds final are detected on the device;
+ * fs_plan_check() then returns FS_ERR_SHARD_REACH and the caller runs the
+ * plan unsharded. */
+typedef struct {
+    int fold;   /* 1..n-1 */
+    int src;    /* rank that computes the strip */
+    int dst;    /* rank that needs it */
+    int stage;  /* after this segment */
+} fs_strip_xfer;
+/* Host-only schedule (no device needed).  boxes: fold k's Area3 box at
+ * boxes[4k..4k+3] (x0, y0, w, h; k >= 1).  fold_rank[k]: in, -1 (or NULL
+ * array) = assign by box area, longest first, to the least loaded rank; out,
+ * the rank.  stage[k]: the segment that computes fold k.  *n_segments =
+ * number of segments (last stage + 2).  xfers: every transfer of every rank. */
+fs_status fs_shard_schedule(int n, const int* boxes, int nranks, int* fold_rank, int* stage,
+                            int* n_segments, fs_strip_xfer* xfers, int max_xfers, int* n_xfers);
+/* configure `plan` as rank `rank` of `nranks` (fold_rank as above, may be
+ * NULL); nranks = 1 restores the unsharded plan. */
+fs_status fs_plan_shard(fs_plan plan, int nranks, int rank, const int* fold_rank);
+int fs_plan_shard_segments(fs_plan plan);
+/* kernel launches of this rank's captured segments (one execution) */
+int fs_plan_shard_launch_count(fs_plan plan);
+/* the transfers of this plan's rank after segment `segment` (sends and receives) */
+fs_status fs_plan_shard_xfers(fs_plan plan, int segment, fs_strip_xfer* out, int max_out,
+                              int* n_out);
+/* device buffer of fold k's strip (box_w * box_h float4) */
+fs_status fs_plan_strip_buffer(fs_plan plan, int fold, void** ptr, size_t* bytes);
+/* run segment `segment` (async on stream).  views_rgba (segment 0): host or
+ * device views copied in first (NULL: already in the plan's buffers);
+ * out_rgba (last segment, rank 0): the RGBA8 canvas copied out. */
+fs_status fs_plan_shard_execute(fs_plan plan, int segment, const uint8_t* const* views_rgba,
+                                uint8_t* out_rgba, void* stream);
 
 /* ---- runtime (parallel.hpp:9-18): kept for drop-in completeness; the GPU
  * path has no host worker pool, so these only record the value. ---- */

@@ -7,8 +7,9 @@ from . import _native
 from .api import *  # noqa: F401,F403
 from .api import __all__ as _api_all
 from .plan import Plan
+from .shard import ShardedPlan, shard_schedule
 
-__all__ = list(_api_all) + ["Plan", "device_available"]
+__all__ = list(_api_all) + ["Plan", "ShardedPlan", "shard_schedule", "device_available"]
 
 
 def device_available() -> bool:

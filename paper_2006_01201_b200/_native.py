@@ -22,7 +22,8 @@ lib = C.CDLL(LIB_PATH)
 FS_OK = 0
 STATUS_NAMES = {0: "FS_OK", 1: "FS_ERR_CONTRACT", 2: "FS_ERR_EMPTY_REGION", 3: "FS_ERR_LAYOUT",
                 4: "FS_ERR_CUDA", 5: "FS_ERR_OOM", 6: "FS_ERR_UNSUPPORTED", 7: "FS_ERR_IO",
-                8: "FS_ERR_FORMAT"}
+                8: "FS_ERR_FORMAT", 9: "FS_ERR_SHARD_REACH"}
+FS_ERR_SHARD_REACH = 9
 
 
 class FlowParams(C.Structure):
@@ -55,6 +56,12 @@ class PairStats(C.Structure):
                 ("blend_seconds", C.c_double), ("crop_box", C.c_int32 * 4),
                 ("misalignment_present", C.c_int32), ("misalignment_before", C.c_double),
                 ("misalignment_after", C.c_double)]
+
+
+class StripXfer(C.Structure):
+    """fs_strip_xfer: fold k's strip moves from rank src to rank dst after
+    segment `stage`."""
+    _fields_ = [("fold", C.c_int), ("src", C.c_int), ("dst", C.c_int), ("stage", C.c_int)]
 
 
 class KernelStat(C.Structure):
@@ -108,6 +115,14 @@ SIGNATURES = {
     "fs_plan_profile": (I, [P, P, C.POINTER(KernelStat), I, C.POINTER(I), C.POINTER(D)]),
     "fs_plan_timeline": (I, [P, PP, P, P, C.c_char_p, I]),
     "fs_plan_destroy": (None, [P]),
+    "fs_shard_schedule": (I, [I, P, I, P, P, C.POINTER(I), C.POINTER(StripXfer), I,
+                              C.POINTER(I)]),
+    "fs_plan_shard": (I, [P, I, I, P]),
+    "fs_plan_shard_segments": (I, [P]),
+    "fs_plan_shard_launch_count": (I, [P]),
+    "fs_plan_shard_xfers": (I, [P, I, C.POINTER(StripXfer), I, C.POINTER(I)]),
+    "fs_plan_strip_buffer": (I, [P, I, C.POINTER(P), C.POINTER(C.c_size_t)]),
+    "fs_plan_shard_execute": (I, [P, I, PP, P, P]),
     "fs_set_thread_count": (None, [I]),
     "fs_thread_count": (I, []),
 }

@@ -19,7 +19,7 @@ from ._native import BlendParams, FlowParams
 
 __all__ = [
     "FlowstitchError", "ContractError", "EmptyRegionError", "LayoutError", "IoError",
-    "FormatError", "DeviceError", "ImageBuf", "Mask", "Region", "RegionPartition", "CropResult",
+    "FormatError", "DeviceError", "ShardReachError", "ImageBuf", "Mask", "Region", "RegionPartition", "CropResult",
     "FlowField", "FlowParams", "DistanceField", "BlendField", "BlendParams", "PlacedImage",
     "PairStats", "StitchReport", "to_gray", "bilinear_sample", "bilinear_sample_batch",
     "compute_partition", "crop_overlap", "place_on_canvas", "build_pyramid", "dense_pyr_lk",
@@ -55,12 +55,18 @@ class FormatError(FlowstitchError):
     pass
 
 
+class ShardReachError(FlowstitchError):
+    """A seam-sharded fold's blend sampled panorama pixels its GPU does not
+    hold final: the sharded result is not certified (run unsharded)."""
+
+
 class DeviceError(FlowstitchError):
     """No usable sm_100 device, or a CUDA failure (there is no CPU fallback)."""
 
 
 _ERRORS = {1: ContractError, 2: EmptyRegionError, 3: LayoutError, 4: DeviceError,
-           5: DeviceError, 6: ContractError, 7: IoError, 8: FormatError}
+           5: DeviceError, 6: ContractError, 7: IoError, 8: FormatError,
+           9: ShardReachError}
 
 
 def _check(status: int) -> None:

@@ -120,6 +120,26 @@ struct FoldStats {
     int bx0, by0, bx1, by1;   // Area3 bbox (inclusive max), init (INT_MAX, INT_MAX, -1, -1)
     unsigned int edt_fail;    // bounded-domain EDT certificate failed (bit per mask)
     unsigned int box_mismatch;
+    unsigned int reach_fail;  // a blend tap read a canvas pixel this rank does not hold final
+};
+
+// Seam-sharded execution (fs_plan_shard): a fold runs on a GPU whose canvas
+// holds the panorama's values before that fold only where they are known to
+// be final — everything inside `allow` except the Area3 boxes listed in
+// `forbid` (earlier folds' strips not received, later folds already
+// composed).  The blend records a tap of L that lands elsewhere, and the
+// execution is repeated unsharded (fs_plan_check).
+struct ReachCheck {
+    int on = 0;
+    int n = 0;
+    Rect allow;
+    Rect forbid[kMaxDagViews];
+    __device__ __forceinline__ bool ok(int x, int y) const {
+        if (!allow.contains(x, y)) return false;
+        for (int i = 0; i < n; ++i)
+            if (forbid[i].contains(x, y)) return false;
+        return true;
+    }
 };
 
 struct CanvasCount {
@@ -235,8 +255,8 @@ void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, cudaStream_t);
 // owner != nullptr: the panorama's validity before fold `fold` is owner < fold
 template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
-                 const int*, const FoldStats*, double, double, float4*, float2*,
-                 const uint8_t* owner, int fold, cudaStream_t);
+                 const int*, FoldStats*, double, double, float4*, float2*,
+                 const uint8_t* owner, int fold, cudaStream_t, const ReachCheck* rc = nullptr);
 template <class V>
 void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
                    uchar4* out = nullptr);

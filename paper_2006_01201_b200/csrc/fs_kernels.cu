@@ -570,8 +570,9 @@ struct CanvasSampler {
 template <class V, class PV>
 __global__ void k_blend_area3(Canvas cv, PV pv, V view, Rect box, const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
-                              const int* __restrict__ d2, const FoldStats* st, double k,
-                              double coef, float4* __restrict__ out, float2* __restrict__ wgray) {
+                              const int* __restrict__ d2, FoldStats* st, double k,
+                              double coef, float4* __restrict__ out, float2* __restrict__ wgray,
+                              const ReachCheck rc) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
@@ -584,7 +585,16 @@ __global__ void k_blend_area3(Canvas cv, PV pv, V view, Rect box, const float2* 
     float2 rl = frl[o], lr = flr[o];
     float cl[3], cr[3];
     CanvasSampler<PV> L{cv.rgb, pv, cv.w};
-    bilinear_rgb(L, cv.w, cv.h, cv.ch, x + rl.x * (1.0 - blend_l), y + rl.y * (1.0 - blend_l), cl);
+    const double lx = x + rl.x * (1.0 - blend_l), ly = y + rl.y * (1.0 - blend_l);
+    if (rc.on) {
+        const BiTap t = bi_tap(cv.w, cv.h, lx, ly);
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (pv(t.xs[q], t.ys[q]) && !rc.ok(t.xs[q], t.ys[q])) bad = true;
+        if (bad) atomicOr(&st->reach_fail, 1u);
+    }
+    bilinear_rgb(L, cv.w, cv.h, cv.ch, lx, ly, cl);
     bilinear_rgb(view, cv.w, cv.h, cv.ch, x + lr.x * (1.0 - blend_r), y + lr.y * (1.0 - blend_r),
                  cr);
     double mag_rl = sqrt((double)rl.x * rl.x + (double)rl.y * rl.y);
@@ -785,17 +795,18 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, cudaStre
 
 template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
-                 const float2* frl, const int* d1, const int* d2, const FoldStats* st, double k,
+                 const float2* frl, const int* d1, const int* d2, FoldStats* st, double k,
                  double coef, float4* out, float2* wgray, const uint8_t* owner, int fold,
-                 cudaStream_t s) {
+                 cudaStream_t s, const ReachCheck* rc) {
+    const ReachCheck r = rc ? *rc : ReachCheck{};
     if (owner)
         k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
             cv, PanoOwnerBefore{owner, cv.w, fold}, view, box, flr, frl, d1, d2, st, k, coef, out,
-            wgray);
+            wgray, r);
     else
         k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
             cv, PanoValidPlane{cv.valid, cv.w}, view, box, flr, frl, d1, d2, st, k, coef, out,
-            wgray);
+            wgray, r);
 }
 template <class V>
 void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
@@ -871,11 +882,13 @@ template void compose_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, c
 template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
                                     const uint8_t*, int, cudaStream_t, uchar4*);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
-                                  const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t);
+                                  const float2*, const int*, const int*, FoldStats*, double,
+                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t,
+                                  const ReachCheck*);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
-                                  const float2*, const int*, const int*, const FoldStats*, double,
-                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t);
+                                  const float2*, const int*, const int*, FoldStats*, double,
+                                  double, float4*, float2*, const uint8_t*, int, cudaStream_t,
+                                  const ReachCheck*);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

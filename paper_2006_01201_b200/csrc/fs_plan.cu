@@ -69,6 +69,20 @@ struct fs_plan_s {
     // timeline capture (fs_plan_timeline): timing events at schedule points
     bool tl = false;
     std::vector<std::pair<std::string, cudaEvent_t>> tl_marks;
+    // seam sharding (fs_plan_shard): this rank's segments, one graph each
+    struct Shard {
+        int nranks = 1, rank = 0, nseg = 1;
+        std::vector<int> fold_rank, stage;
+        std::vector<fs_strip_xfer> xfers;          // every rank's transfers
+        std::vector<std::vector<int>> apply, own;  // per segment: strips composed, folds run
+        std::vector<ReachCheck> reach;             // per fold (own folds)
+        std::vector<int> wait_local;  // per fold: last same-segment local fold its crop needs
+        std::vector<cudaGraph_t> graph;
+        std::vector<cudaGraphExec_t> exec;
+        cudaEvent_t ev_seg = nullptr;
+        std::vector<int> launches;  // per segment
+        std::vector<const void*> hkey;  // host pointers captured into the segments
+    } shard;
 };
 
 namespace {
@@ -295,6 +309,244 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     return launches;
 }
 
+// ---- seam sharding ----
+bool rects_meet(const Rect& a, const Rect& b) {
+    Rect i = rect_inter(a, b);
+    return i.w > 0 && i.h > 0;
+}
+
+// The global schedule (identical on every rank): fold -> rank, fold -> stage
+// (the segment computing it), which ranks need which strips, the transfers.
+// Fold k's L crop needs the strips of D_k = {m < k : box m meets box k}; a
+// strip m needed on rank r is composed there at the start of segment
+// stage[m] + 1, in fold order, so stage[k] = max over D_k of stage[m]
+// (+1 when m runs elsewhere).  Rank 0 composes every strip.  A rank composing
+// strip j also needs j's own D_j first (the later strip must win where the
+// boxes meet).
+void shard_schedule(int n, const std::vector<Rect>& boxes, int nranks, std::vector<int>& fold_rank,
+                    std::vector<int>& stage, int& nseg, std::vector<fs_strip_xfer>& xfers,
+                    std::vector<std::vector<char>>& needed) {
+    if (nranks < 1) raise(FS_ERR_CONTRACT, "shard: nranks must be >= 1");
+    fold_rank.resize(n, -1);
+    fold_rank[0] = 0;
+    // list scheduling in fold order, earliest finish first: a fold costs its
+    // box area (the flow dominates), a strip moving to another rank 1/10 of
+    // its box; ties go to the rank that is not the canvas GPU, then the least
+    // loaded
+    std::vector<double> avail(nranks, 0.0), finish(n, 0.0);
+    for (int k = 1; k < n; ++k) {
+        if (fold_rank[k] >= nranks) raise(FS_ERR_CONTRACT, "shard: fold rank out of range");
+        const double cost = (double)boxes[k].area();
+        auto finish_on = [&](int r) {
+            double ready = 0.0;
+            for (int m = 1; m < k; ++m)
+                if (rects_meet(boxes[m], boxes[k]))
+                    ready = std::max(ready, finish[m] + (fold_rank[m] != r ? 0.1 * boxes[m].area() : 0.0));
+            return std::max(ready, avail[r]) + cost;
+        };
+        int best = fold_rank[k];
+        if (best < 0) {
+            double bf = 0.0;
+            for (int r = 0; r < nranks; ++r) {
+                const double f = finish_on(r);
+                const bool better = best < 0 || f < bf ||
+                                    (f == bf && ((best == 0 && r != 0) ||
+                                                 ((best == 0) == (r == 0) && avail[r] < avail[best])));
+                if (better) {
+                    best = r;
+                    bf = f;
+                }
+            }
+            fold_rank[k] = best;
+        }
+        finish[k] = finish_on(best);
+        avail[best] = finish[k];
+    }
+    stage.assign(n, 0);
+    int last = 0;
+    for (int k = 1; k < n; ++k) {
+        for (int m = 1; m < k; ++m)
+            if (rects_meet(boxes[m], boxes[k]))
+                stage[k] = std::max(stage[k], stage[m] + (fold_rank[m] != fold_rank[k] ? 1 : 0));
+        last = std::max(last, stage[k]);
+    }
+    nseg = last + 2;
+    needed.assign(nranks, std::vector<char>(n, 0));
+    for (int r = 0; r < nranks; ++r) {
+        for (int k = 1; k < n; ++k) {
+            if (fold_rank[k] == r) continue;
+            if (r == 0) needed[r][k] = 1;
+            for (int j = k + 1; j < n; ++j)
+                if (fold_rank[j] == r && rects_meet(boxes[k], boxes[j])) needed[r][k] = 1;
+        }
+        for (bool grew = true; grew;) {  // closure over the strips composed here
+            grew = false;
+            for (int j = n - 1; j >= 1; --j) {
+                if (!needed[r][j]) continue;
+                for (int m = 1; m < j; ++m)
+                    if (fold_rank[m] != r && !needed[r][m] && rects_meet(boxes[m], boxes[j])) {
+                        needed[r][m] = 1;
+                        grew = true;
+                    }
+            }
+        }
+    }
+    xfers.clear();
+    for (int st = 0; st <= last; ++st)
+        for (int m = 1; m < n; ++m) {
+            if (stage[m] != st) continue;
+            for (int r = 0; r < nranks; ++r)
+                if (needed[r][m]) xfers.push_back(fs_strip_xfer{m, fold_rank[m], r, st});
+        }
+}
+
+void shard_configure(fs_plan_s* p, int nranks, int rank, const int* fold_rank) {
+    if (!p->dag) raise(FS_ERR_UNSUPPORTED, "shard: needs the DAG schedule (n <= 16 views)");
+    if (rank < 0 || rank >= nranks) raise(FS_ERR_CONTRACT, "shard: rank out of range");
+    auto& S = p->shard;
+    for (auto e : S.exec)
+        if (e) cudaGraphExecDestroy(e);
+    for (auto g : S.graph)
+        if (g) cudaGraphDestroy(g);
+    S.exec.clear();
+    S.graph.clear();
+    S.nranks = nranks;
+    S.rank = rank;
+    const int n = p->n;
+    S.fold_rank.assign(n, -1);
+    if (fold_rank)
+        for (int k = 1; k < n; ++k) S.fold_rank[k] = fold_rank[k];
+    std::vector<std::vector<char>> needed;
+    shard_schedule(n, p->boxes, nranks, S.fold_rank, S.stage, S.nseg, S.xfers, needed);
+    S.apply.assign(S.nseg, {});
+    S.own.assign(S.nseg, {});
+    for (int k = 1; k < n; ++k) {
+        if (needed[rank][k]) S.apply[S.stage[k] + 1].push_back(k);
+        if (S.fold_rank[k] == rank) S.own[S.stage[k]].push_back(k);
+    }
+    // what the canvas holds final when each own fold runs
+    S.reach.assign(n, ReachCheck{});
+    S.wait_local.assign(n, 0);
+    std::vector<char> present(n, 0);
+    for (int sg = 0; sg < S.nseg; ++sg) {
+        for (int m : S.apply[sg]) present[m] = 1;
+        for (int k : S.own[sg]) {
+            ReachCheck& rc = S.reach[k];
+            rc.on = nranks > 1;
+            rc.allow = Rect{0, 0, p->cw, p->chh};
+            rc.n = 0;
+            for (int m = 1; m < n; ++m)
+                if (m != k && (m < k) != (present[m] != 0)) rc.forbid[rc.n++] = p->boxes[m];
+            for (int m = 1; m < k; ++m)
+                if (S.fold_rank[m] == rank && S.stage[m] == sg && rects_meet(p->boxes[m], p->boxes[k]))
+                    S.wait_local[k] = m;
+            present[k] = 1;
+        }
+    }
+    S.exec.assign(S.nseg, nullptr);
+    S.graph.assign(S.nseg, nullptr);
+    S.launches.assign(S.nseg, 0);
+    S.hkey.clear();
+    if (!S.ev_seg) FS_CK(cudaEventCreateWithFlags(&S.ev_seg, cudaEventDisableTiming));
+}
+
+// One segment of this rank's sharded execution on stream s.  Segment 0 also
+// does what every rank needs whatever folds it owns: view 0's placement, the
+// owner claims, every fold's partition counts and first-cover copies (the
+// L taps of a blend may read any first-cover pixel).  Then: compose the
+// strips received after the previous segment (fold order), run the own
+// folds of this segment (branch: crop, pyramid, flow, distance transforms;
+// chain on s: blend + compose).
+int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
+    const auto& S = p->shard;
+    uchar4* out = S.rank == 0 ? p->out : nullptr;
+    const bool hin = io && io->views;
+    int launches = 0;
+    if (seg == 0) {
+        FS_CK(cudaEventRecord(p->ev_start, s));
+        if (hin) {  // views land in fold order; each gates its claim and its fold
+            FS_CK(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
+            for (int k = 0; k < p->n; ++k) {
+                FS_CK(cudaMemcpyAsync(p->views[k], io->views[k],
+                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
+                                      cudaMemcpyDefault, p->h2d));
+                FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
+            }
+        }
+        FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
+        init_count(p->cc, s);
+        if (out) FS_CK(cudaMemsetAsync(out, 0, (size_t)p->cw * p->chh * 4, s));
+        if (hin) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[0], 0));
+        launch::place_view(p->cv, view_of(p, 0), p->cc, s, out);
+        launches += 2;
+        FS_CK(cudaEventRecord(p->ev_place, s));
+        FS_CK(cudaStreamWaitEvent(p->own, p->ev_start, 0));
+        FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
+        for (int k = 0; k < p->n; ++k) {
+            if (hin) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
+            launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own);
+            ++launches;
+            FS_CK(cudaEventRecord(p->ev_own[k], p->own));
+        }
+        for (int k = 1; k < p->n; ++k) {
+            FoldWS<ViewU8>& f = p->folds[k - 1];
+            cudaStream_t b = p->branch[k - 1];
+            if (hin) FS_CK(cudaStreamWaitEvent(b, p->ev_h2d[k], 0));
+            FS_CK(cudaStreamWaitEvent(b, p->ev_own[k - 1], 0));
+            launches += fold_enqueue_pre(f, views_before(p, k), view_of(p, k), b);
+            FS_CK(cudaStreamWaitEvent(b, k == 1 ? p->ev_place : p->ev_cnt[k - 1], 0));
+            launch::chain_count(f.st, k == 1 ? nullptr : p->folds[k - 2].st, p->cc, b);
+            FS_CK(cudaEventRecord(p->ev_cnt[k], b));
+            FS_CK(cudaStreamWaitEvent(b, p->ev_own[k], 0));
+            launch::compose_area2(p->cv, view_of(p, k), p->owner, k, b, out);
+            launches += 2;
+            FS_CK(cudaEventRecord(p->ev_a2[k], b));
+        }
+        // the chain reads first-cover pixels of every view
+        for (int k = 1; k < p->n; ++k) FS_CK(cudaStreamWaitEvent(s, p->ev_a2[k], 0));
+        FS_CK(cudaStreamWaitEvent(s, p->ev_own[p->n - 1], 0));
+    }
+    for (int m : S.apply[seg]) {
+        launch::compose_area3(p->cv, view_of(p, m), p->boxes[m], p->folds[m - 1].blended,
+                              p->owner, m, s, out);
+        ++launches;
+    }
+    FS_CK(cudaEventRecord(S.ev_seg, s));
+    const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
+    for (int k : S.own[seg]) {
+        FoldWS<ViewU8>& f = p->folds[k - 1];
+        ViewU8 v = view_of(p, k);
+        cudaStream_t b = p->branch[k - 1];
+        cudaStream_t es = p->edt_stream[k - 1];
+        const PanoViews pv = views_before(p, k);
+        if (seg > 0) FS_CK(cudaStreamWaitEvent(b, S.ev_seg, 0));
+        bool hybrid = false;
+        for (int m = 1; m < k; ++m) hybrid = hybrid || rects_meet(p->boxes[m], p->boxes[k]);
+        if (!hybrid) {
+            launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr, es,
+                                              p->ev_efork[k], p->ev_ejoin[k]);
+        } else {
+            FS_CK(cudaEventRecord(p->ev_efork[k], b));
+            FS_CK(cudaStreamWaitEvent(es, p->ev_efork[k], 0));
+            launches += fold_enqueue_edt(f, pv, v, es);
+            FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
+            if (S.wait_local[k]) FS_CK(cudaStreamWaitEvent(b, p->ev_compose[S.wait_local[k]], 0));
+            launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, nullptr,
+                                              nullptr, nullptr, nullptr, nullptr, false);
+            FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
+        }
+        FS_CK(cudaEventRecord(p->ev_branch[k], b));
+        FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
+        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, out,
+                                       &S.reach[k]);
+        FS_CK(cudaEventRecord(p->ev_compose[k], s));
+    }
+    if (seg == S.nseg - 1 && out && io && io->out)
+        FS_CK(cudaMemcpyAsync(io->out, out, (size_t)p->cw * p->chh * 4, cudaMemcpyDefault, s));
+    FS_CK(cudaGetLastError());
+    return launches;
+}
+
 void capture(fs_plan_s* p, const HostIO* io, cudaGraph_t* graph, cudaGraphExec_t* exec) {
     FS_CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
     int launches = 0;
@@ -312,6 +564,37 @@ void capture(fs_plan_s* p, const HostIO* io, cudaGraph_t* graph, cudaGraphExec_t
     p->launches = launches;
 }
 
+void capture_shard(fs_plan_s* p, int seg, const HostIO* io) {
+    auto& S = p->shard;
+    FS_CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+    try {
+        S.launches[seg] = enqueue_shard(p, p->cap, seg, io);
+    } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(p->cap, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    FS_CK(cudaStreamEndCapture(p->cap, &S.graph[seg]));
+    FS_CK(cudaGraphInstantiateWithFlags(&S.exec[seg], S.graph[seg],
+                                        cudaGraphInstantiateFlagUseNodePriority));
+}
+
+void drop_shard_graphs(fs_plan_s* p) {
+    auto& S = p->shard;
+    for (auto& e : S.exec)
+        if (e) {
+            cudaGraphExecDestroy(e);
+            e = nullptr;
+        }
+    for (auto& g : S.graph)
+        if (g) {
+            cudaGraphDestroy(g);
+            g = nullptr;
+        }
+    S.hkey.clear();
+}
+
 void build_graph(fs_plan_s* p) {
     if (!p->exec) capture(p, nullptr, &p->graph, &p->exec);
 }
@@ -326,6 +609,7 @@ void drop_graph(fs_plan_s* p) {
     p->hexec = nullptr;
     p->hgraph = nullptr;
     p->hkey.clear();
+    drop_shard_graphs(p);
 }
 
 // Page-locked (or device) memory can be read by a graph's copy nodes
@@ -671,6 +955,11 @@ fs_status fs_plan_check(fs_plan p) {
             if (hs[k].box_mismatch)
                 raise(FS_ERR_CONTRACT, "plan: the views' masks no longer produce the planned "
                                        "overlap of fold #" + std::to_string(k + 1));
+        for (size_t k = 0; k < p->folds.size(); ++k)
+            if (hs[k].reach_fail)
+                raise(FS_ERR_SHARD_REACH, "plan: sharded fold #" + std::to_string(k + 1) +
+                                              " sampled the panorama outside the strips its GPU "
+                                              "holds; execute unsharded");
         bool widened = false;
         for (size_t k = 0; k < p->folds.size(); ++k)
             if (hs[k].edt_fail && !p->folds[k].full_domain) {
@@ -831,6 +1120,122 @@ fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_
     });
 }
 
+fs_status fs_shard_schedule(int n, const int* boxes, int nranks, int* fold_rank, int* stage,
+                            int* n_segments, fs_strip_xfer* xfers, int max_xfers, int* n_xfers) {
+    return plan_guard([&] {
+        if (n < 2) raise(FS_ERR_CONTRACT, "shard: at least two images required");
+        std::vector<Rect> bx(n);
+        for (int k = 1; k < n; ++k)
+            bx[k] = Rect{boxes[4 * k], boxes[4 * k + 1], boxes[4 * k + 2], boxes[4 * k + 3]};
+        std::vector<int> fr(n, -1), stg;
+        if (fold_rank)
+            for (int k = 1; k < n; ++k) fr[k] = fold_rank[k];
+        int nseg = 0;
+        std::vector<fs_strip_xfer> xf;
+        std::vector<std::vector<char>> needed;
+        shard_schedule(n, bx, nranks, fr, stg, nseg, xf, needed);
+        if ((int)xf.size() > max_xfers) raise(FS_ERR_CONTRACT, "shard: transfer list too small");
+        if (fold_rank)
+            for (int k = 0; k < n; ++k) fold_rank[k] = fr[k];
+        if (stage)
+            for (int k = 0; k < n; ++k) stage[k] = stg[k];
+        if (n_segments) *n_segments = nseg;
+        for (size_t i = 0; i < xf.size(); ++i) xfers[i] = xf[i];
+        if (n_xfers) *n_xfers = (int)xf.size();
+    });
+}
+
+fs_status fs_plan_shard(fs_plan p, int nranks, int rank, const int* fold_rank) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        shard_configure(p, nranks, rank, fold_rank);
+    });
+}
+
+int fs_plan_shard_segments(fs_plan p) { return p ? p->shard.nseg : 0; }
+
+int fs_plan_shard_launch_count(fs_plan p) {
+    int n = 0;
+    if (p)
+        for (int l : p->shard.launches) n += l;
+    return n;
+}
+
+fs_status fs_plan_shard_xfers(fs_plan p, int segment, fs_strip_xfer* out, int max_out,
+                              int* n_out) {
+    return plan_guard([&] {
+        const auto& S = p->shard;
+        int n = 0;
+        for (const auto& x : S.xfers)
+            if (x.stage == segment && (x.src == S.rank || x.dst == S.rank)) {
+                if (n == max_out) raise(FS_ERR_CONTRACT, "shard: transfer list too small");
+                out[n++] = x;
+            }
+        *n_out = n;
+    });
+}
+
+fs_status fs_plan_strip_buffer(fs_plan p, int fold, void** ptr, size_t* bytes) {
+    if (!p || fold < 1 || fold >= p->n) return FS_ERR_CONTRACT;
+    const FoldWS<ViewU8>& f = p->folds[fold - 1];
+    *ptr = f.blended;
+    *bytes = (size_t)f.box.w * f.box.h * sizeof(float4);
+    return FS_OK;
+}
+
+fs_status fs_plan_shard_execute(fs_plan p, int segment, const uint8_t* const* views_rgba,
+                                uint8_t* out_rgba, void* stream) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        auto& S = p->shard;
+        if (segment < 0 || segment >= S.nseg) raise(FS_ERR_CONTRACT, "shard: segment out of range");
+        if ((int)S.exec.size() != S.nseg) shard_configure(p, S.nranks, S.rank, S.fold_rank.data());
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        // host buffers the graphs can copy asynchronously are captured into
+        // segment 0 (views, overlapping the folds) and the last segment (the
+        // canvas); others are copied around the graphs
+        const bool last = segment == S.nseg - 1;
+        const uint8_t* const* vin = segment == 0 ? views_rgba : nullptr;
+        uint8_t* hout = last && S.rank == 0 ? out_rgba : nullptr;
+        bool async = true;
+        for (int k = 0; vin && k < p->n; ++k) async = async && async_copyable(vin[k]);
+        if (hout) async = async && async_copyable(hout);
+        if (!async) {
+            for (int k = 0; vin && k < p->n; ++k)
+                FS_CK(cudaMemcpyAsync(p->views[k], vin[k],
+                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
+                                      cudaMemcpyDefault, s));
+            vin = nullptr;
+        }
+        // one key per segment slot: views (segment 0) / canvas (last segment)
+        if (S.hkey.size() != (size_t)p->n + 1) S.hkey.assign(p->n + 1, nullptr);
+        auto rekey = [&](size_t i, const void* v) {
+            if (S.hkey[i] != v) {
+                S.hkey[i] = v;
+                return true;
+            }
+            return false;
+        };
+        bool stale = false;
+        if (segment == 0)
+            for (int k = 0; k < p->n; ++k) stale = rekey(k, vin ? vin[k] : nullptr) || stale;
+        if (last) stale = rekey(p->n, async ? hout : nullptr) || stale;
+        if (stale && S.exec[segment]) {
+            cudaGraphExecDestroy(S.exec[segment]);
+            cudaGraphDestroy(S.graph[segment]);
+            S.exec[segment] = nullptr;
+            S.graph[segment] = nullptr;
+        }
+        if (!S.exec[segment]) {
+            HostIO io{vin, async ? hout : nullptr};
+            capture_shard(p, segment, &io);
+        }
+        FS_CK(cudaGraphLaunch(S.exec[segment], s));
+        if (hout && !async)
+            FS_CK(cudaMemcpyAsync(hout, p->out, (size_t)p->cw * p->chh * 4, cudaMemcpyDefault, s));
+    });
+}
+
 void fs_plan_destroy(fs_plan p) {
     if (!p) return;
     drop_graph(p);
@@ -862,6 +1267,7 @@ void fs_plan_destroy(fs_plan p) {
     if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->arena) cudaFree(p->arena);
     if (p->hstats) cudaFreeHost(p->hstats);
+    if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;
 }
