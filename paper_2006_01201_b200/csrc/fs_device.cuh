@@ -232,7 +232,9 @@ void init();     // one-time kernel attributes (call before any graph capture)
 void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 // owner[p] = k where view k is valid and no earlier view claimed p
-void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t);
+// (hist: += the pixels claimed, at hist[k])
+void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t,
+                 unsigned long long* hist = nullptr);
 // out != nullptr: also the RGBA8 value of every valid pixel written
 template <class V>
 void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t, uchar4* out = nullptr);
@@ -259,7 +261,10 @@ void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const floa
                  const uint8_t* owner, int fold, cudaStream_t, const ReachCheck* rc = nullptr);
 template <class V>
 void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
-                   uchar4* out = nullptr);
+                   uchar4* out = nullptr, const Rect* clip = nullptr,
+                   const Rect* cv_clip = nullptr);  // float canvas written only inside cv_clip
+// pv_count of fold k = sum of hist[m] over m < k
+void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaStream_t);
 template <class V>
 void compose_area3(const Canvas&, const V&, const Rect& box, const float4*, const uint8_t* owner,
                    int fold, cudaStream_t, uchar4* out = nullptr);

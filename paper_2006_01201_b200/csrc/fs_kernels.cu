@@ -4,6 +4,7 @@
 // -fmad=false keeps every float/double expression that mirrors the reference
 // un-contracted, which is what makes the outputs bit-comparable with the
 // reference's Release build (no -march, hence no FMA).
+#include <algorithm>
 #include <climits>
 
 #include "fs_device.cuh"
@@ -132,6 +133,14 @@ __global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
 }
 __global__ void k_chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc) {
     st->pv_count = prev ? prev->pv_count + prev->cnt2 : cc->valid_count;
+}
+
+// |pano valid| before fold k from the claims' counts (hist[m]: pixels first
+// covered by view m)
+__global__ void k_count_from_hist(FoldStats* st, const unsigned long long* hist, int k) {
+    unsigned long long c = 0;
+    for (int m = 0; m < k; ++m) c += hist[m];
+    st->pv_count = c;
 }
 
 // src/image.cpp:134-162 then src/image.cpp:70-83: crop of both sides over the
@@ -633,17 +642,53 @@ __global__ void k_compose(Canvas cv, V view, Rect box, const float4* __restrict_
 // written on the fold's branch as soon as the view is claimed; only its Area3
 // (the blended box) is written in the ordered chain.
 template <class V>
-__global__ void k_compose_area2(Canvas cv, V view, const uint8_t* __restrict__ owner, int k,
-                                uchar4* __restrict__ out) {
-    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = view.rect.y0 + blockIdx.y;
-    if (x >= view.rect.x1()) return;
-    const size_t p = (size_t)y * cv.w + x;
-    if (owner[p] != k) return;
-    const float4 v = view.value_at(x, y);
-    cv.rgb[p] = v;
-    cv.valid[p] = 1;
-    if (out) out[p] = quantize_px(v, cv.ch);
+__global__ void __launch_bounds__(256) k_compose_area2(Canvas cv, V view,
+                                                       const uint8_t* __restrict__ owner, int k,
+                                                       uchar4* __restrict__ out, Rect r,
+                                                       Rect cvr) {
+    // 4 pixels per thread: one aligned word of the owner plane; rows strided
+    // over the grid.  The 8-bit value of a view byte b is b itself
+    // (lroundf((b * (1/255.f)) * 255.f) == b for every b: checked exhaustively).
+    const float sc = 1.0f / 255.0f;
+    for (int y = r.y0 + blockIdx.y; y < r.y1(); y += gridDim.y) {
+        const size_t row = (size_t)y * cv.w;
+        const int lead = (int)((row + (size_t)r.x0) & 3);
+        const int x = r.x0 - lead + 4 * (int)(blockIdx.x * blockDim.x + threadIdx.x);
+        if (x >= r.x1()) continue;
+        const uchar4 o = *reinterpret_cast<const uchar4*>(owner + row + x);
+        const bool m0 = o.x == k && x >= r.x0, m1 = o.y == k && x + 1 >= r.x0 && x + 1 < r.x1(),
+                   m2 = o.z == k && x + 2 >= r.x0 && x + 2 < r.x1(), m3 = o.w == k && x + 3 < r.x1();
+        if (!(m0 | m1 | m2 | m3)) continue;
+        const uchar4* src = view.px + (size_t)(y - view.rect.y0) * view.rect.w + (x - view.rect.x0);
+        const bool mine[4] = {m0, m1, m2, m3};
+        uchar4 q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = mine[j] ? src[j] : make_uchar4(0, 0, 0, 0);
+        const bool cv_row = y >= cvr.y0 && y < cvr.y1();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!mine[j]) continue;
+            if (cv_row && x + j >= cvr.x0 && x + j < cvr.x1()) {  // the float canvas where it is read
+                cv.rgb[row + x + j] = make_float4(q[j].x * sc, q[j].y * sc, q[j].z * sc, 0.f);
+                cv.valid[row + x + j] = 1;
+            }
+            q[j].w = 255;
+            if (cv.ch != 3) q[j].y = q[j].z = q[j].x;
+        }
+        if (!out) continue;
+        if (m0 & m1 & m2 & m3) {  // the word is this view's: one store
+            uint4 w4;
+            w4.x = *reinterpret_cast<const unsigned int*>(&q[0]);
+            w4.y = *reinterpret_cast<const unsigned int*>(&q[1]);
+            w4.z = *reinterpret_cast<const unsigned int*>(&q[2]);
+            w4.w = *reinterpret_cast<const unsigned int*>(&q[3]);
+            *reinterpret_cast<uint4*>(out + row + x) = w4;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (mine[j]) out[row + x + j] = q[j];
+        }
+    }
 }
 template <class V>
 __global__ void k_compose_area3(Canvas cv, V view, Rect box, const float4* __restrict__ blended,
@@ -669,12 +714,46 @@ __global__ void k_union_valid(Canvas cv, V view) {
     if (view.valid_at(x, y)) cv.valid[(size_t)y * cv.w + x] = 1;
 }
 
-__global__ void k_claim_owner(uint8_t* __restrict__ owner, int w, ViewU8 view, int k) {
-    const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = view.rect.y0 + blockIdx.y;
-    if (x >= view.rect.x1()) return;
-    uint8_t* o = owner + (size_t)y * w + x;
-    if (*o == 0xFF && view.valid_at(x, y)) *o = (uint8_t)k;
+// 4 owner bytes per thread (one aligned 32-bit word of the plane; bytes of
+// the word outside the view are written back unchanged), rows strided over
+// the grid; with `hist`, the claimed pixels are counted into hist[k] (one
+// atomic per block).
+__global__ void __launch_bounds__(256) k_claim_owner(uint8_t* __restrict__ owner, int w,
+                                                     ViewU8 view, int k,
+                                                     unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int red[8];
+    unsigned int claimed = 0;
+    for (int y = view.rect.y0 + blockIdx.y; y < view.rect.y1(); y += gridDim.y) {
+        const size_t row = (size_t)y * w;
+        const size_t f = ((row + view.rect.x0) & ~(size_t)3) +
+                         4 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+        if (f >= row + view.rect.x1()) continue;
+        uchar4 o = *reinterpret_cast<const uchar4*>(owner + f);
+        uint8_t b[4] = {o.x, o.y, o.z, o.w};
+        const uchar4* src = view.px + (size_t)(y - view.rect.y0) * view.rect.w;
+        unsigned int c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long long x = (long long)(f + j) - (long long)row;
+            if (x >= view.rect.x0 && x < view.rect.x1() && b[j] == 0xFF &&
+                src[x - view.rect.x0].w >= 128) {
+                b[j] = (uint8_t)k;
+                ++c;
+            }
+        }
+        if (c) *reinterpret_cast<uchar4*>(owner + f) = make_uchar4(b[0], b[1], b[2], b[3]);
+        claimed += c;
+    }
+    if (hist) {
+        for (int d = 16; d; d >>= 1) claimed += __shfl_xor_sync(0xffffffffu, claimed, d);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = claimed;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int i = 0; i < 8; ++i) t += red[i];
+            if (t) atomicAdd(&hist[k], t);
+        }
+    }
 }
 
 __global__ void k_count_update(CanvasCount* cc, const FoldStats* st) {
@@ -810,8 +889,21 @@ void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2*
 }
 template <class V>
 void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
-                   cudaStream_t s, uchar4* out) {
-    k_compose_area2<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view, owner, fold, out);
+                   cudaStream_t s, uchar4* out, const Rect* clip, const Rect* cv_clip) {
+    Rect r = view.rect;
+    if (clip) {  // the part of the view inside clip
+        const int x0 = max(r.x0, clip->x0), y0 = max(r.y0, clip->y0);
+        const int x1 = min(r.x1(), clip->x1()), y1 = min(r.y1(), clip->y1());
+        r = Rect{x0, y0, x1 - x0, y1 - y0};
+        if (r.w <= 0 || r.h <= 0) return;
+    }
+    const Rect cvr = cv_clip ? *cv_clip : Rect{0, 0, cv.w, cv.h};
+    const int bx = ((r.w + 3) / 4 + 1 + 255) / 256;
+    const int by = std::min(r.h, std::max(1, 148 * 8 / bx));
+    k_compose_area2<<<dim3(bx, by), 256, 0, s>>>(cv, view, owner, fold, out, r, cvr);
+}
+void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaStream_t s) {
+    k_count_from_hist<<<1, 1, 0, s>>>(st, hist, k);
 }
 template <class V>
 void compose_area3(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -829,8 +921,12 @@ template <class V>
 void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
-void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t s) {
-    k_claim_owner<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(owner, w, view, k);
+void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t s,
+                 unsigned long long* hist) {
+    const int words = (view.rect.w + 3) / 4 + 1;  // the row's span may straddle one more word
+    const int bx = (words + 255) / 256;
+    const int by = std::min(view.rect.h, std::max(1, 148 * 8 / bx));
+    k_claim_owner<<<dim3(bx, by), 256, 0, s>>>(owner, w, view, k, hist);
 }
 void quantize(const Canvas& cv, uchar4* out, cudaStream_t s) {
     quantize_rect(cv, Rect{0, 0, cv.w, cv.h}, out, s);
@@ -876,7 +972,7 @@ template void edt<PlaneMask>(const EdtJob<PlaneMask>&, const EdtJob<PlaneMask>&,
 template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
                              const FoldStats*, cudaStream_t);
 template void compose_area2<ViewU8>(const Canvas&, const ViewU8&, const uint8_t*, int,
-                                    cudaStream_t, uchar4*);
+                                    cudaStream_t, uchar4*, const Rect*, const Rect*);
 template void compose_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                                     const uint8_t*, int, cudaStream_t, uchar4*);
 template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

@@ -14,6 +14,10 @@
 
 using namespace fs;
 
+// first-cover copies a sharded rank keeps around each own fold's Area3 box:
+// a blend tap farther out is refused (ReachCheck) and the panorama runs unsharded
+constexpr int kShardMargin = 128;
+
 struct fs_plan_s {
     int device = 0;
     int n = 0;
@@ -82,6 +86,9 @@ struct fs_plan_s {
         cudaEvent_t ev_seg = nullptr;
         std::vector<int> launches;  // per segment
         std::vector<const void*> hkey;  // host pointers captured into the segments
+        Rect clip;                          // first-cover copies needed here (rank != 0)
+        unsigned long long* hist = nullptr;  // owner-plane histogram (|pano valid| per fold)
+        cudaEvent_t ev_hist = nullptr;
     } shard;
 };
 
@@ -424,8 +431,10 @@ void shard_configure(fs_plan_s* p, int nranks, int rank, const int* fold_rank) {
         if (needed[rank][k]) S.apply[S.stage[k] + 1].push_back(k);
         if (S.fold_rank[k] == rank) S.own[S.stage[k]].push_back(k);
     }
-    // what the canvas holds final when each own fold runs
+    // what the canvas holds final when each own fold runs: first-cover
+    // copies within kShardMargin of the fold's box, the strips composed here
     S.reach.assign(n, ReachCheck{});
+    S.clip = Rect{0, 0, 0, 0};
     S.wait_local.assign(n, 0);
     std::vector<char> present(n, 0);
     for (int sg = 0; sg < S.nseg; ++sg) {
@@ -433,7 +442,12 @@ void shard_configure(fs_plan_s* p, int nranks, int rank, const int* fold_rank) {
         for (int k : S.own[sg]) {
             ReachCheck& rc = S.reach[k];
             rc.on = nranks > 1;
-            rc.allow = Rect{0, 0, p->cw, p->chh};
+            const Rect& b = p->boxes[k];
+            const int x0 = std::max(0, b.x0 - kShardMargin), y0 = std::max(0, b.y0 - kShardMargin);
+            const int x1 = std::min(p->cw, b.x1() + kShardMargin);
+            const int y1 = std::min(p->chh, b.y1() + kShardMargin);
+            rc.allow = nranks == 1 ? Rect{0, 0, p->cw, p->chh} : Rect{x0, y0, x1 - x0, y1 - y0};
+            S.clip = rect_union(S.clip, rc.allow);
             rc.n = 0;
             for (int m = 1; m < n; ++m)
                 if (m != k && (m < k) != (present[m] != 0)) rc.forbid[rc.n++] = p->boxes[m];
@@ -448,6 +462,8 @@ void shard_configure(fs_plan_s* p, int nranks, int rank, const int* fold_rank) {
     S.launches.assign(S.nseg, 0);
     S.hkey.clear();
     if (!S.ev_seg) FS_CK(cudaEventCreateWithFlags(&S.ev_seg, cudaEventDisableTiming));
+    if (!S.ev_hist) FS_CK(cudaEventCreateWithFlags(&S.ev_hist, cudaEventDisableTiming));
+    if (!S.hist) FS_CK(cudaMalloc(&S.hist, sizeof(unsigned long long) * kMaxDagViews));
 }
 
 // One segment of this rank's sharded execution on stream s.  Segment 0 also
@@ -473,38 +489,48 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
                 FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
             }
         }
-        FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
-        init_count(p->cc, s);
+        // the canvas writers (first-cover copies) start after the clear
         if (out) FS_CK(cudaMemsetAsync(out, 0, (size_t)p->cw * p->chh * 4, s));
-        if (hin) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[0], 0));
-        launch::place_view(p->cv, view_of(p, 0), p->cc, s, out);
-        launches += 2;
         FS_CK(cudaEventRecord(p->ev_place, s));
-        FS_CK(cudaStreamWaitEvent(p->own, p->ev_start, 0));
+        FS_CK(cudaStreamWaitEvent(p->own, p->ev_place, 0));
         FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
+        // the claims count their pixels: |pano valid| before fold k is the sum
+        // of hist[m] over m < k (no partition chain over the other folds)
+        FS_CK(cudaMemsetAsync(S.hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->own));
         for (int k = 0; k < p->n; ++k) {
             if (hin) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
-            launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own);
+            launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own, S.hist);
             ++launches;
             FS_CK(cudaEventRecord(p->ev_own[k], p->own));
         }
+        FS_CK(cudaEventRecord(S.ev_hist, p->own));
+        // first-cover copies: the whole canvas on rank 0 (its RGBA8 panorama),
+        // around the own folds' boxes elsewhere (their blends' L taps)
+        const Rect* clip = S.rank == 0 ? nullptr : &S.clip;
+        if (S.rank == 0 || S.clip.w > 0) {
+            FS_CK(cudaStreamWaitEvent(s, p->ev_own[0], 0));
+            launch::compose_area2(p->cv, view_of(p, 0), p->owner, 0, s, out, clip, &S.clip);
+            ++launches;
+        }
         for (int k = 1; k < p->n; ++k) {
+            const bool mine = S.fold_rank[k] == S.rank;
+            if (!mine && S.rank != 0 && S.clip.w <= 0) continue;
             FoldWS<ViewU8>& f = p->folds[k - 1];
             cudaStream_t b = p->branch[k - 1];
             if (hin) FS_CK(cudaStreamWaitEvent(b, p->ev_h2d[k], 0));
-            FS_CK(cudaStreamWaitEvent(b, p->ev_own[k - 1], 0));
-            launches += fold_enqueue_pre(f, views_before(p, k), view_of(p, k), b);
-            FS_CK(cudaStreamWaitEvent(b, k == 1 ? p->ev_place : p->ev_cnt[k - 1], 0));
-            launch::chain_count(f.st, k == 1 ? nullptr : p->folds[k - 2].st, p->cc, b);
-            FS_CK(cudaEventRecord(p->ev_cnt[k], b));
+            if (mine) {  // the fold's own partition (Area counts, box, statistics)
+                FS_CK(cudaStreamWaitEvent(b, p->ev_own[k - 1], 0));
+                launches += fold_enqueue_pre(f, views_before(p, k), view_of(p, k), b);
+                launch::count_from_hist(f.st, S.hist, k, b);  // claims < k are in
+                ++launches;
+            }
             FS_CK(cudaStreamWaitEvent(b, p->ev_own[k], 0));
-            launch::compose_area2(p->cv, view_of(p, k), p->owner, k, b, out);
-            launches += 2;
+            launch::compose_area2(p->cv, view_of(p, k), p->owner, k, b, out, clip, &S.clip);
+            ++launches;
             FS_CK(cudaEventRecord(p->ev_a2[k], b));
+            FS_CK(cudaStreamWaitEvent(s, p->ev_a2[k], 0));
         }
-        // the chain reads first-cover pixels of every view
-        for (int k = 1; k < p->n; ++k) FS_CK(cudaStreamWaitEvent(s, p->ev_a2[k], 0));
-        FS_CK(cudaStreamWaitEvent(s, p->ev_own[p->n - 1], 0));
+        FS_CK(cudaStreamWaitEvent(s, S.ev_hist, 0));
     }
     for (int m : S.apply[seg]) {
         launch::compose_area3(p->cv, view_of(p, m), p->boxes[m], p->folds[m - 1].blended,
@@ -1268,6 +1294,8 @@ void fs_plan_destroy(fs_plan p) {
     if (p->arena) cudaFree(p->arena);
     if (p->hstats) cudaFreeHost(p->hstats);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
+    if (p->shard.ev_hist) cudaEventDestroy(p->shard.ev_hist);
+    if (p->shard.hist) cudaFree(p->shard.hist);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;
 }
