@@ -223,6 +223,10 @@ typedef struct {
  * JSON object {"label": ms since start} into json (cap bytes). */
 fs_status fs_plan_timeline(fs_plan plan, const uint8_t* const* views_rgba, uint8_t* out_rgba,
                            void* stream, char* json, int cap);
+/* The same points inside the production CUDA graph itself (a one-warp
+ * %globaltimer stamp kernel at each point; third replay reported). */
+fs_status fs_plan_timeline_graph(fs_plan plan, const uint8_t* const* views_rgba,
+                                 uint8_t* out_rgba, void* stream, char* json, int cap);
 fs_status fs_plan_profile(fs_plan plan, void* stream, fs_kernel_stat* out, int max_out,
                           int* n_out, double* total_ms);
 void fs_plan_destroy(fs_plan plan);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "fs_plan_fold_info": (I, [P, I, P, P]),
     "fs_plan_profile": (I, [P, P, C.POINTER(KernelStat), I, C.POINTER(I), C.POINTER(D)]),
     "fs_plan_timeline": (I, [P, PP, P, P, C.c_char_p, I]),
+    "fs_plan_timeline_graph": (I, [P, PP, P, P, C.c_char_p, I]),
     "fs_plan_destroy": (None, [P]),
     "fs_shard_schedule": (I, [I, P, I, P, P, C.POINTER(I), C.POINTER(StripXfer), I,
                               C.POINTER(I)]),

@@ -229,6 +229,7 @@ struct EdtJob {
 
 namespace launch {
 void init();     // one-time kernel attributes (call before any graph capture)
+void stamp(unsigned long long* slot, cudaStream_t);  // %globaltimer (ns) into *slot
 void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 // owner[p] = k where view k is valid and no earlier view claimed p

@@ -921,6 +921,12 @@ template <class V>
 void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
+__global__ void k_stamp(unsigned long long* t) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    if (threadIdx.x == 0) *t = v;
+}
+void stamp(unsigned long long* slot, cudaStream_t s) { k_stamp<<<1, 32, 0, s>>>(slot); }
 void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t s,
                  unsigned long long* hist) {
     const int words = (view.rect.w + 3) / 4 + 1;  // the row's span may straddle one more word

@@ -14,6 +14,8 @@
 
 using namespace fs;
 
+constexpr size_t kMaxStamps = 512;
+
 // first-cover copies a sharded rank keeps around each own fold's Area3 box:
 // a blend tap farther out is refused (ReachCheck) and the panorama runs unsharded
 constexpr int kShardMargin = 128;
@@ -73,6 +75,10 @@ struct fs_plan_s {
     // timeline capture (fs_plan_timeline): timing events at schedule points
     bool tl = false;
     std::vector<std::pair<std::string, cudaEvent_t>> tl_marks;
+    // graph timeline (fs_plan_timeline_graph): %globaltimer stamp kernels
+    bool tl_stamp = false;
+    unsigned long long* stamps = nullptr;
+    std::vector<std::string> stamp_labels;
     // seam sharding (fs_plan_shard): this rank's segments, one graph each
     struct Shard {
         int nranks = 1, rank = 0, nseg = 1;
@@ -151,6 +157,13 @@ struct HostIO {
 int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullptr) {
     int launches = 0;
     auto mark = [&](const std::string& label, cudaStream_t st) -> cudaEvent_t {
+        if (p->tl_stamp) {
+            if (p->stamp_labels.size() < kMaxStamps) {
+                launch::stamp(p->stamps + p->stamp_labels.size(), st);
+                p->stamp_labels.push_back(label);
+            }
+            return nullptr;
+        }
         if (!p->tl) return nullptr;
         cudaEvent_t e;
         FS_CK(cudaEventCreate(&e));
@@ -176,8 +189,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
                 FS_CK(cudaMemcpyAsync(p->views[k], io->views[k],
                                       (size_t)p->rects[k].w * p->rects[k].h * 4,
                                       cudaMemcpyDefault, p->h2d));
-                FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
                 mark("h2d_" + std::to_string(k), p->h2d);
+                FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
             }
         }
     }
@@ -275,6 +288,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         launch::compose_area2(p->cv, v, p->owner, k, b, p->out);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_a2[k], b));
+        if (p->tl_stamp && p->crop_wait[k] == 0) mark("fold" + fk + "_flow_start", b);
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
         cudaStream_t es = p->edt_stream[k - 1];
         if (p->crop_wait[k] == 0) {
@@ -287,12 +301,13 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             launches += fold_enqueue_edt(f, pv, v, es);
             FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
             FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
+            if (p->tl_stamp) mark("fold" + fk + "_flow_start", b);
             launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1,
                                               nullptr, nullptr, nullptr, false);
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
-        FS_CK(cudaEventRecord(p->ev_branch[k], b));
         mark("fold" + fk + "_edt_end", b);
+        FS_CK(cudaEventRecord(p->ev_branch[k], b));
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         mark("fold" + fk + "_blend_start", s);
         launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out);
@@ -862,7 +877,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             if (r.w <= 0 || r.h <= 0) raise(FS_ERR_CONTRACT, "plan: empty view");
             p->rects.push_back(r);
         }
-        FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
         std::vector<Rect> boxes = views_rgba ? boxes_from_masks(p, views_rgba) : boxes_from_rects(p);
         // DAG: fold k's L crop may come straight from the views when no earlier
         // fold's Area3 box overlaps its own (those pixels hold the first
@@ -1101,6 +1116,51 @@ fs_status fs_plan_timeline(fs_plan p, const uint8_t* const* views_rgba, uint8_t*
     });
 }
 
+fs_status fs_plan_timeline_graph(fs_plan p, const uint8_t* const* views_rgba, uint8_t* out_rgba,
+                                 void* stream, char* json, int cap) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        if (!p->dag) raise(FS_ERR_UNSUPPORTED, "plan: timeline needs the DAG schedule");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        HostIO io{views_rgba, out_rgba};
+        if (!p->stamps) FS_CK(cudaMalloc(&p->stamps, sizeof(unsigned long long) * kMaxStamps));
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t e = nullptr;
+        const int saved = p->launches;
+        p->tl_stamp = true;
+        p->stamp_labels.clear();
+        auto cleanup = [&] {
+            p->tl_stamp = false;
+            if (e) cudaGraphExecDestroy(e);
+            if (g) cudaGraphDestroy(g);
+            p->launches = saved;
+        };
+        try {
+            // the production graph with stamp kernels at the schedule points
+            capture(p, (views_rgba || out_rgba) ? &io : nullptr, &g, &e);
+            for (int rep = 0; rep < 3; ++rep) FS_CK(cudaGraphLaunch(e, s));
+            FS_CK(cudaStreamSynchronize(s));
+            std::vector<unsigned long long> t(p->stamp_labels.size());
+            FS_CK(cudaMemcpy(t.data(), p->stamps, sizeof(unsigned long long) * t.size(),
+                             cudaMemcpyDeviceToHost));
+            std::string js = "{";
+            for (size_t i = 0; i < t.size(); ++i) {
+                char item[160];
+                std::snprintf(item, sizeof item, "%s\"%s\": %.4f", i ? ", " : "",
+                              p->stamp_labels[i].c_str(), (double)(t[i] - t[0]) * 1e-6);
+                js += item;
+            }
+            js += "}";
+            if ((int)js.size() + 1 > cap) raise(FS_ERR_CONTRACT, "plan: timeline buffer too small");
+            std::memcpy(json, js.c_str(), js.size() + 1);
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    });
+}
+
 fs_status fs_plan_profile(fs_plan p, void* stream, fs_kernel_stat* out, int max_out, int* n_out,
                           double* total_ms) {
     return plan_guard([&] {
@@ -1293,6 +1353,7 @@ void fs_plan_destroy(fs_plan p) {
     if (p->d2h) cudaStreamDestroy(p->d2h);
     if (p->arena) cudaFree(p->arena);
     if (p->hstats) cudaFreeHost(p->hstats);
+    if (p->stamps) cudaFree(p->stamps);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
     if (p->shard.ev_hist) cudaEventDestroy(p->shard.ev_hist);
     if (p->shard.hist) cudaFree(p->shard.hist);

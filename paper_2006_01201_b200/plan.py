@@ -102,6 +102,18 @@ class Plan:
         import json
         return json.loads(buf.value.decode())
 
+    def timeline_graph(self, view_ptrs: Optional[Sequence[int]] = None,
+                       out_ptr: Optional[int] = None, stream: int = 0) -> dict:
+        """The schedule points inside the production graph (%globaltimer
+        stamp kernels), ms since the first."""
+        arg = C.cast((C.c_void_p * self.n)(*view_ptrs), N.PP) if view_ptrs else None
+        buf = C.create_string_buffer(1 << 16)
+        _raise(N.lib.fs_plan_timeline_graph(self._h, arg,
+                                            C.c_void_p(out_ptr) if out_ptr else None,
+                                            C.c_void_p(stream), buf, len(buf)))
+        import json
+        return json.loads(buf.value.decode())
+
     def profile(self, stream: int = 0):
         """One un-captured execution with CUDA events around every launch.
         Returns ({family: {"launches", "ms", "bytes"}}, total_ms)."""

@@ -22,7 +22,10 @@ def main():
     out = torch.empty((lay.canvas_h, lay.canvas_w, 4), dtype=torch.uint8).pin_memory()
     dev = plan.timeline()
     host = plan.timeline([t.data_ptr() for t in pin], out.data_ptr())
-    print(json.dumps({"device": dev, "host": host}, indent=1))
+    gdev = plan.timeline_graph()
+    ghost = plan.timeline_graph([t.data_ptr() for t in pin], out.data_ptr())
+    print(json.dumps({"device": dev, "host": host, "graph_device": gdev, "graph_host": ghost},
+                     indent=1))
 
 
 if __name__ == "__main__":
