@@ -877,7 +877,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             if (r.w <= 0 || r.h <= 0) raise(FS_ERR_CONTRACT, "plan: empty view");
             p->rects.push_back(r);
         }
-FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+        FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
         std::vector<Rect> boxes = views_rgba ? boxes_from_masks(p, views_rgba) : boxes_from_rects(p);
         // DAG: fold k's L crop may come straight from the views when no earlier
         // fold's Area3 box overlaps its own (those pixels hold the first
