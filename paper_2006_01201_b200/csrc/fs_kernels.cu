@@ -519,8 +519,8 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st) 
 // box, and the composition onto the canvas (src/blender.cpp:66-71,
 // src/pipeline.cpp:201-204).
 // ============================================================================
-template <class S>
-__device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, double x, double y,
+template <int CH, class S>
+__device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, double x, double y,
                                              float out[3]) {
     BiTap t = bi_tap(W, H, x, y);
     bool v[4];
@@ -538,15 +538,24 @@ __device__ __forceinline__ void bilinear_rgb(const S& s, int W, int H, int ch, d
         out[0] = out[1] = out[2] = 0.f;
         return;
     }
-    const double inv = 1.0 / wsum;  // one division for the channels
-    for (int c = 0; c < ch; ++c) {
-        double acc = 0.0;
+    double acc[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        acc[c] = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            float pv = c == 0 ? px[k].x : (c == 1 ? px[k].y : px[k].z);
-            if (v[k]) acc += t.ws[k] * pv;
+            const float pv = c == 0 ? px[k].x : (c == 1 ? px[k].y : px[k].z);
+            if (v[k]) acc[c] += t.ws[k] * pv;
         }
-        out[c] = div_to_float(acc, wsum, inv);
+    }
+    // all taps valid and the weights summing to exactly 1.0 (~97% of the
+    // pixels): acc / 1.0 == acc, no division
+    if (wsum == 1.0) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) out[c] = static_cast<float>(acc[c]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) out[c] = static_cast<float>(acc[c] / wsum);
     }
 }
 
@@ -576,8 +585,12 @@ struct CanvasSampler {
     __device__ __forceinline__ float4 value_at(int x, int y) const { return rgb[(size_t)y * w + x]; }
 };
 
-template <class V, class PV>
-__global__ void k_blend_area3(Canvas cv, PV pv, V view, Rect box, const float2* __restrict__ flr,
+#ifndef BLEND_MINB
+#define BLEND_MINB 12  // 40 registers: 12 CTAs of 128 per SM (latency-bound gathers)
+#endif
+template <class V, class PV, int CH>
+__global__ void __launch_bounds__(128, BLEND_MINB) k_blend_area3(Canvas cv, PV pv, V view, Rect box,
+                                                     const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
                               const int* __restrict__ d2, FoldStats* st, double k,
                               double coef, float4* __restrict__ out, float2* __restrict__ wgray,
@@ -603,22 +616,22 @@ __global__ void k_blend_area3(Canvas cv, PV pv, V view, Rect box, const float2* 
             if (pv(t.xs[q], t.ys[q]) && !rc.ok(t.xs[q], t.ys[q])) bad = true;
         if (bad) atomicOr(&st->reach_fail, 1u);
     }
-    bilinear_rgb(L, cv.w, cv.h, cv.ch, lx, ly, cl);
-    bilinear_rgb(view, cv.w, cv.h, cv.ch, x + lr.x * (1.0 - blend_r), y + lr.y * (1.0 - blend_r),
-                 cr);
+    bilinear_rgb<CH>(L, cv.w, cv.h, lx, ly, cl);
+    bilinear_rgb<CH>(view, cv.w, cv.h, x + lr.x * (1.0 - blend_r), y + lr.y * (1.0 - blend_r), cr);
     double mag_rl = sqrt((double)rl.x * rl.x + (double)rl.y * rl.y);
     double mag_lr = sqrt((double)lr.x * lr.x + (double)lr.y * lr.y);
     double sl, sr;
     softmax_weights(blend_l, blend_r, mag_rl, mag_lr, k, coef, sl, sr);
     float res[3] = {0.f, 0.f, 0.f};
-    for (int c = 0; c < cv.ch; ++c) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
         double v = cl[c] * sl + cr[c] * sr;
         res[c] = (float)clampd(v, 0.0, 1.0);
     }
     out[o] = make_float4(res[0], res[1], res[2], 0.f);
     if (wgray)  // gray of the warped constituents (warp_constituents, src/blender.cpp:150-158)
-        wgray[o] = cv.ch == 3 ? make_float2(gray3(cl[0], cl[1], cl[2]), gray3(cr[0], cr[1], cr[2]))
-                              : make_float2(cl[0], cr[0]);
+        wgray[o] = CH == 3 ? make_float2(gray3(cl[0], cl[1], cl[2]), gray3(cr[0], cr[1], cr[2]))
+                           : make_float2(cl[0], cr[0]);
 }
 
 template <class V>
@@ -878,14 +891,24 @@ void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2*
                  double coef, float4* out, float2* wgray, const uint8_t* owner, int fold,
                  cudaStream_t s, const ReachCheck* rc) {
     const ReachCheck r = rc ? *rc : ReachCheck{};
-    if (owner)
-        k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
-            cv, PanoOwnerBefore{owner, cv.w, fold}, view, box, flr, frl, d1, d2, st, k, coef, out,
-            wgray, r);
-    else
-        k_blend_area3<<<row_grid(box.w, box.h, 128), 128, 0, s>>>(
-            cv, PanoValidPlane{cv.valid, cv.w}, view, box, flr, frl, d1, d2, st, k, coef, out,
-            wgray, r);
+    const dim3 g = row_grid(box.w, box.h, 128);
+    if (owner) {
+        const PanoOwnerBefore pv{owner, cv.w, fold};
+        if (cv.ch == 3)
+            k_blend_area3<V, PanoOwnerBefore, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
+                                                                 d2, st, k, coef, out, wgray, r);
+        else
+            k_blend_area3<V, PanoOwnerBefore, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
+                                                                 d2, st, k, coef, out, wgray, r);
+    } else {
+        const PanoValidPlane pv{cv.valid, cv.w};
+        if (cv.ch == 3)
+            k_blend_area3<V, PanoValidPlane, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
+                                                                d2, st, k, coef, out, wgray, r);
+        else
+            k_blend_area3<V, PanoValidPlane, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
+                                                                d2, st, k, coef, out, wgray, r);
+    }
 }
 template <class V>
 void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
