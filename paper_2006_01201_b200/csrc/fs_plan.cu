@@ -895,17 +895,17 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             p->branch.assign(n - 1, nullptr);
             p->ev_branch.assign(n, nullptr);
             p->ev_compose.assign(n, nullptr);
-            // earlier folds' branches get higher priority: the ordered
-            // blend/compose chain needs them first, and their canvas
-            // rectangles can be read back while later folds still run
+            // every fold's branch at one (high) priority, above the chain:
+            // folds released together (e.g. C2's two bands) share the GPU
+            // instead of the later one starving behind the earlier one's
+            // sweeps (measured: ordering branches by fold was 0.15-0.25 ms slower)
             int least = 0, greatest = 0;
             FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            const int levels = least - greatest + 1;
             p->edt_stream.assign(n - 1, nullptr);
             for (int k = 0; k < n - 1; ++k) {
-                const int prio = greatest + (n - 1 > 1 ? k * (levels - 1) / (n - 2) : 0);
-                FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, prio));
-                FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking, prio));
+                FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
+                FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
+                                                   greatest));
             }
             p->ev_h2d.assign(n, nullptr);
             p->ev_cnt.assign(n, nullptr);
