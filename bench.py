@@ -238,8 +238,7 @@ def main():
     host_views = [torch.from_numpy(v).pin_memory() for v in lay.views]
     host_out = torch.empty((lay.canvas_h, lay.canvas_w, 4), dtype=torch.uint8).pin_memory()
     view_ptrs = [t.data_ptr() for t in host_views]
-    h2d_bytes = sum(v.nbytes for v in lay.views)
-    d2h_bytes = host_out.numel()
+    h2d_bytes, d2h_bytes = plan.transfer_bytes()  # page-locked path: what crosses PCIe
     # first execution: uploads the views, validates the plan's EDT domains
     plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
     shard_mode = None

@@ -206,6 +206,9 @@ fs_status fs_plan_execute_host(fs_plan plan, const uint8_t* const* views_rgba, u
 fs_status fs_plan_check(fs_plan plan);
 /* number of kernel launches of one execution (for accounting) */
 int fs_plan_launch_count(fs_plan plan);
+/* bytes fs_plan_execute_host moves with page-locked buffers: views in, and
+ * the canvas read back (rectangles no view covers are zeroed on the host) */
+fs_status fs_plan_transfer_bytes(fs_plan plan, size_t* h2d, size_t* d2h);
 /* fold geometry: for fold k (1..n-1) the Area3 box {x0,y0,w,h} and depth */
 fs_status fs_plan_fold_info(fs_plan plan, int k, int* box, int* depth);
 /* one un-captured execution with CUDA events around every kernel launch on

@@ -58,6 +58,12 @@ class Plan:
         _raise(N.lib.fs_plan_fold_info(self._h, k, box.ctypes.data_as(C.c_void_p), C.byref(depth)))
         return tuple(int(v) for v in box), depth.value
 
+    def transfer_bytes(self):
+        """(h2d, d2h) bytes of execute_host with page-locked buffers."""
+        a, b = C.c_size_t(), C.c_size_t()
+        _raise(N.lib.fs_plan_transfer_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     @property
     def launch_count(self) -> int:
         return N.lib.fs_plan_launch_count(self._h)

@@ -680,14 +680,31 @@ def _grid_layout(seed=3):
     return S.Layout("grid", W, H, views, offs, 3)
 
 
-@pytest.mark.parametrize("which", ["panorama", "grid"])
+def _gaps_layout(seed=5):
+    """A ring-like strip on a taller canvas with a gap column: canvas
+    rectangles no view covers (zeroed on the host in the overlap path)."""
+    W, H = 520, 260
+    scene = S.rgb_scene(H, W, seed)
+    offs = [(0, 40), (150, 40), (300, 60), (330, 150)]
+    sizes = [(190, 150), (190, 150), (170, 100), (150, 90)]
+    views = [S.rgba(np.roll(scene, k, axis=1)[y:y + h, x:x + w])
+             for k, ((x, y), (w, h)) in enumerate(zip(offs, sizes))]
+    return S.Layout("gaps", W, H, views, offs, 3)
+
+
+@pytest.mark.parametrize("which", ["panorama", "grid", "gaps"])
 def test_plan_host_overlap_matches_sync_path(fs, which):
     """execute_host with page-locked buffers runs the graph whose copies
-    overlap the folds (per-view H2D, per-rectangle quantise + D2H); it must
-    reproduce the pageable (copy, graph, copy) path and the device path."""
+    overlap the folds (per-view H2D, per-rectangle D2H, uncovered canvas
+    zeroed by a host node); it must reproduce the pageable (copy, graph,
+    copy) path and the device path."""
     import torch
-    lay = S.small_panorama(seed=2) if which == "panorama" else _grid_layout()
+    lay = {"panorama": lambda: S.small_panorama(seed=2), "grid": _grid_layout,
+           "gaps": _gaps_layout}[which]()
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=3))
+    h2d, d2h = plan.transfer_bytes()
+    assert h2d == sum(v.nbytes for v in lay.views)
+    assert (d2h < lay.canvas_w * lay.canvas_h * 4) == (which == "gaps")
     ref = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
     plan.execute_host(lay.views, ref)  # pageable numpy: synchronous copies
     pin = [torch.from_numpy(v).pin_memory() for v in lay.views]
