@@ -57,6 +57,9 @@ struct LkCfg {
 #ifndef LK_MINB_ITER
 #define LK_MINB_ITER 3
 #endif
+#ifndef LK_CARRY_FULL
+#define LK_CARRY_FULL 1
+#endif
 constexpr int LK_IW = 128;  // producer threads = input columns per CTA
 constexpr int LK_THREADS = 2 * LK_IW;
 
@@ -172,6 +175,15 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     float2 fl[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
+    // FULL (128 registers): the column of `from` walks down in registers,
+    // cen[j] = F(x, clamp(y)) for y = ybase - 1 .. ybase + NB (the vertical
+    // gradient's rows); later iterations (80 registers) reload them
+    constexpr bool CARRY = FULL && LK_CARRY_FULL;
+    float cen[CARRY ? NB + 2 : 1];
+    if (CARRY) {
+#pragma unroll
+        for (int j = 0; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ystart - 1 + j));
+    }
     int slot = 0;
     for (int i = 0; i < nbat; ++i) {
         const int buf = i & 1;
@@ -190,9 +202,14 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 const int yy = INNER ? y : clampi(y, 0, h - 1);
                 const float* Fr = INNER ? Fb + b * w : Fc + yy * w;
                 gxs[b] = 0.5f * (__ldg(Fr + dxr) - __ldg(Fr + dxl));  // src/flow.cpp:230-235
-                gys[b] = INNER ? 0.5f * (__ldg(Fr + w) - __ldg(Fr - w))
-                               : 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
-                ctr[b] = __ldg(Fr);
+                if (CARRY) {
+                    gys[b] = 0.5f * (cen[b + 2] - cen[b]);
+                    ctr[b] = cen[b + 1];
+                } else {
+                    gys[b] = INNER ? 0.5f * (__ldg(Fr + w) - __ldg(Fr - w))
+                                   : 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
+                    ctr[b] = __ldg(Fr);
+                }
                 const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
                 tfx[b] = t.fx;
                 tfy[b] = t.fy;
@@ -210,6 +227,12 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
         if (i + 1 < nbat) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + NB + b)];
+            if (CARRY) {
+                cen[0] = cen[NB];
+                cen[1] = cen[NB + 1];
+#pragma unroll
+                for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
+            }
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
