@@ -70,19 +70,29 @@ __global__ void __launch_bounds__(256) k_partition(P pano, V view, FoldStats* st
     const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
     const int yb = min(ya + PART_ROWS, view.rect.y1());
     int n2 = 0, n3 = 0, minx = INT_MAX, maxx = -1, miny = INT_MAX, maxy = -1;
-    if (x < view.rect.x1())
-        for (int y = ya; y < yb; ++y) {
-            if (!view.valid_at(x, y)) continue;
-            if (pano.valid_at(x, y)) {
+    if (x < view.rect.x1()) {
+        // the rows' masks loaded first (independent loads), then classified
+        bool vv[PART_ROWS], pp[PART_ROWS];
+#pragma unroll
+        for (int j = 0; j < PART_ROWS; ++j) {
+            const int y = ya + j;
+            vv[j] = y < yb && view.valid_at(x, y);
+            pp[j] = y < yb && pano.valid_at(x, y);
+        }
+#pragma unroll
+        for (int j = 0; j < PART_ROWS; ++j) {
+            if (!vv[j]) continue;
+            if (pp[j]) {
                 ++n3;
                 minx = min(minx, x);
                 maxx = max(maxx, x);
-                miny = min(miny, y);
-                maxy = max(maxy, y);
+                miny = min(miny, ya + j);
+                maxy = max(maxy, ya + j);
             } else {
                 ++n2;
             }
         }
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     n2 = __reduce_add_sync(0xffffffffu, n2);
     n3 = __reduce_add_sync(0xffffffffu, n3);
