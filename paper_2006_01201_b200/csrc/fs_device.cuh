@@ -249,7 +249,9 @@ void crop_gray(const P&, const V&, const Rect&, int ch, float*, float*, cudaStre
 void downsample(const float* in0, const float* in1, float* out0, float* out1, int w, int h,
                 int nimg, cudaStream_t);
 cudaError_t lk_prep(const LkArgs&, cudaStream_t);              // mode 0 or 2
-cudaError_t lk_sweep(const LkArgs&, bool full, cudaStream_t);  // one LK iteration
+// one LK sweep; mode: 0 a later iteration, 1 a level's first iteration in one
+// pass, 2 the level's structure tensor alone, 3 a first iteration on it
+cudaError_t lk_sweep(const LkArgs&, int mode, cudaStream_t);
 int lk_max_radius();
 void smooth(const SmoothArgs&, cudaStream_t);
 void finalize_flow(const SmoothArgs&, cudaStream_t);

@@ -116,12 +116,29 @@ void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
             fb[d][q] = a.take<float2>(n);
             ok[d][q] = a.take<uint8_t>(n);
         }
-        coef[d] = a.take<float4>(n);
+        coef[d].assign(depth, nullptr);
+        for (int l = 0; l < depth; ++l) coef[d][l] = a.take<float4>((size_t)lv[l].w * lv[l].h);
     }
 }
 
+void flow_split_events(FlowWS& ws) {
+    if (!ws.ev_fork) FS_CK(cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming));
+    while ((int)ws.ev_tensor.size() < ws.depth) {
+        cudaEvent_t e;
+        FS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ws.ev_tensor.push_back(e);
+    }
+}
+void flow_destroy_events(FlowWS& ws) {
+    if (ws.ev_fork) cudaEventDestroy(ws.ev_fork);
+    for (auto e : ws.ev_tensor) cudaEventDestroy(e);
+    ws.ev_fork = nullptr;
+    ws.ev_tensor.clear();
+}
+
 int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_params& p,
-                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s) {
+                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s,
+                 cudaStream_t ts) {
     int launches = 0;
     ws.pyr[0][0] = const_cast<float*>(g0);
     ws.pyr[1][0] = const_cast<float*>(g1);
@@ -137,15 +154,15 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     const int r = p.window_radius;
     const double win_area = static_cast<double>(2 * r + 1) * (2 * r + 1);
     const double eig_thresh = p.min_eigen_eps * win_area;  // src/flow.cpp:205-206
-    static const char* kSweepNames[2][8] = {
+    static const char* kSweepNames[3][8] = {
         {"lk_iter", "lk_iter_L1", "lk_iter_L2", "lk_iter_L3", "lk_iter_L4", "lk_iter_L5",
          "lk_iter_L6", "lk_iter_L7"},
         {"lk_first", "lk_first_L1", "lk_first_L2", "lk_first_L3", "lk_first_L4",
-         "lk_first_L5", "lk_first_L6", "lk_first_L7"}};
-    int fcur = 0, okcur = 0;
-    for (int l = ws.depth - 1; l >= 0; --l) {
+         "lk_first_L5", "lk_first_L6", "lk_first_L7"},
+        {"lk_tensor", "lk_tensor_L1", "lk_tensor_L2", "lk_tensor_L3", "lk_tensor_L4",
+         "lk_tensor_L5", "lk_tensor_L6", "lk_tensor_L7"}};
+    auto level_args = [&](int l) {
         const Level L = ws.lv[l];
-        const double npx = (double)L.w * L.h * ws.ndir;
         LkArgs a{};
         a.ndir = ws.ndir;
         a.w = L.w;
@@ -154,6 +171,37 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
         a.th = 0;  // per-level choice (launch::lk_tile_rows)
         a.eig_thresh = eig_thresh;
         a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
+        for (int d = 0; d < ws.ndir; ++d) {
+            int src = ws.ndir == 1 ? 0 : d;
+            a.d[d].F = ws.pyr[src][l];
+            a.d[d].T = ws.pyr[1 - src][l];
+            a.d[d].coef = ws.coef[d][l];
+        }
+        return a;
+    };
+    // split schedule: the structure tensors need only the pyramid (the level's
+    // `from` gradients), so they run on ts while the chain works coarse to fine
+    const bool split = ts && ws.ev_fork && (int)ws.ev_tensor.size() >= ws.depth;
+    if (split) {
+        FS_CK(cudaEventRecord(ws.ev_fork, s));
+        FS_CK(cudaStreamWaitEvent(ts, ws.ev_fork, 0));
+        for (int l = ws.depth - 1; l >= 0; --l) {
+            LkArgs a = level_args(l);
+            {
+                // per pixel and direction: F 4 in, coef 16 out
+                ProfScope ps(kSweepNames[2][std::min(l, 7)],
+                             20.0 * ws.lv[l].w * ws.lv[l].h * ws.ndir, ts);
+                FS_CK(launch::lk_sweep(a, 2, ts));
+            }
+            ++launches;
+            FS_CK(cudaEventRecord(ws.ev_tensor[l], ts));
+        }
+    }
+    int fcur = 0, okcur = 0;
+    for (int l = ws.depth - 1; l >= 0; --l) {
+        const Level L = ws.lv[l];
+        const double npx = (double)L.w * L.h * ws.ndir;
+        LkArgs a = level_args(l);
         a.mode = l == ws.depth - 1 ? 0 : 2;
         if (a.mode == 2) {
             a.cw = ws.lv[l + 1].w;
@@ -161,12 +209,8 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             a.sx = static_cast<double>(a.cw) / L.w;  // src/flow.cpp:145-146
             a.sy = static_cast<double>(a.ch) / L.h;
         }
-        for (int d = 0; d < ws.ndir; ++d) {
-            int src = ws.ndir == 1 ? 0 : d;
-            a.d[d].F = ws.pyr[src][l];
-            a.d[d].T = ws.pyr[1 - src][l];
-            a.d[d].coef = p.iterations_per_level > 1 ? ws.coef[d] : nullptr;
-        }
+        if (!split && p.iterations_per_level == 1)
+            for (int d = 0; d < ws.ndir; ++d) a.d[d].coef = nullptr;  // FULL alone: not stored
         // level start: flow (zero / upsampled), ever_ok, It
         for (int d = 0; d < ws.ndir; ++d) {
             a.d[d].fin = ws.fb[d][fcur];
@@ -190,13 +234,14 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.d[d].fout = ws.fb[d][fcur ^ 1];
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
             }
+            if (full && split) FS_CK(cudaStreamWaitEvent(s, ws.ev_tensor[l], 0));
             {
                 // per pixel and direction: F 4 + T 4 (It gather) + flow 8 in,
-                //  flow 8 out; first iteration: ok 1 in/out + coef 16 out;
-                //  later: coef 16 in
+                //  flow 8 out; first iteration: ok 1 in/out + coef 16 out (FULL)
+                //  or in (split); later: coef 16 in
                 double per = 24.0 + (full ? 2.0 + (a.d[0].coef ? 16.0 : 0.0) : 16.0);
-                ProfScope ps(kSweepNames[full][std::min(l, 7)], per * npx, s);
-                FS_CK(launch::lk_sweep(a, full, s));
+                ProfScope ps(kSweepNames[full && !split][std::min(l, 7)], per * npx, s);
+                FS_CK(launch::lk_sweep(a, full ? (split ? 3 : 1) : 0, s));
             }
             ++launches;
             fcur ^= 1;
@@ -355,7 +400,7 @@ template <class V, class P, class PC>
 int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1, cudaStream_t es, cudaEvent_t ev_fork,
-                          cudaEvent_t ev_join, bool with_edt) {
+                          cudaEvent_t ev_join, bool with_edt, cudaStream_t ts) {
     int launches = 0;
     // the distance transforms need only the masks and the fold's counts: with
     // a second stream they run concurrently with the flow
@@ -375,7 +420,7 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
     launches += 2;
     if (ev_flow0) FS_CK(cudaEventRecord(ev_flow0, s));
     if (es) launches += fold_enqueue_edt(f, pano, view, se);
-    launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s);
+    launches += flow_enqueue(f.flow, f.gray[0], f.gray[1], fp, f.fvec, f.fvalid, s, ts);
     if (ev_flow1) FS_CK(cudaEventRecord(ev_flow1, s));
     if (es) {
         FS_CK(cudaEventRecord(ev_join, es));
@@ -457,19 +502,19 @@ template int fold_enqueue_pre<ViewF4, PanoPlane>(FoldWS<ViewF4>&, const PanoPlan
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoViews>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoViews&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoHybrid>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoHybrid&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoPlane, PanoPlane>(
     FoldWS<ViewU8>&, const PanoPlane&, const PanoPlane&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
 template int fold_enqueue_flow_edt<ViewF4, PanoPlane, PanoPlane>(
     FoldWS<ViewF4>&, const PanoPlane&, const PanoPlane&, const ViewF4&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
 template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoViews&, const ViewU8&,
                                                  cudaStream_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,

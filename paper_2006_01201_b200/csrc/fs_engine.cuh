@@ -73,14 +73,22 @@ struct FlowWS {
     std::vector<float*> pyr[2];  // level pointers (level 0 = caller's gray buffers)
     float2* fb[2][2] = {};       // [dir][pingpong] level flow
     uint8_t* ok[2][2] = {};
-    float4* coef[2] = {};        // [dir] level-constant inverse structure tensor
+    std::vector<float4*> coef[2];  // [dir][level] level-constant inverse structure tensor
+    // split schedule (flow_split_events): every level's structure tensor on a
+    // side stream right after the pyramid, off the coarse-to-fine chain
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_tensor;
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
+void flow_split_events(FlowWS& ws);   // create the split schedule's events
+void flow_destroy_events(FlowWS& ws);
 // Enqueue the whole coarse-to-fine flow on stream s.  ndir = 1: from=g0,
 // to=g1.  ndir = 2: dir 0 is L->R (from g0), dir 1 is R->L (from g1).
 // Outputs are the reference FlowField layouts (interleaved dx,dy + valid).
+// With ts (and flow_split_events done) the structure tensors run on ts.
 int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_params& p,
-                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s);
+                 float2* const out_vec[2], uint8_t* const out_valid[2], cudaStream_t s,
+                 cudaStream_t ts = nullptr);
 
 // Distance-transform job layout for one seed mask of a fold.
 struct EdtPlan {
@@ -127,7 +135,7 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1, cudaStream_t es = nullptr,
                           cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
-                          bool with_edt = true);
+                          bool with_edt = true, cudaStream_t ts = nullptr);
 template <class V, class P>
 int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
 // Code 1 blend on Area3 + composition of the view onto the canvas

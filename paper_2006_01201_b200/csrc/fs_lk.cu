@@ -38,9 +38,25 @@
 
 namespace fs {
 
-template <bool FULL>
+// Sweep modes: ITER (a later iteration: two mismatch sums, update by the
+// stored inverse tensor), FULL (a level's first iteration in one pass: five
+// sums, eigenvalue test, division-form update, stores the inverse tensor),
+// TENSOR (the level-constant structure tensor alone: three sums, eigenvalue
+// test, inverse tensor — no flow, so it runs off the coarse-to-fine chain),
+// FIRST (an ITER that also writes the level's ever_ok from the TENSOR test).
+enum { LK_ITER = 0, LK_FULL = 1, LK_TENSOR = 2, LK_FIRST = 3 };
+
+#ifndef LK_MINB_FULL
+#define LK_MINB_FULL 2
+#endif
+#ifndef LK_MINB_ITER
+#define LK_MINB_ITER 3
+#endif
+
+template <int M>
 struct LkCfg {
-    static constexpr int NQ = FULL ? 5 : 2;  // window sums carried
+    static constexpr bool FULL = M == LK_FULL;
+    static constexpr int NQ = M == LK_FULL ? 5 : M == LK_TENSOR ? 3 : 2;  // window sums carried
 #ifndef LK_NB_FULL
 #define LK_NB_FULL 4
 #define LK_S_FULL 4
@@ -49,14 +65,14 @@ struct LkCfg {
 #endif
     static constexpr int NB = FULL ? LK_NB_FULL : LK_NB_ITER;  // rows per staged batch
     static constexpr int S = FULL ? LK_S_FULL : LK_S_ITER;     // outputs per horizontal run
+    static constexpr bool GATHER = M != LK_TENSOR;              // It = T(p + d) - F(p)
+    // ring entries per column and row: FULL (Ix, Iy, It) and TENSOR (Ix, Iy)
+    // as floats (products re-formed), ITER/FIRST the two double products
+    static constexpr size_t RING = M == LK_FULL ? 3 * sizeof(float)
+                                 : M == LK_TENSOR ? 2 * sizeof(float) : 2 * sizeof(double);
+    static constexpr int MINB = M == LK_FULL ? LK_MINB_FULL : LK_MINB_ITER;
 };
 
-#ifndef LK_MINB_FULL
-#define LK_MINB_FULL 2
-#endif
-#ifndef LK_MINB_ITER
-#define LK_MINB_ITER 3
-#endif
 #ifndef LK_CARRY_FULL
 #define LK_CARRY_FULL 1
 #endif
@@ -70,18 +86,17 @@ __host__ __device__ inline int lk_iwp(int iw) { return iw + 1; }
 // Ring of the last 2r+1 rows per column, so the row leaving the window is
 // subtracted exactly: FULL keeps (Ix, Iy, It) as floats (five products are
 // re-formed), later iterations keep the two double products themselves.
-template <bool FULL>
+template <int M>
 __host__ __device__ inline size_t lk_ring_bytes(int r) {
-    const size_t per = FULL ? 3 * sizeof(float) : 2 * sizeof(double);
-    return ((size_t)(2 * r + 1) * LK_IW * per + 15) & ~size_t(15);
+    return ((size_t)(2 * r + 1) * LK_IW * LkCfg<M>::RING + 15) & ~size_t(15);
 }
-template <bool FULL>
+template <int M>
 __host__ __device__ inline size_t lk_stage_doubles() {
-    return (size_t)LkCfg<FULL>::NB * LkCfg<FULL>::NQ * lk_iwp(LK_IW);
+    return (size_t)LkCfg<M>::NB * LkCfg<M>::NQ * lk_iwp(LK_IW);
 }
-template <bool FULL>
+template <int M>
 __host__ inline size_t lk_smem_bytes(int r) {
-    return lk_ring_bytes<FULL>(r) + 2 * lk_stage_doubles<FULL>() * sizeof(double);
+    return lk_ring_bytes<M>(r) + 2 * lk_stage_doubles<M>() * sizeof(double);
 }
 
 __device__ __forceinline__ void bar_sync(int id) {
@@ -143,11 +158,12 @@ __global__ void __launch_bounds__(256) k_lk_prep(LkArgs a) {
 // warp's edge lanes load them.  It = to(p + d) - from(p) (src/flow.cpp:248-249)
 // is gathered at every window pixel from the current flow (loaded one batch
 // ahead).  All indices are 32-bit (levels hold < 2^31 pixels).
-template <bool FULL>
+template <int M>
 __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void* ringv,
                                            double* stage, int x0, int ystart, int yend, int nbat) {
-    using Cfg = LkCfg<FULL>;
+    using Cfg = LkCfg<M>;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ;
+    constexpr bool FULL = Cfg::FULL, GATHER = Cfg::GATHER, TENSOR = M == LK_TENSOR;
     const int r = a.r, K = 2 * r + 1, w = a.w, h = a.h;
     const int IWP = lk_iwp(LK_IW);
     const int c = threadIdx.x;
@@ -164,6 +180,9 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
         if (FULL) {
             float* rs = ringf + (k * LK_IW + c) * 3;
             rs[0] = rs[1] = rs[2] = 0.f;
+        } else if (TENSOR) {
+            float* rs = ringf + (k * LK_IW + c) * 2;
+            rs[0] = rs[1] = 0.f;
         } else {
             ringd[k * LK_IW + c] = make_double2(0.0, 0.0);
         }
@@ -173,8 +192,10 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     for (int q = 0; q < NQ; ++q) V[q] = 0.0;
     auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
     float2 fl[NB];
+    if (GATHER) {
 #pragma unroll
-    for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
+        for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
+    }
     // FULL (128 registers): the column of `from` walks down in registers,
     // cen[j] = F(x, clamp(y)) for y = ybase - 1 .. ybase + NB (the vertical
     // gradient's rows); later iterations (80 registers) reload them
@@ -210,14 +231,16 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                                    : 0.5f * (__ldg(Fc + ro(y + 1)) - __ldg(Fc + ro(y - 1)));
                     ctr[b] = __ldg(Fr);
                 }
-                const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
-                tfx[b] = t.fx;
-                tfy[b] = t.fy;
-                const float* p = T + t.off;
-                tap[b][0] = __ldg(p);
-                tap[b][1] = __ldg(p + t.dx);
-                tap[b][2] = __ldg(p + t.dy);
-                tap[b][3] = __ldg(p + (t.dy + t.dx));
+                if (GATHER) {
+                    const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
+                    tfx[b] = t.fx;
+                    tfy[b] = t.fy;
+                    const float* p = T + t.off;
+                    tap[b][0] = __ldg(p);
+                    tap[b][1] = __ldg(p + t.dx);
+                    tap[b][2] = __ldg(p + t.dy);
+                    tap[b][3] = __ldg(p + (t.dy + t.dx));
+                }
             }
         };
         if (ybase >= 1 && ybase + NB <= h - 1 && ybase + NB <= yend)
@@ -225,8 +248,10 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
         else
             loads(std::false_type{});
         if (i + 1 < nbat) {
+            if (GATHER) {
 #pragma unroll
-            for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + NB + b)];
+                for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + NB + b)];
+            }
             if (CARRY) {
                 cen[0] = cen[NB];
                 cen[1] = cen[NB + 1];
@@ -234,20 +259,30 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
             }
         }
+        if (GATHER) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            LevelTap t;
-            t.fx = tfx[b];
-            t.fy = tfy[b];
-            dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - ctr[b];
+            for (int b = 0; b < NB; ++b) {
+                LevelTap t;
+                t.fx = tfx[b];
+                t.fy = tfy[b];
+                dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - ctr[b];
+            }
         }
         if (i >= 2) bar_sync(3 + buf);  // consumers released this buffer
-        double* st = stage + (size_t)buf * lk_stage_doubles<FULL>();
+        double* st = stage + (size_t)buf * lk_stage_doubles<M>();
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             const double ix = in[b] ? gxs[b] : 0.f, iy = in[b] ? gys[b] : 0.f;
-            const double tt = in[b] ? dts[b] : 0.f;
-            if (FULL) {
+            const double tt = (GATHER && in[b]) ? dts[b] : 0.f;
+            if (TENSOR) {
+                float* rs = ringf + (slot * LK_IW + c) * 2;
+                const double ogx = rs[0], ogy = rs[1];
+                rs[0] = (float)ix;
+                rs[1] = (float)iy;
+                V[0] = (V[0] + ix * ix) - ogx * ogx;
+                V[1] = (V[1] + ix * iy) - ogx * ogy;
+                V[2] = (V[2] + iy * iy) - ogy * ogy;
+            } else if (FULL) {
                 float* rs = ringf + (slot * LK_IW + c) * 3;
                 const double ogx = rs[0], ogy = rs[1], odt = rs[2];
                 rs[0] = (float)ix;
@@ -276,11 +311,12 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
 }
 
 // ---- consumer: horizontal sums, solve, update, next It ---------------------
-template <bool FULL>
+template <int M>
 __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, const double* stage,
                                            int x0, int y0, int ystart, int yo_end, int nbat) {
-    using Cfg = LkCfg<FULL>;
+    using Cfg = LkCfg<M>;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ, S = Cfg::S;
+    constexpr bool FULL = Cfg::FULL, TENSOR = M == LK_TENSOR, FIRST = M == LK_FIRST;
     const int r = a.r, w = a.w;
     const int IWP = lk_iwp(LK_IW);
     const int nruns = (a.tw + S - 1) / S;
@@ -296,20 +332,18 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
         float2 fo[S];
         float4 cf[S];
         uint8_t okv[S];
-        if (active) {
+        if (active && !TENSOR) {
 #pragma unroll
             for (int o = 0; o < S; ++o) {
                 const int oi = yo * w + min(x0 + cs + o, w - 1);
                 fo[o] = D.fin[oi];
-                if (FULL)
-                    okv[o] = D.okin[oi];
-                else
-                    cf[o] = D.coef[oi];
+                if (FULL || FIRST) okv[o] = D.okin[oi];
+                if (!FULL) cf[o] = D.coef[oi];
             }
         }
         bar_sync(1 + buf);
         if (active) {
-            const double* vb = stage + (size_t)buf * lk_stage_doubles<FULL>() + b * IWP + cs;
+            const double* vb = stage + (size_t)buf * lk_stage_doubles<M>() + b * IWP + cs;
             const int QS = NB * IWP;  // plane stride
             double s[NQ], s2[NQ];
 #pragma unroll
@@ -338,7 +372,17 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                         s[q] = (s[q] + va[q * QS + o]) - vb[q * QS + o - 1];
                 }
                 const int oi = yo * w + (x0 + cs + o);
+                if (TENSOR) {  // the level's eigenvalue test and inverse tensor
+                    double inv_det;
+                    float4 coef = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (lk_tensor_ok(s[0], s[1], s[2], a.eig_thresh, inv_det))
+                        coef = make_float4((float)(s[2] * inv_det), (float)(s[1] * inv_det),
+                                           (float)(s[0] * inv_det), 1.f);
+                    D.coef[oi] = coef;
+                    continue;
+                }
                 float2 f = fo[o];
+                if (FIRST) D.okout[oi] = (okv[o] || cf[o].w != 0.f) ? 1 : 0;
                 if (FULL) {
                     uint8_t ok = okv[o];
                     const double A = s[0], B = s[1], Cc = s[2];
@@ -368,21 +412,21 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
     }
 }
 
-template <bool FULL>
-__global__ void __launch_bounds__(LK_THREADS, FULL ? LK_MINB_FULL : LK_MINB_ITER) k_lk_sweep(LkArgs a) {
+template <int M>
+__global__ void __launch_bounds__(LK_THREADS, LkCfg<M>::MINB) k_lk_sweep(LkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     void* ring = smem;
-    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes<FULL>(a.r));
+    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes<M>(a.r));
     const LkDir& D = a.d[blockIdx.z];
     const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
     const int yo_end = min(y0 + a.th, a.h);
     const int ystart = y0 - a.r;
     const int yend = yo_end + a.r;
-    const int nbat = (yend - ystart + LkCfg<FULL>::NB - 1) / LkCfg<FULL>::NB;
+    const int nbat = (yend - ystart + LkCfg<M>::NB - 1) / LkCfg<M>::NB;
     if (threadIdx.x < LK_IW)
-        lk_produce<FULL>(a, D, ring, stage, x0, ystart, yend, nbat);
+        lk_produce<M>(a, D, ring, stage, x0, ystart, yend, nbat);
     else
-        lk_consume<FULL>(a, D, stage, x0, y0, ystart, yo_end, nbat);
+        lk_consume<M>(a, D, stage, x0, y0, ystart, yo_end, nbat);
 }
 
 namespace launch {
@@ -391,8 +435,10 @@ static bool lk_configured = false;
 void lk_init() {
     if (lk_configured) return;
     const int mx = 200 * 1024;
-    cudaFuncSetAttribute(k_lk_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_sweep<LK_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_sweep<LK_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_sweep<LK_TENSOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_lk_sweep<LK_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     lk_configured = true;
 }
 
@@ -428,16 +474,23 @@ cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t lk_sweep(const LkArgs& a0, bool full, cudaStream_t s) {
+template <int M>
+static void sweep_launch(LkArgs a, cudaStream_t s) {
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB);
+    dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
+    k_lk_sweep<M><<<g, LK_THREADS, lk_smem_bytes<M>(a.r), s>>>(a);
+}
+
+cudaError_t lk_sweep(const LkArgs& a0, int mode, cudaStream_t s) {
     LkArgs a = a0;
     a.tw = LK_IW - 2 * a.r;
-    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, full ? LK_MINB_FULL : LK_MINB_ITER);
     lk_init();
-    dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
-    if (full)
-        k_lk_sweep<true><<<g, LK_THREADS, lk_smem_bytes<true>(a.r), s>>>(a);
-    else
-        k_lk_sweep<false><<<g, LK_THREADS, lk_smem_bytes<false>(a.r), s>>>(a);
+    switch (mode) {
+        case LK_FULL: sweep_launch<LK_FULL>(a, s); break;
+        case LK_TENSOR: sweep_launch<LK_TENSOR>(a, s); break;
+        case LK_FIRST: sweep_launch<LK_FIRST>(a, s); break;
+        default: sweep_launch<LK_ITER>(a, s); break;
+    }
     return cudaGetLastError();
 }
 

@@ -96,8 +96,9 @@ FS_HD float div_to_float(double acc, double n, double inv_n) {
 // src/flow.cpp:267-291 — the 2x2 structure-tensor solve of one pixel.
 // Returns true (and the updated flow) when lambda_min >= threshold, with
 // inv_det = 1/det (the level's stored inverse structure tensor needs it).
-FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double eig_thresh,
-                        float flow_cap, float& dx, float& dy, double& inv_det) {
+// The eigenvalue test of the structure tensor (a, b; b, c) and, when it
+// passes, 1/det.
+FS_HD bool lk_tensor_ok(double a, double b, double c, double eig_thresh, double& inv_det) {
     double tr = a + c;
     double det = a * c - b * b;
     double disc = tr * tr - 4.0 * det;
@@ -105,6 +106,13 @@ FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double e
     double lambda_min = 0.5 * (tr - sqrt(disc));
     if (lambda_min < eig_thresh) return false;
     inv_det = 1.0 / det;
+    return true;
+}
+
+FS_HD bool lk_solve(double a, double b, double c, double bx, double by, double eig_thresh,
+                        float flow_cap, float& dx, float& dy, double& inv_det) {
+    if (!lk_tensor_ok(a, b, c, eig_thresh, inv_det)) return false;
+    const double det = a * c - b * b;
     float ndx = dx + -div_to_float(c * bx - b * by, det, inv_det);
     float ndy = dy + -div_to_float(a * by - b * bx, det, inv_det);
     final_cap(flow_cap, ndx, ndy);  // src/flow.cpp:283-287

@@ -17,6 +17,12 @@ using namespace fs;
 
 constexpr size_t kMaxStamps = 512;
 
+// LK structure tensors off the coarse-to-fine chain (FlowWS split schedule)
+#ifndef FS_LK_SPLIT
+#define FS_LK_SPLIT 0  // measured: C2 4.28 -> 4.45 ms device, C4 e2e 14.5 -> 14.2 ms
+#endif
+constexpr bool kLkSplit = FS_LK_SPLIT != 0;
+
 // first-cover copies a sharded rank keeps around each own fold's Area3 box:
 // a blend tap farther out is refused (ReachCheck) and the panorama runs unsharded
 constexpr int kShardMargin = 128;
@@ -48,6 +54,7 @@ struct fs_plan_s {
     std::vector<cudaStream_t> branch;
     std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt, ev_own, ev_efork, ev_ejoin;
     std::vector<cudaStream_t> edt_stream;  // per fold: the distance transforms
+    std::vector<cudaStream_t> tensor_stream;  // per fold: the LK structure tensors
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr, own = nullptr;
     uint8_t* owner = nullptr;  // first covering view per canvas pixel (PanoViews)
@@ -261,7 +268,9 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             ViewU8 v = view_of(p, k);
             launches += fold_enqueue_pre(f, plane, v, s);
             launch::snapshot_count(f.st, p->cc, s);
-            launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr);
+            launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr,
+                                                  nullptr, nullptr, nullptr, true,
+                                                  kLkSplit ? s : nullptr);
             launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
         }
         {
@@ -342,7 +351,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         cudaStream_t es = p->edt_stream[k - 1];
         if (p->crop_wait[k] == 0) {
             launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1, es,
-                                              p->ev_efork[k], p->ev_ejoin[k]);
+                                              p->ev_efork[k], p->ev_ejoin[k], true,
+                                              p->tensor_stream[k - 1]);
         } else {  // blended pixels inside the box: after that fold's compose
             // (the distance transforms need only the masks: fork them first)
             FS_CK(cudaEventRecord(p->ev_efork[k], b));
@@ -352,7 +362,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
             if (p->tl_stamp) mark("fold" + fk + "_flow_start", b);
             launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1,
-                                              nullptr, nullptr, nullptr, false);
+                                              nullptr, nullptr, nullptr, false,
+                                              p->tensor_stream[k - 1]);
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
         mark("fold" + fk + "_edt_end", b);
@@ -615,7 +626,8 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
         for (int m = 1; m < k; ++m) hybrid = hybrid || rects_meet(p->boxes[m], p->boxes[k]);
         if (!hybrid) {
             launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, nullptr, nullptr, es,
-                                              p->ev_efork[k], p->ev_ejoin[k]);
+                                              p->ev_efork[k], p->ev_ejoin[k], true,
+                                              p->tensor_stream[k - 1]);
         } else {
             FS_CK(cudaEventRecord(p->ev_efork[k], b));
             FS_CK(cudaStreamWaitEvent(es, p->ev_efork[k], 0));
@@ -623,7 +635,8 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
             FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
             if (S.wait_local[k]) FS_CK(cudaStreamWaitEvent(b, p->ev_compose[S.wait_local[k]], 0));
             launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, nullptr,
-                                              nullptr, nullptr, nullptr, nullptr, false);
+                                              nullptr, nullptr, nullptr, nullptr, false,
+                                              p->tensor_stream[k - 1]);
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
@@ -956,9 +969,12 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             int least = 0, greatest = 0;
             FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
             p->edt_stream.assign(n - 1, nullptr);
+            p->tensor_stream.assign(n - 1, nullptr);
             for (int k = 0; k < n - 1; ++k) {
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
+                                                   greatest));
+                FS_CK(cudaStreamCreateWithPriority(&p->tensor_stream[k], cudaStreamNonBlocking,
                                                    greatest));
             }
             p->ev_h2d.assign(n, nullptr);
@@ -1001,6 +1017,8 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         Arena a1;
         a1.base = p->arena;
         layout_plan(p, a1, boxes);
+        if (kLkSplit)
+            for (auto& f : p->folds) flow_split_events(f.flow);
         if (views_rgba)
             for (int k = 0; k < n; ++k)
                 FS_CK(cudaMemcpy(p->views[k], views_rgba[k],
@@ -1414,6 +1432,9 @@ void fs_plan_destroy(fs_plan p) {
         if (e) cudaEventDestroy(e);
     for (auto st : p->edt_stream)
         if (st) cudaStreamDestroy(st);
+    for (auto st : p->tensor_stream)
+        if (st) cudaStreamDestroy(st);
+    for (auto& f : p->folds) flow_destroy_events(f.flow);
     if (p->own) cudaStreamDestroy(p->own);
     for (auto e : p->ev_a2)
         if (e) cudaEventDestroy(e);
