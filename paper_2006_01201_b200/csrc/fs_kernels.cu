@@ -384,17 +384,30 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
     const unsigned long long* B = J.bits + line;
     const unsigned long long mine = B[(size_t)seg * nlines];
     long long prev = -(1LL << 40), next = 1LL << 40;  // nearest seed before / after the segment
-    for (int s = seg - 1; s >= 0; --s) {
-        unsigned long long m = B[(size_t)s * nlines];
-        if (m) {
-            prev = (long long)s * EDT_SEG + 63 - __clzll((long long)m);
+    // nearest seeds outside the segment: four segments' masks per round trip
+    for (int s = seg - 1; s >= 0; s -= 4) {
+        unsigned long long m[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = s - j >= 0 ? B[(size_t)(s - j) * nlines] : 0ull;
+        int hit = -1;
+#pragma unroll
+        for (int j = 3; j >= 0; --j)
+            if (m[j]) hit = j;
+        if (hit >= 0) {
+            prev = (long long)(s - hit) * EDT_SEG + 63 - __clzll((long long)m[hit]);
             break;
         }
     }
-    for (int s = seg + 1; s < nseg; ++s) {
-        unsigned long long m = B[(size_t)s * nlines];
-        if (m) {
-            next = (long long)s * EDT_SEG + __ffsll((long long)m) - 1;
+    for (int s = seg + 1; s < nseg; s += 4) {
+        unsigned long long m[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = s + j < nseg ? B[(size_t)(s + j) * nlines] : 0ull;
+        int hit = -1;
+#pragma unroll
+        for (int j = 3; j >= 0; --j)
+            if (m[j]) hit = j;
+        if (hit >= 0) {
+            next = (long long)(s + hit) * EDT_SEG + __ffsll((long long)m[hit]) - 1;
             break;
         }
     }
