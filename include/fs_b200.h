@@ -173,6 +173,33 @@ fs_status fs_misalignment_score(const float* l, const uint8_t* valid_l, const fl
 fs_status fs_estimate_translation(const float* a, const float* b, int w, int h, int ch,
                                   int max_shift, int* dx, int* dy, double* score, void* stream);
 
+/* ---- pre-processing (north_star stage 1) ----
+ * Absent from the reference (SPEC.md:12 delegates it to Hugin/PanoTools):
+ * parity UNPINNED — checked against a numpy restatement (oracle/remap.py)
+ * only.  An equidistant fisheye camera (r = f * theta) at orientation
+ * yaw/pitch/roll is resampled onto a rectangle of an equirectangular canvas
+ * (canvas_w x canvas_h covers 360 x 180 degrees), which is then a placed view
+ * of stitch_placed / fs_plan_*. */
+typedef struct {
+    int width, height;      /* fisheye image */
+    double cx, cy;          /* optical centre (px) */
+    double focal;           /* px per radian (equidistant) */
+    double radius;          /* image circle radius (px); taps beyond are invalid */
+    double yaw, pitch, roll;  /* radians: camera = Ry(yaw) Rx(pitch) Rz(roll) */
+} fs_fisheye_camera;
+/* Host-only remap table: for every pixel of the canvas rectangle
+ * (x0, y0, w, h), the fisheye source position (x, y) as two floats
+ * (computed in double), or (-1, -1) where the ray misses the image circle. */
+fs_status fs_fisheye_map(const fs_fisheye_camera* cam, int canvas_w, int canvas_h, int x0, int y0,
+                         int w, int h, float* map_xy);
+/* Device remap of an RGBA8 (or RGB8 with channels = 3) fisheye image through
+ * a table (device pointers), with per-channel chromaticity gains:
+ * out = min(255, floor(bilinear(src) * gain + 0.5)), alpha 255 where the
+ * table is valid, else the pixel is (0, 0, 0, 0).  Pointers may be host or
+ * device memory (gains3: three floats, NULL = no correction). */
+fs_status fs_remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float* map_xy,
+                         int w, int h, const float* gains3, uint8_t* out_rgba, void* stream);
+
 /* ---- pipeline fold (pipeline.hpp:63-67) ---- */
 /* stitch_placed: images[i] is dims[2i] x dims[2i+1] x ch at offsets[2i],
  * offsets[2i+1]; valids may be NULL or hold NULL entries (all valid).  The

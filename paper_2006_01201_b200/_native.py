@@ -58,6 +58,13 @@ class PairStats(C.Structure):
                 ("misalignment_after", C.c_double)]
 
 
+class FisheyeCamera(C.Structure):
+    """fs_fisheye_camera (include/fs_b200.h): equidistant fisheye, radians."""
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("cx", C.c_double), ("cy", C.c_double),
+                ("focal", C.c_double), ("radius", C.c_double), ("yaw", C.c_double),
+                ("pitch", C.c_double), ("roll", C.c_double)]
+
+
 class StripXfer(C.Structure):
     """fs_strip_xfer: fold k's strip moves from rank src to rank dst after
     segment `stage`."""
@@ -103,6 +110,8 @@ SIGNATURES = {
     "fs_estimate_translation": (I, [P, P, I, I, I, I, P, P, P, P]),
     "fs_stitch_placed": (I, [I, PP, PP, P, P, I, I, I, C.POINTER(FlowParams),
                              C.POINTER(BlendParams), P, P, P, P]),
+    "fs_fisheye_map": (I, [C.POINTER(FisheyeCamera), I, I, I, I, I, I, P]),
+    "fs_remap_rgba8": (I, [P, I, I, I, P, I, I, P, P, P]),
     "fs_plan_create": (I, [C.POINTER(P), I, I, P, P, I, I, C.POINTER(FlowParams),
                            C.POINTER(BlendParams), PP]),
     "fs_plan_view_buffer": (P, [P, I]),

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native as N
-from ._native import BlendParams, FlowParams
+from ._native import BlendParams, FisheyeCamera, FlowParams
 
 __all__ = [
     "FlowstitchError", "ContractError", "EmptyRegionError", "LayoutError", "IoError",
@@ -25,7 +25,8 @@ __all__ = [
     "compute_partition", "crop_overlap", "place_on_canvas", "build_pyramid", "dense_pyr_lk",
     "bidirectional_flow", "flow_magnitude", "embed_flow", "distance_transform",
     "compute_blend", "softmax_weights", "blend_pair", "feather_blend", "warp_constituents",
-    "misalignment_score", "estimate_translation", "TranslationEstimate", "stitch_placed", "set_thread_count", "thread_count",
+    "misalignment_score", "estimate_translation", "TranslationEstimate", "stitch_placed",
+    "FisheyeCamera", "fisheye_map", "remap_rgba8", "set_thread_count", "thread_count",
     "resolved_thread_count",
 ]
 
@@ -530,3 +531,29 @@ def stitch_placed(placed: Sequence[PlacedImage], canvas_width: int, canvas_heigh
                                    s.misalignment_before if s.misalignment_present & 1 else None,
                                    s.misalignment_after if s.misalignment_present & 2 else None))
     return ImageBuf(out, ov), rep
+
+
+# ---- pre-processing: fisheye remap + chromaticity gains (north_star stage 1;
+# no reference counterpart — parity unpinned, see include/fs_b200.h) ----
+def fisheye_map(cam: FisheyeCamera, canvas_width: int, canvas_height: int, x0: int, y0: int,
+                width: int, height: int) -> np.ndarray:
+    """Remap table of the canvas rectangle (x0, y0, width, height): (h, w, 2)
+    float32 fisheye source positions, (-1, -1) where the ray misses."""
+    out = np.empty((height, width, 2), np.float32)
+    _check(N.lib.fs_fisheye_map(C.byref(cam), canvas_width, canvas_height, x0, y0, width,
+                                height, _p(out)))
+    return out
+
+
+def remap_rgba8(src: np.ndarray, table: np.ndarray, gains=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """Bilinear remap of an RGB8/RGBA8 image (h, w, 3|4) through a table, with
+    per-channel gains; returns the RGBA8 view (alpha 255 where valid)."""
+    src = np.ascontiguousarray(src, np.uint8)
+    table = np.ascontiguousarray(table, np.float32)
+    if src.ndim != 3 or src.shape[2] not in (3, 4) or table.ndim != 3 or table.shape[2] != 2:
+        raise ContractError("remap_rgba8: src must be (h, w, 3|4) uint8, table (h, w, 2)")
+    g = np.asarray(gains, np.float32).reshape(3)
+    out = np.empty(table.shape[:2] + (4,), np.uint8)
+    _check(N.lib.fs_remap_rgba8(_p(src), src.shape[1], src.shape[0], src.shape[2], _p(table),
+                                table.shape[1], table.shape[0], _p(g), _p(out), None))
+    return out

@@ -187,6 +187,32 @@ fs_status fs_to_gray(const float* img, int w, int h, int ch, float* out, void* s
     });
 }
 
+// north_star stage 1 (parity unpinned: no reference counterpart)
+fs_status fs_remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float* map_xy,
+                         int w, int h, const float* gains3, uint8_t* out_rgba, void* stream) {
+    return guarded([&] {
+        if (sw <= 0 || sh <= 0 || w < 0 || h < 0 || (channels != 3 && channels != 4))
+            raise(FS_ERR_CONTRACT, "remap_rgba8: invalid image or table size");
+        float g[3] = {1.f, 1.f, 1.f};
+        if (gains3) {  // three floats, host or device
+            if (is_device_ptr(gains3))
+                FS_CK(cudaMemcpy(g, gains3, sizeof g, cudaMemcpyDeviceToHost));
+            else
+                std::memcpy(g, gains3, sizeof g);
+        }
+        if (!(g[0] >= 0.f && g[1] >= 0.f && g[2] >= 0.f))
+            raise(FS_ERR_CONTRACT, "remap_rgba8: chromaticity gains must be >= 0");
+        const size_t n = (size_t)w * h;
+        if (!n) return;
+        Stage st(stream);
+        launch::remap_rgba8(st.in(src, (size_t)sw * sh * channels), sw, sh, channels,
+                            reinterpret_cast<const float2*>(st.in(map_xy, 2 * n)), w, h, g,
+                            reinterpret_cast<uchar4*>(st.out(out_rgba, 4 * n)), st.s);
+        FS_CK(cudaGetLastError());
+        st.finish();
+    });
+}
+
 // image.hpp:98 / src/image.cpp:85-113
 fs_status fs_bilinear_sample(const float* img, const uint8_t* valid, int w, int h, int ch,
                              const double* xy, int n, float* out, void* stream) {

@@ -230,6 +230,9 @@ struct EdtJob {
 namespace launch {
 void init();     // one-time kernel attributes (call before any graph capture)
 void stamp(unsigned long long* slot, cudaStream_t);  // %globaltimer (ns) into *slot
+// fs_remap.cu: table-driven bilinear fisheye remap with chromaticity gains
+void remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float2* map, int w, int h,
+                 const float g[3], uchar4* out, cudaStream_t s);
 void lk_init();  // fs_lk.cu: LK kernels' shared-memory opt-in
 template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 // owner[p] = k where view k is valid and no earlier view claimed p
