@@ -200,6 +200,17 @@ fs_status fs_fisheye_map(const fs_fisheye_camera* cam, int canvas_w, int canvas_
 fs_status fs_remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float* map_xy,
                          int w, int h, const float* gains3, uint8_t* out_rgba, void* stream);
 
+/* Chromaticity gains (exposure compensation) of n placed RGBA8 views:
+ * view 0 keeps (1, 1, 1); view k's gain per channel makes its overlap with
+ * the earlier views (each pixel's first covering view m, scaled by gain m)
+ * agree in the mean: g_k = sum_m g_m * S[k][m] / sum_m T[k][m], where S and
+ * T are the exact integer channel sums of view m and view k over the pixels
+ * both cover (k valid, first covered by m < k).  gains: n x 3 floats out
+ * (host memory); views host or device. */
+fs_status fs_chroma_gains(int n, const uint8_t* const* views_rgba, const int* dims,
+                          const int* offsets, int canvas_w, int canvas_h, float* gains,
+                          void* stream);
+
 /* ---- pipeline fold (pipeline.hpp:63-67) ---- */
 /* stitch_placed: images[i] is dims[2i] x dims[2i+1] x ch at offsets[2i],
  * offsets[2i+1]; valids may be NULL or hold NULL entries (all valid).  The

@@ -92,3 +92,34 @@ def render_fisheye(scene, cam):
     img = scene[v, u]
     img[r > cam["radius"]] = 0
     return img
+
+
+def chroma_gains(views, offsets, canvas_w, canvas_h):
+    """(n, 3) gains: exact integer overlap sums against each pixel's first
+    covering earlier view, chained from view 0 (float64 on the host)."""
+    n = len(views)
+    owner = np.full((canvas_h, canvas_w), 255, np.int64)
+    for k, (v, (x, y)) in enumerate(zip(views, offsets)):
+        h, w = v.shape[:2]
+        sub = owner[y:y + h, x:x + w]
+        sub[(sub == 255) & (v[..., 3] >= 128)] = k
+    g = np.ones((n, 3), np.float64)
+    for k in range(1, n):
+        v, (x, y) = views[k], offsets[k]
+        h, w = v.shape[:2]
+        own = owner[y:y + h, x:x + w]
+        valid = v[..., 3] >= 128
+        num = np.zeros(3)
+        den = np.zeros(3)
+        for m in range(k):
+            sel = valid & (own == m)
+            if not sel.any():
+                continue
+            vm, (xm, ym) = views[m], offsets[m]
+            yy, xx = np.nonzero(sel)
+            q = vm[yy + y - ym, xx + x - xm, :3].astype(np.int64).sum(0)
+            p = v[yy, xx, :3].astype(np.int64).sum(0)
+            num += g[m] * q.astype(np.float64)
+            den += p.astype(np.float64)
+        g[k] = np.where(den > 0, num / np.where(den > 0, den, 1), 1.0)
+    return g.astype(np.float32)

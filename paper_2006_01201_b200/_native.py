@@ -112,6 +112,7 @@ SIGNATURES = {
                              C.POINTER(BlendParams), P, P, P, P]),
     "fs_fisheye_map": (I, [C.POINTER(FisheyeCamera), I, I, I, I, I, I, P]),
     "fs_remap_rgba8": (I, [P, I, I, I, P, I, I, P, P, P]),
+    "fs_chroma_gains": (I, [I, PP, P, P, I, I, P, P]),
     "fs_plan_create": (I, [C.POINTER(P), I, I, P, P, I, I, C.POINTER(FlowParams),
                            C.POINTER(BlendParams), PP]),
     "fs_plan_view_buffer": (P, [P, I]),

@@ -26,7 +26,7 @@ __all__ = [
     "bidirectional_flow", "flow_magnitude", "embed_flow", "distance_transform",
     "compute_blend", "softmax_weights", "blend_pair", "feather_blend", "warp_constituents",
     "misalignment_score", "estimate_translation", "TranslationEstimate", "stitch_placed",
-    "FisheyeCamera", "fisheye_map", "remap_rgba8", "set_thread_count", "thread_count",
+    "FisheyeCamera", "fisheye_map", "remap_rgba8", "chroma_gains", "set_thread_count", "thread_count",
     "resolved_thread_count",
 ]
 
@@ -556,4 +556,19 @@ def remap_rgba8(src: np.ndarray, table: np.ndarray, gains=(1.0, 1.0, 1.0)) -> np
     out = np.empty(table.shape[:2] + (4,), np.uint8)
     _check(N.lib.fs_remap_rgba8(_p(src), src.shape[1], src.shape[0], src.shape[2], _p(table),
                                 table.shape[1], table.shape[0], _p(g), _p(out), None))
+    return out
+
+
+def chroma_gains(views: Sequence[np.ndarray], offsets: Sequence, canvas_width: int,
+                 canvas_height: int) -> np.ndarray:
+    """Per-view (n, 3) chromaticity gains from the overlaps of placed RGBA8
+    views (view 0 keeps 1; include/fs_b200.h fs_chroma_gains)."""
+    vs = [np.ascontiguousarray(v, np.uint8) for v in views]
+    n = len(vs)
+    dims = np.array([(v.shape[1], v.shape[0]) for v in vs], np.int32).ravel()
+    offs = np.array(offsets, np.int32).ravel()
+    arr = C.cast((C.c_void_p * n)(*[v.ctypes.data for v in vs]), N.PP)
+    out = np.empty((n, 3), np.float32)
+    _check(N.lib.fs_chroma_gains(n, arr, _p(dims), _p(offs), canvas_width, canvas_height,
+                                 _p(out), None))
     return out

@@ -213,6 +213,53 @@ fs_status fs_remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const
     });
 }
 
+fs_status fs_chroma_gains(int n, const uint8_t* const* views_rgba, const int* dims,
+                          const int* offsets, int canvas_w, int canvas_h, float* gains,
+                          void* stream) {
+    return guarded([&] {
+        if (n < 1 || n > kMaxDagViews) raise(FS_ERR_UNSUPPORTED, "chroma_gains: 1..16 views");
+        if (!views_rgba || !dims || !offsets || !gains || canvas_w <= 0 || canvas_h <= 0)
+            raise(FS_ERR_CONTRACT, "chroma_gains: invalid arguments");
+        Stage st(stream);
+        PanoViews pv{};
+        pv.n = n;
+        for (int k = 0; k < n; ++k) {
+            Rect r{offsets[2 * k], offsets[2 * k + 1], dims[2 * k], dims[2 * k + 1]};
+            if (r.w <= 0 || r.h <= 0 || r.x0 < 0 || r.y0 < 0 || r.x1() > canvas_w ||
+                r.y1() > canvas_h)
+                raise(FS_ERR_LAYOUT, "chroma_gains: view does not fit inside the canvas");
+            pv.v[k] = ViewU8{reinterpret_cast<const uchar4*>(st.in(views_rgba[k], r.area() * 4)), r};
+        }
+        const size_t nc = (size_t)canvas_w * canvas_h;
+        uint8_t* owner = st.tmp<uint8_t>(nc + 4);
+        unsigned long long* sums = st.tmp<unsigned long long>((size_t)n * kMaxDagViews * 6);
+        FS_CK(cudaMemsetAsync(owner, 0xFF, nc + 4, st.s));
+        FS_CK(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * n * kMaxDagViews * 6, st.s));
+        for (int k = 0; k < n; ++k) launch::claim_owner(owner, canvas_w, pv.v[k], k, st.s);
+        pv.owner = owner;
+        pv.w = canvas_w;
+        for (int k = 1; k < n; ++k)
+            launch::chroma_sums(owner, canvas_w, pv.v[k], pv, k, sums + (size_t)k * kMaxDagViews * 6,
+                                st.s);
+        FS_CK(cudaGetLastError());
+        std::vector<unsigned long long> hs((size_t)n * kMaxDagViews * 6);
+        st.read(hs.data(), sums, hs.size());
+        std::vector<double> g((size_t)n * 3, 1.0);
+        for (int k = 1; k < n; ++k)
+            for (int c = 0; c < 3; ++c) {
+                double num = 0.0, den = 0.0;
+                for (int m = 0; m < k; ++m) {
+                    const unsigned long long* b = &hs[((size_t)k * kMaxDagViews + m) * 6];
+                    num += g[(size_t)m * 3 + c] * (double)b[c];
+                    den += (double)b[3 + c];
+                }
+                g[(size_t)k * 3 + c] = den > 0.0 ? num / den : 1.0;
+            }
+        for (size_t i = 0; i < g.size(); ++i) gains[i] = (float)g[i];
+        st.finish();
+    });
+}
+
 // image.hpp:98 / src/image.cpp:85-113
 fs_status fs_bilinear_sample(const float* img, const uint8_t* valid, int w, int h, int ch,
                              const double* xy, int n, float* out, void* stream) {

@@ -230,6 +230,9 @@ struct EdtJob {
 namespace launch {
 void init();     // one-time kernel attributes (call before any graph capture)
 void stamp(unsigned long long* slot, cudaStream_t);  // %globaltimer (ns) into *slot
+// fs_remap.cu: overlap channel sums of view k against its first covering views
+void chroma_sums(const uint8_t* owner, int cw, const ViewU8& vk, const PanoViews& pv, int k,
+                 unsigned long long* sums, cudaStream_t s);
 // fs_remap.cu: table-driven bilinear fisheye remap with chromaticity gains
 void remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float2* map, int w, int h,
                  const float g[3], uchar4* out, cudaStream_t s);

@@ -9,6 +9,7 @@
 // table-driven bilinear gather, one thread per output pixel, HBM-bound:
 // table 8 B + out 4 B + the source taps (~4 B, each source pixel is read
 // about once through L1/L2) per pixel.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -66,9 +67,61 @@ __global__ void __launch_bounds__(256) k_remap_rgba8(const uint8_t* __restrict__
     out[o] = make_uchar4(q[0], q[1], q[2], 255);
 }
 
+// Overlap channel sums of view k against the first covering earlier view:
+// sums[m][0..2] += view m's channels, sums[m][3..5] += view k's channels.
+__global__ void __launch_bounds__(256) k_chroma_sums(const uint8_t* __restrict__ owner, int cw,
+                                                     ViewU8 vk, PanoViews pv, int k,
+                                                     unsigned long long* __restrict__ sums) {
+    __shared__ unsigned long long bins[kMaxDagViews * 6];
+    for (int i = threadIdx.x; i < kMaxDagViews * 6; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    const int x = vk.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
+    // a thread's column mostly meets one earlier view: accumulate in
+    // registers, flush to the block's bins when the owner changes
+    int cur = -1;
+    unsigned int acc[6] = {0, 0, 0, 0, 0, 0};  // <= 8192 rows x 255 per flush fits
+    int rows = 0;
+    auto flush = [&]() {
+        if (cur >= 0)
+            for (int i = 0; i < 6; ++i)
+                if (acc[i]) atomicAdd(&bins[cur * 6 + i], (unsigned long long)acc[i]);
+        for (int i = 0; i < 6; ++i) acc[i] = 0;
+        rows = 0;
+    };
+    for (int y = vk.rect.y0 + blockIdx.y; y < vk.rect.y1() && x < vk.rect.x1(); y += gridDim.y) {
+        const uchar4 p = vk.px[(size_t)(y - vk.rect.y0) * vk.rect.w + (x - vk.rect.x0)];
+        if (p.w < 128) continue;
+        const int m = owner[(size_t)y * cw + x];
+        if (m >= k) continue;
+        if (m != cur || rows == 8192) {
+            flush();
+            cur = m;
+        }
+        const ViewU8& vm = pv.v[m];
+        const uchar4 q = vm.px[(size_t)(y - vm.rect.y0) * vm.rect.w + (x - vm.rect.x0)];
+        acc[0] += q.x;
+        acc[1] += q.y;
+        acc[2] += q.z;
+        acc[3] += p.x;
+        acc[4] += p.y;
+        acc[5] += p.z;
+        ++rows;
+    }
+    flush();
+    __syncthreads();
+    for (int i = threadIdx.x; i < k * 6; i += blockDim.x)
+        if (bins[i]) atomicAdd(&sums[i], bins[i]);
+}
+
 }  // namespace
 
 namespace launch {
+void chroma_sums(const uint8_t* owner, int cw, const ViewU8& vk, const PanoViews& pv, int k,
+                 unsigned long long* sums, cudaStream_t s) {
+    const int bx = (vk.rect.w + 255) / 256;
+    const int by = std::min(vk.rect.h, std::max(1, 148 * 8 / bx));
+    k_chroma_sums<<<dim3(bx, by), 256, 0, s>>>(owner, cw, vk, pv, k, sums);
+}
 void remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float2* map, int w, int h,
                  const float g[3], uchar4* out, cudaStream_t s) {
     if (w > 0 && h > 0)

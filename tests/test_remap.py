@@ -80,3 +80,23 @@ def test_remap_round_trip(fs):
     g = fs.remap_rgba8(photo, t, (0.5, 1.0, 1.0))
     assert np.array_equal(g, R.remap_rgba8(photo, t, (0.5, 1.0, 1.0)))
     assert g[..., 0][ok].mean() < 0.6 * view[..., 0][ok].mean() + 1
+
+
+@pytest.mark.gpu
+def test_chroma_gains_match_restatement(fs):
+    """Views of one scene with per-view exposure factors: the estimated gains
+    equal the restatement's (exact integer sums) and undo the exposure."""
+    from oracle import remap as R
+    lay = S.small_panorama(seed=3)
+    expo = [(1.0, 1.0, 1.0), (0.8, 0.9, 1.1), (1.2, 1.0, 0.85), (0.9, 1.1, 1.0),
+            (1.05, 0.95, 1.0), (0.95, 1.0, 1.05)][:len(lay.views)]
+    views = []
+    for v, e in zip(lay.views, expo):
+        w = v.copy()
+        w[..., :3] = np.clip(np.rint(v[..., :3] * np.array(e)), 0, 255).astype(np.uint8)
+        views.append(w)
+    got = fs.chroma_gains(views, lay.offsets, lay.canvas_w, lay.canvas_h)
+    want = R.chroma_gains(views, lay.offsets, lay.canvas_w, lay.canvas_h)
+    assert np.array_equal(got, want)
+    assert np.allclose(got[1], 1.0 / np.array(expo[1]), rtol=0.03)
+    assert np.array_equal(got[0], [1, 1, 1])
