@@ -244,6 +244,11 @@ fs_status fs_plan_execute_host(fs_plan plan, const uint8_t* const* views_rgba, u
 fs_status fs_plan_check(fs_plan plan);
 /* number of kernel launches of one execution (for accounting) */
 int fs_plan_launch_count(fs_plan plan);
+/* Host buffer formats of fs_plan_execute_host / fs_plan_shard_execute:
+ * views RGBA8 (4, default) or RGB8 (3: every pixel valid, expanded to RGBA8
+ * on the device), canvas RGBA8 (4, default) or RGB8 (3: alpha dropped, for
+ * canvases the views cover completely).  Fewer bytes cross PCIe. */
+fs_status fs_plan_set_host_format(fs_plan plan, int view_channels, int out_channels);
 /* bytes fs_plan_execute_host moves with page-locked buffers: views in, and
  * the canvas read back (rectangles no view covers are zeroed on the host) */
 fs_status fs_plan_transfer_bytes(fs_plan plan, size_t* h2d, size_t* d2h);

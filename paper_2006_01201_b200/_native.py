@@ -121,6 +121,7 @@ SIGNATURES = {
     "fs_plan_execute_host": (I, [P, PP, P, P]),
     "fs_plan_check": (I, [P]),
     "fs_plan_launch_count": (I, [P]),
+    "fs_plan_set_host_format": (I, [P, I, I]),
     "fs_plan_transfer_bytes": (I, [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "fs_plan_fold_info": (I, [P, I, P, P]),
     "fs_plan_profile": (I, [P, P, C.POINTER(KernelStat), I, C.POINTER(I), C.POINTER(D)]),

@@ -230,6 +230,10 @@ struct EdtJob {
 namespace launch {
 void init();     // one-time kernel attributes (call before any graph capture)
 void stamp(unsigned long long* slot, cudaStream_t);  // %globaltimer (ns) into *slot
+// RGB8 host formats: n RGB8 pixels -> RGBA8 (alpha 255); canvas rect -> RGB8
+// (canvas-indexed: out + 3 * (y * cw + x)); `in` of expand_rgb 4-byte aligned
+void expand_rgb(const uint8_t* in, uchar4* out, size_t n, cudaStream_t);
+void pack_rgb(const uchar4* in, int cw, const Rect& r, uint8_t* out, cudaStream_t);
 // fs_remap.cu: overlap channel sums of view k against its first covering views
 void chroma_sums(const uint8_t* owner, int cw, const ViewU8& vk, const PanoViews& pv, int k,
                  unsigned long long* sums, cudaStream_t s);

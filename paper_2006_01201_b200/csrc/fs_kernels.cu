@@ -967,6 +967,63 @@ template <class V>
 void union_valid(const Canvas& cv, const V& view, cudaStream_t s) {
     k_union_valid<<<row_grid(view.rect.w, view.rect.h), 256, 0, s>>>(cv, view);
 }
+// Host formats of the plan: RGB8 views (alpha implicitly 255) are expanded
+// to RGBA8 on arrival; the RGBA8 canvas is packed to RGB8 before a read-back.
+// 4 pixels per thread: 12 bytes in as three words, 16 out as one.
+__global__ void __launch_bounds__(256) k_expand_rgb(const uint8_t* __restrict__ in,
+                                                    uchar4* __restrict__ out, size_t n) {
+    const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t p0 = 4 * g;
+    if (p0 >= n) return;
+    if (p0 + 4 <= n) {
+        const uint3 w = *reinterpret_cast<const uint3*>(in + 3 * p0);  // 12-byte aligned
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&w);
+        uint4 o;
+        o.x = b[0] | (b[1] << 8) | (b[2] << 16) | 0xFF000000u;
+        o.y = b[3] | (b[4] << 8) | (b[5] << 16) | 0xFF000000u;
+        o.z = b[6] | (b[7] << 8) | (b[8] << 16) | 0xFF000000u;
+        o.w = b[9] | (b[10] << 8) | (b[11] << 16) | 0xFF000000u;
+        *reinterpret_cast<uint4*>(out + p0) = o;
+    } else {
+        for (size_t p = p0; p < n; ++p)
+            out[p] = make_uchar4(in[3 * p], in[3 * p + 1], in[3 * p + 2], 255);
+    }
+}
+// r: canvas rectangle; 4-pixel groups aligned in the flat canvas index, so
+// the 12 output bytes of a group inside the rectangle are three words.
+__global__ void __launch_bounds__(256) k_pack_rgb(const uchar4* __restrict__ in, int cw, Rect r,
+                                                  uint8_t* __restrict__ out) {
+    const int y = r.y0 + blockIdx.y;
+    const size_t row = (size_t)y * cw;
+    const size_t f = ((row + r.x0) & ~(size_t)3) + 4 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (f >= row + r.x1()) return;
+    const long long x = (long long)f - (long long)row;
+    if (x >= r.x0 && x + 4 <= r.x1()) {
+        const uint4 q = *reinterpret_cast<const uint4*>(in + f);
+        uint3 w;
+        w.x = (q.x & 0xFFFFFFu) | (q.y << 24);
+        w.y = ((q.y >> 8) & 0xFFFFu) | (q.z << 16);
+        w.z = ((q.z >> 16) & 0xFFu) | (q.w << 8);
+        *reinterpret_cast<uint3*>(out + 3 * f) = w;
+    } else {
+        for (int j = 0; j < 4; ++j) {
+            if (x + j < r.x0 || x + j >= r.x1()) continue;
+            const uchar4 q = in[f + j];
+            out[3 * (f + j)] = q.x;
+            out[3 * (f + j) + 1] = q.y;
+            out[3 * (f + j) + 2] = q.z;
+        }
+    }
+}
+void expand_rgb(const uint8_t* in, uchar4* out, size_t n, cudaStream_t s) {
+    if (n) k_expand_rgb<<<(unsigned)((n / 4 + 1 + 255) / 256), 256, 0, s>>>(in, out, n);
+}
+void pack_rgb(const uchar4* in, int cw, const Rect& r, uint8_t* out, cudaStream_t s) {
+    if (r.w > 0 && r.h > 0)
+        k_pack_rgb<<<dim3((unsigned)(((r.w + 3) / 4 + 1 + 255) / 256), r.h), 256, 0, s>>>(in, cw, r,
+                                                                                          out);
+}
+
 __global__ void k_stamp(unsigned long long* t) {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));

@@ -86,6 +86,12 @@ struct fs_plan_s {
     cudaGraph_t hgraph = nullptr;
     cudaGraphExec_t hexec = nullptr;
     std::vector<const void*> hkey;
+    // host formats (fs_plan_set_host_format): RGB8 views are expanded on
+    // arrival, the canvas packed to RGB8 before its read-backs
+    int hv_ch = 4, ho_ch = 4;
+    uint8_t* stage_in = nullptr;   // RGB8 views, 4-byte aligned each
+    std::vector<size_t> stage_off;
+    uint8_t* stage_out = nullptr;  // RGB8 canvas
     // timeline capture (fs_plan_timeline): timing events at schedule points
     bool tl = false;
     std::vector<std::pair<std::string, cudaEvent_t>> tl_marks;
@@ -148,6 +154,34 @@ PanoViews views_before(const fs_plan_s* p, int k) {
     return pv;
 }
 
+// One view's host -> device copy in the plan's host format.
+void upload_view(fs_plan_s* p, int k, const uint8_t* src, cudaStream_t st) {
+    const size_t np = (size_t)p->rects[k].w * p->rects[k].h;
+    if (p->hv_ch == 4) {
+        FS_CK(cudaMemcpyAsync(p->views[k], src, np * 4, cudaMemcpyDefault, st));
+        return;
+    }
+    uint8_t* stg = p->stage_in + p->stage_off[k];
+    FS_CK(cudaMemcpyAsync(stg, src, np * 3, cudaMemcpyDefault, st));
+    launch::expand_rgb(stg, p->views[k], np, st);
+}
+// A canvas rectangle device -> host in the plan's host format.
+void download_rect(fs_plan_s* p, const Rect& r, uint8_t* dst, cudaStream_t st) {
+    const int c = p->ho_ch;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p->out);
+    if (c == 3) {
+        launch::pack_rgb(p->out, p->cw, r, p->stage_out, st);
+        src = p->stage_out;
+    }
+    const size_t pitch = (size_t)p->cw * c;
+    const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * c;
+    if (r.w == p->cw)
+        FS_CK(cudaMemcpyAsync(dst + off, src + off, pitch * r.h, cudaMemcpyDefault, st));
+    else
+        FS_CK(cudaMemcpy2DAsync(dst + off, pitch, src + off, pitch, (size_t)r.w * c, r.h,
+                                cudaMemcpyDefault, st));
+}
+
 // Host buffers of one execute_host call (nullptr members: device-resident).
 struct HostIO {
     const uint8_t* const* views = nullptr;
@@ -159,7 +193,8 @@ struct HostIO {
 // and concurrent with the device-to-host copies instead of queued with them).
 void CUDART_CB host_fill_empty(void* arg) {
     const fs_plan_s* p = static_cast<const fs_plan_s*>(arg);
-    const size_t pitch = (size_t)p->cw * 4;
+    const size_t c = (size_t)p->ho_ch;
+    const size_t pitch = (size_t)p->cw * c;
     struct Band {
         uint8_t* dst;
         size_t row_bytes, rows;
@@ -167,12 +202,12 @@ void CUDART_CB host_fill_empty(void* arg) {
     std::vector<Band> bands;
     size_t total = 0;
     for (const Rect& r : p->empty_rects) {
-        uint8_t* d = p->hfill_out + (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
+        uint8_t* d = p->hfill_out + (size_t)r.y0 * pitch + (size_t)r.x0 * c;
         if (r.w == p->cw)
             bands.push_back({d, pitch * r.h, 1});
         else
-            bands.push_back({d, (size_t)r.w * 4, (size_t)r.h});
-        total += (size_t)r.w * r.h * 4;
+            bands.push_back({d, (size_t)r.w * c, (size_t)r.h});
+        total += (size_t)r.w * r.h * c;
     }
     auto fill = [&](size_t part, size_t nparts) {
         for (const Band& b : bands)
@@ -242,9 +277,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         if (hin) {
             FS_CK(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
             for (int k = 0; k < p->n; ++k) {
-                FS_CK(cudaMemcpyAsync(p->views[k], io->views[k],
-                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
-                                      cudaMemcpyDefault, p->h2d));
+                upload_view(p, k, io->views[k], p->h2d);
                 mark("h2d_" + std::to_string(k), p->h2d);
                 FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
             }
@@ -295,16 +328,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     // the read-backs: quantise (and copy) every rectangle once final
     // (the RGBA8 canvas is written by each pixel's writers: copies only)
     auto read_rect = [&](const Rect& r, cudaStream_t st) {
-        if (!hout) return;
-        const size_t pitch = (size_t)p->cw * 4;
-        const size_t off = (size_t)r.y0 * pitch + (size_t)r.x0 * 4;
-        if (r.w == p->cw)
-            FS_CK(cudaMemcpyAsync(io->out + off, reinterpret_cast<const uint8_t*>(p->out) + off,
-                                  pitch * r.h, cudaMemcpyDefault, st));
-        else
-            FS_CK(cudaMemcpy2DAsync(io->out + off, pitch,
-                                    reinterpret_cast<const uint8_t*>(p->out) + off, pitch,
-                                    (size_t)r.w * 4, r.h, cudaMemcpyDefault, st));
+        if (hout) download_rect(p, r, io->out, st);
     };
     // early reads of fold k: after the Area2 copies and composes that may
     // write them (all recorded by the time fold k's branch copied its Area2)
@@ -559,9 +583,7 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
         if (hin) {  // views land in fold order; each gates its claim and its fold
             FS_CK(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
             for (int k = 0; k < p->n; ++k) {
-                FS_CK(cudaMemcpyAsync(p->views[k], io->views[k],
-                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
-                                      cudaMemcpyDefault, p->h2d));
+                upload_view(p, k, io->views[k], p->h2d);
                 FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
             }
         }
@@ -645,8 +667,7 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
                                        &S.reach[k]);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
     }
-    if (seg == S.nseg - 1 && out && io && io->out)
-        FS_CK(cudaMemcpyAsync(io->out, out, (size_t)p->cw * p->chh * 4, cudaMemcpyDefault, s));
+    if (seg == S.nseg - 1 && out && io && io->out) download_rect(p, Rect{0, 0, p->cw, p->chh}, io->out, s);
     FS_CK(cudaGetLastError());
     return launches;
 }
@@ -1038,15 +1059,45 @@ void* fs_plan_view_buffer(fs_plan p, int k) {
 void* fs_plan_output_buffer(fs_plan p) { return p ? p->out : nullptr; }
 int fs_plan_launch_count(fs_plan p) { return p ? p->launches : 0; }
 
+fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels) {
+    return plan_guard([&] {
+        if (!p || (view_channels != 3 && view_channels != 4) ||
+            (out_channels != 3 && out_channels != 4))
+            raise(FS_ERR_CONTRACT, "plan: host formats are RGB8 (3) or RGBA8 (4)");
+        FS_CK(cudaSetDevice(p->device));
+        if (view_channels == p->hv_ch && out_channels == p->ho_ch) return;
+        if (view_channels == 3 && !p->stage_in) {
+            size_t off = 0;
+            p->stage_off.assign(p->n, 0);
+            for (int k = 0; k < p->n; ++k) {
+                p->stage_off[k] = off;
+                off += ((size_t)p->rects[k].w * p->rects[k].h * 3 + 255) & ~size_t(255);
+            }
+            FS_CK(cudaMalloc(&p->stage_in, off));
+        }
+        if (out_channels == 3 && !p->stage_out)
+            FS_CK(cudaMalloc(&p->stage_out, (size_t)p->cw * p->chh * 3 + 16));
+        p->hv_ch = view_channels;
+        p->ho_ch = out_channels;
+        // the graphs holding host copies were captured for the old formats
+        if (p->hexec) cudaGraphExecDestroy(p->hexec);
+        if (p->hgraph) cudaGraphDestroy(p->hgraph);
+        p->hexec = nullptr;
+        p->hgraph = nullptr;
+        p->hkey.clear();
+        drop_shard_graphs(p);
+    });
+}
+
 fs_status fs_plan_transfer_bytes(fs_plan p, size_t* h2d, size_t* d2h) {
     if (!p) return FS_ERR_CONTRACT;
-    size_t in = 0, out = (size_t)p->cw * p->chh * 4;
-    for (const Rect& r : p->rects) in += (size_t)r.w * r.h * 4;
+    size_t in = 0, out = (size_t)p->cw * p->chh * p->ho_ch;
+    for (const Rect& r : p->rects) in += (size_t)r.w * r.h * p->hv_ch;
     if (p->dag) {
         out = 0;
         for (const auto* v : {&p->early, &p->late})
             for (const auto& rbs : *v)
-                for (const auto& rb : rbs) out += (size_t)rb.r.w * rb.r.h * 4;
+                for (const auto& rb : rbs) out += (size_t)rb.r.w * rb.r.h * p->ho_ch;
     }
     if (h2d) *h2d = in;
     if (d2h) *d2h = out;
@@ -1138,15 +1189,10 @@ fs_status fs_plan_execute_host(fs_plan p, const uint8_t* const* views_rgba, uint
                 FS_CK(cudaGraphLaunch(p->hexec, s));
             } else {
                 if (views_rgba)
-                    for (int k = 0; k < p->n; ++k)
-                        FS_CK(cudaMemcpyAsync(p->views[k], views_rgba[k],
-                                              (size_t)p->rects[k].w * p->rects[k].h * 4,
-                                              cudaMemcpyDefault, s));
+                    for (int k = 0; k < p->n; ++k) upload_view(p, k, views_rgba[k], s);
                 build_graph(p);
                 FS_CK(cudaGraphLaunch(p->exec, s));
-                if (out_rgba)
-                    FS_CK(cudaMemcpyAsync(out_rgba, p->out, (size_t)p->cw * p->chh * 4,
-                                          cudaMemcpyDefault, s));
+                if (out_rgba) download_rect(p, Rect{0, 0, p->cw, p->chh}, out_rgba, s);
             }
             FS_CK(cudaStreamSynchronize(s));
             fs_status c = fs_plan_check(p);
@@ -1376,10 +1422,7 @@ fs_status fs_plan_shard_execute(fs_plan p, int segment, const uint8_t* const* vi
         for (int k = 0; vin && k < p->n; ++k) async = async && async_copyable(vin[k]);
         if (hout) async = async && async_copyable(hout);
         if (!async) {
-            for (int k = 0; vin && k < p->n; ++k)
-                FS_CK(cudaMemcpyAsync(p->views[k], vin[k],
-                                      (size_t)p->rects[k].w * p->rects[k].h * 4,
-                                      cudaMemcpyDefault, s));
+            for (int k = 0; vin && k < p->n; ++k) upload_view(p, k, vin[k], s);
             vin = nullptr;
         }
         // one key per segment slot: views (segment 0) / canvas (last segment)
@@ -1406,8 +1449,7 @@ fs_status fs_plan_shard_execute(fs_plan p, int segment, const uint8_t* const* vi
             capture_shard(p, segment, &io);
         }
         FS_CK(cudaGraphLaunch(S.exec[segment], s));
-        if (hout && !async)
-            FS_CK(cudaMemcpyAsync(hout, p->out, (size_t)p->cw * p->chh * 4, cudaMemcpyDefault, s));
+        if (hout && !async) download_rect(p, Rect{0, 0, p->cw, p->chh}, hout, s);
     });
 }
 
@@ -1448,6 +1490,8 @@ void fs_plan_destroy(fs_plan p) {
     if (p->arena) cudaFree(p->arena);
     if (p->hstats) cudaFreeHost(p->hstats);
     if (p->stamps) cudaFree(p->stamps);
+    if (p->stage_in) cudaFree(p->stage_in);
+    if (p->stage_out) cudaFree(p->stage_out);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
     if (p->shard.ev_hist) cudaEventDestroy(p->shard.ev_hist);
     if (p->shard.hist) cudaFree(p->shard.hist);

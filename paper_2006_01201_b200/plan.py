@@ -58,6 +58,10 @@ class Plan:
         _raise(N.lib.fs_plan_fold_info(self._h, k, box.ctypes.data_as(C.c_void_p), C.byref(depth)))
         return tuple(int(v) for v in box), depth.value
 
+    def set_host_format(self, view_channels: int = 4, out_channels: int = 4) -> None:
+        """Host views RGB8 (3, all valid) or RGBA8 (4); host canvas RGB8 or RGBA8."""
+        _raise(N.lib.fs_plan_set_host_format(self._h, view_channels, out_channels))
+
     def transfer_bytes(self):
         """(h2d, d2h) bytes of execute_host with page-locked buffers."""
         a, b = C.c_size_t(), C.c_size_t()

@@ -759,3 +759,36 @@ def test_gpu_matches_golden_vectors(fs):
     pyr = fs.build_pyramid(_img(fs, g["pyr_in"]), 4)
     for k, lv in enumerate(pyr):
         assert np.array_equal(lv.data[..., 0], g["pyr_l%d" % k])
+
+
+@pytest.mark.parametrize("which", ["panorama", "gaps"])
+def test_plan_rgb8_host_formats(fs, which):
+    """RGB8 host views (alpha implicit) and an RGB8 host canvas give the RGBA8
+    path's panorama (its RGB channels), through the overlapped graph
+    (page-locked) and the copy / graph / copy path (pageable)."""
+    import torch
+    lay = S.small_panorama(seed=2) if which == "panorama" else _gaps_layout()
+    assert all((v[..., 3] == 255).all() for v in lay.views)
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=3))
+    ref = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+    plan.execute_host(lay.views, ref)
+    rgb = [np.ascontiguousarray(v[..., :3]) for v in lay.views]
+    for out_ch in (4, 3):
+        plan.set_host_format(3, out_ch)
+        h2d, d2h = plan.transfer_bytes()
+        assert h2d == sum(v.nbytes for v in rgb)
+        want = ref if out_ch == 4 else np.ascontiguousarray(ref[..., :3])
+        pin = [torch.from_numpy(v).pin_memory() for v in rgb]
+        out = torch.full(want.shape, 7, dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            out.fill_(7)
+            plan.execute_ptrs([t.data_ptr() for t in pin], out.data_ptr())
+            assert np.array_equal(out.numpy(), want)
+        page = np.full(want.shape, 7, np.uint8)
+        plan.execute_host(rgb, page)
+        assert np.array_equal(page, want)
+    plan.set_host_format(4, 4)
+    again = np.empty_like(ref)
+    plan.execute_host(lay.views, again)
+    assert np.array_equal(again, ref)
+    plan.close()

@@ -18,8 +18,18 @@ def main():
     lay = {"c1": S.c1_pair, "c2": S.c2_panorama, "c3": S.c3_large_parallax, "c4": S.c4_ring}[cfg](0)
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=lay.levels))
     plan.execute_host(lay.views, None)
-    pin = [torch.from_numpy(v).pin_memory() for v in lay.views]
-    out = torch.empty((lay.canvas_h, lay.canvas_w, 4), dtype=torch.uint8).pin_memory()
+    # the bench's host formats: RGB8 views when all valid, RGB8 canvas when covered
+    import numpy as np
+    rgb_in = all(bool((v[..., 3] == 255).all()) for v in lay.views)
+    cov = np.zeros((lay.canvas_h, lay.canvas_w), bool)
+    for v, (x, y) in zip(lay.views, lay.offsets):
+        cov[y:y + v.shape[0], x:x + v.shape[1]] |= v[..., 3] >= 128
+    rgb_out = rgb_in and bool(cov.all())
+    plan.set_host_format(3 if rgb_in else 4, 3 if rgb_out else 4)
+    pin = [torch.from_numpy(np.ascontiguousarray(v[..., :3]) if rgb_in else v).pin_memory()
+           for v in lay.views]
+    out = torch.empty((lay.canvas_h, lay.canvas_w, 3 if rgb_out else 4),
+                      dtype=torch.uint8).pin_memory()
     dev = plan.timeline()
     host = plan.timeline([t.data_ptr() for t in pin], out.data_ptr())
     gdev = plan.timeline_graph()
