@@ -251,8 +251,6 @@ template <class V>
 void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t, uchar4* out = nullptr);
 template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
-// pv_count = prev->pv_count + prev->cnt2 (prev: the previous fold), or cc for fold 1
-void chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc, cudaStream_t);
 void check_box(FoldStats*, const Rect&, cudaStream_t);
 template <class V, class P>
 void crop_gray(const P&, const V&, const Rect&, int ch, float*, float*, cudaStream_t);

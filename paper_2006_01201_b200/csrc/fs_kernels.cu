@@ -141,9 +141,6 @@ __global__ void k_check_box(FoldStats* st, Rect planned) {
 __global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
     st->pv_count = cc->valid_count;
 }
-__global__ void k_chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc) {
-    st->pv_count = prev ? prev->pv_count + prev->cnt2 : cc->valid_count;
-}
 
 // |pano valid| before fold k from the claims' counts (hist[m]: pixels first
 // covered by view m)
@@ -850,9 +847,6 @@ void partition(const P& pano, const V& view, FoldStats* st, cudaStream_t s) {
 }
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t s) {
     k_snapshot_count<<<1, 1, 0, s>>>(st, cc);
-}
-void chain_count(FoldStats* st, const FoldStats* prev, const CanvasCount* cc, cudaStream_t s) {
-    k_chain_count<<<1, 1, 0, s>>>(st, prev, cc);
 }
 void check_box(FoldStats* st, const Rect& planned, cudaStream_t s) {
     k_check_box<<<1, 1, 0, s>>>(st, planned);

@@ -52,7 +52,7 @@ struct fs_plan_s {
     // k's (0: none, the L crop is read from the views alone).
     bool dag = false;
     std::vector<cudaStream_t> branch;
-    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_cnt, ev_own, ev_efork, ev_ejoin;
+    std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_own, ev_efork, ev_ejoin;
     std::vector<cudaStream_t> edt_stream;  // per fold: the distance transforms
     std::vector<cudaStream_t> tensor_stream;  // per fold: the LK structure tensors
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
@@ -1008,7 +1008,6 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
                                                    greatest));
             }
             p->ev_h2d.assign(n, nullptr);
-            p->ev_cnt.assign(n, nullptr);
             p->ev_own.assign(n, nullptr);
             p->ev_a2.assign(n, nullptr);
             p->ev_efork.assign(n, nullptr);
@@ -1017,7 +1016,6 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
                 FS_CK(cudaEventCreateWithFlags(&p->ev_branch[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_compose[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
-                FS_CK(cudaEventCreateWithFlags(&p->ev_cnt[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_own[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_a2[k], cudaEventDisableTiming));
                 FS_CK(cudaEventCreateWithFlags(&p->ev_efork[k], cudaEventDisableTiming));
@@ -1474,8 +1472,6 @@ void fs_plan_destroy(fs_plan p) {
     for (auto e : p->ev_compose)
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_h2d)
-        if (e) cudaEventDestroy(e);
-    for (auto e : p->ev_cnt)
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_own)
         if (e) cudaEventDestroy(e);
