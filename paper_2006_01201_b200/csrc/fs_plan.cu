@@ -4,6 +4,7 @@
 // (partition, crop+gray, pyramid, bidirectional LK, distance transforms,
 // Code 1 blend, composition, 8-bit quantisation) from the views in HBM.
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <climits>
 #include <cstring>
@@ -113,7 +114,13 @@ struct fs_plan_s {
         std::vector<cudaGraphExec_t> exec;
         cudaEvent_t ev_seg = nullptr;
         std::vector<int> launches;  // per segment
-        std::vector<const void*> hkey;  // host pointers captured into the segments
+        std::vector<std::vector<const void*>> hkeys;  // host pointers captured, per segment
+        // rank 0's read-backs per segment: [seg][0] once the segment's strips
+        // are composed (segment 0: the first-cover copies), [seg][1] after its
+        // own folds' composes
+        std::vector<std::array<std::vector<fs_plan_s::Readback>, 2>> reads;
+        cudaEvent_t ev_place0 = nullptr;  // view 0's first-cover copy on rank 0
+        cudaEvent_t ev_segend = nullptr, ev_d2h = nullptr;
         Rect clip;                          // first-cover copies needed here (rank != 0)
         unsigned long long* hist = nullptr;  // owner-plane histogram (|pano valid| per fold)
         cudaEvent_t ev_hist = nullptr;
@@ -566,12 +573,37 @@ void shard_configure(fs_plan_s* p, int nranks, int rank, const int* fold_rank) {
             present[k] = 1;
         }
     }
+    // rank 0's read-back pieces (the DAG's split of the canvas): each is
+    // final once every fold whose box meets it has been composed here
+    S.reads.assign(S.nseg, {});
+    if (rank == 0) {
+        auto seg_of = [&](int m) { return S.stage[m] + (S.fold_rank[m] == 0 ? 0 : 1); };
+        for (const auto* lists : {&p->early, &p->late})
+            for (const auto& rbs : *lists)
+                for (const auto& rb : rbs) {
+                    int rs = 0;
+                    bool own_last = false;
+                    for (int m = 1; m < n; ++m) {
+                        if (!rects_meet(p->boxes[m], rb.r)) continue;
+                        const int sm = seg_of(m);
+                        if (sm > rs) {
+                            rs = sm;
+                            own_last = false;
+                        }
+                        if (sm == rs && S.fold_rank[m] == 0) own_last = true;
+                    }
+                    S.reads[rs][own_last ? 1 : 0].push_back(rb);
+                }
+    }
     S.exec.assign(S.nseg, nullptr);
     S.graph.assign(S.nseg, nullptr);
     S.launches.assign(S.nseg, 0);
-    S.hkey.clear();
+    S.hkeys.clear();
     if (!S.ev_seg) FS_CK(cudaEventCreateWithFlags(&S.ev_seg, cudaEventDisableTiming));
     if (!S.ev_hist) FS_CK(cudaEventCreateWithFlags(&S.ev_hist, cudaEventDisableTiming));
+    if (!S.ev_segend) FS_CK(cudaEventCreateWithFlags(&S.ev_segend, cudaEventDisableTiming));
+    if (!S.ev_place0) FS_CK(cudaEventCreateWithFlags(&S.ev_place0, cudaEventDisableTiming));
+    if (!S.ev_d2h) FS_CK(cudaEventCreateWithFlags(&S.ev_d2h, cudaEventDisableTiming));
     if (!S.hist) FS_CK(cudaMalloc(&S.hist, sizeof(unsigned long long) * kMaxDagViews));
 }
 
@@ -596,6 +628,12 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
                 FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
             }
         }
+        if (out && io && io->out && !p->empty_rects.empty()) {  // uncovered canvas: host zeroes
+            p->hfill_out = io->out;
+            FS_CK(cudaStreamWaitEvent(p->hfill, p->ev_start, 0));
+            FS_CK(cudaLaunchHostFunc(p->hfill, host_fill_empty, p));
+            FS_CK(cudaEventRecord(p->ev_hfill1, p->hfill));
+        }
         // the canvas writers (first-cover copies) start after the clear
         if (out) FS_CK(cudaMemsetAsync(out, 0, (size_t)p->cw * p->chh * 4, s));
         FS_CK(cudaEventRecord(p->ev_place, s));
@@ -619,6 +657,7 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
             launch::compose_area2(p->cv, view_of(p, 0), p->owner, 0, s, out, clip, &S.clip);
             ++launches;
         }
+        FS_CK(cudaEventRecord(S.ev_place0, s));
         for (int k = 1; k < p->n; ++k) {
             const bool mine = S.fold_rank[k] == S.rank;
             if (!mine && S.rank != 0 && S.clip.w <= 0) continue;
@@ -645,6 +684,19 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
         ++launches;
     }
     FS_CK(cudaEventRecord(S.ev_seg, s));
+    const bool reads = out && io && io->out;
+    if (reads && !S.reads[seg][0].empty()) {  // final once this segment's strips are in
+        if (seg == 0) {  // first-cover pieces: as soon as their own copies are done
+            for (const auto& rb : S.reads[0][0]) {
+                if (rb.place) FS_CK(cudaStreamWaitEvent(p->d2h, S.ev_place0, 0));
+                for (int m : rb.a2) FS_CK(cudaStreamWaitEvent(p->d2h, p->ev_a2[m], 0));
+                download_rect(p, rb.r, io->out, p->d2h);
+            }
+        } else {
+            FS_CK(cudaStreamWaitEvent(p->d2h, S.ev_seg, 0));
+            for (const auto& rb : S.reads[seg][0]) download_rect(p, rb.r, io->out, p->d2h);
+        }
+    }
     const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
     for (int k : S.own[seg]) {
         FoldWS<ViewU8>& f = p->folds[k - 1];
@@ -676,7 +728,18 @@ int enqueue_shard(fs_plan_s* p, cudaStream_t s, int seg, const HostIO* io) {
                                        &S.reach[k]);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
     }
-    if (seg == S.nseg - 1 && out && io && io->out) download_rect(p, Rect{0, 0, p->cw, p->chh}, io->out, s);
+    if (reads) {
+        if (!S.reads[seg][1].empty()) {  // after this segment's own composes
+            FS_CK(cudaEventRecord(S.ev_segend, s));
+            FS_CK(cudaStreamWaitEvent(p->d2h, S.ev_segend, 0));
+            for (const auto& rb : S.reads[seg][1]) download_rect(p, rb.r, io->out, p->d2h);
+        }
+        if (!S.reads[seg][0].empty() || !S.reads[seg][1].empty()) {
+            FS_CK(cudaEventRecord(S.ev_d2h, p->d2h));
+            FS_CK(cudaStreamWaitEvent(s, S.ev_d2h, 0));
+        }
+        if (seg == 0 && !p->empty_rects.empty()) FS_CK(cudaStreamWaitEvent(s, p->ev_hfill1, 0));
+    }
     FS_CK(cudaGetLastError());
     return launches;
 }
@@ -726,7 +789,7 @@ void drop_shard_graphs(fs_plan_s* p) {
             cudaGraphDestroy(g);
             g = nullptr;
         }
-    S.hkey.clear();
+    S.hkeys.clear();
 }
 
 void build_graph(fs_plan_s* p) {
@@ -1422,43 +1485,36 @@ fs_status fs_plan_shard_execute(fs_plan p, int segment, const uint8_t* const* vi
         if ((int)S.exec.size() != S.nseg) shard_configure(p, S.nranks, S.rank, S.fold_rank.data());
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         // host buffers the graphs can copy asynchronously are captured into
-        // segment 0 (views, overlapping the folds) and the last segment (the
-        // canvas); others are copied around the graphs
+        // the segments: the views into segment 0 (overlapping the folds), the
+        // canvas pieces on rank 0 into the segment after which each is final;
+        // pageable buffers are copied around the graphs
         const bool last = segment == S.nseg - 1;
         const uint8_t* const* vin = segment == 0 ? views_rgba : nullptr;
-        uint8_t* hout = last && S.rank == 0 ? out_rgba : nullptr;
-        bool async = true;
-        for (int k = 0; vin && k < p->n; ++k) async = async && async_copyable(vin[k]);
-        if (hout) async = async && async_copyable(hout);
-        if (!async) {
-            for (int k = 0; vin && k < p->n; ++k) upload_view(p, k, vin[k], s);
+        uint8_t* hout = S.rank == 0 ? out_rgba : nullptr;
+        bool async_in = true;
+        for (int k = 0; vin && k < p->n; ++k) async_in = async_in && async_copyable(vin[k]);
+        const bool async_out = hout && async_copyable(hout);
+        if (vin && !async_in) {
+            for (int k = 0; k < p->n; ++k) upload_view(p, k, vin[k], s);
             vin = nullptr;
         }
-        // one key per segment slot: views (segment 0) / canvas (last segment)
-        if (S.hkey.size() != (size_t)p->n + 1) S.hkey.assign(p->n + 1, nullptr);
-        auto rekey = [&](size_t i, const void* v) {
-            if (S.hkey[i] != v) {
-                S.hkey[i] = v;
-                return true;
-            }
-            return false;
-        };
-        bool stale = false;
-        if (segment == 0)
-            for (int k = 0; k < p->n; ++k) stale = rekey(k, vin ? vin[k] : nullptr) || stale;
-        if (last) stale = rekey(p->n, async ? hout : nullptr) || stale;
-        if (stale && S.exec[segment]) {
+        std::vector<const void*> key;
+        for (int k = 0; vin && k < p->n; ++k) key.push_back(vin[k]);
+        key.push_back(async_out ? hout : nullptr);
+        if (S.hkeys.size() != (size_t)S.nseg) S.hkeys.assign(S.nseg, {});
+        if (S.hkeys[segment] != key && S.exec[segment]) {
             cudaGraphExecDestroy(S.exec[segment]);
             cudaGraphDestroy(S.graph[segment]);
             S.exec[segment] = nullptr;
             S.graph[segment] = nullptr;
         }
         if (!S.exec[segment]) {
-            HostIO io{vin, async ? hout : nullptr};
+            HostIO io{vin, async_out ? hout : nullptr};
             capture_shard(p, segment, &io);
+            S.hkeys[segment] = key;
         }
         FS_CK(cudaGraphLaunch(S.exec[segment], s));
-        if (hout && !async) download_rect(p, Rect{0, 0, p->cw, p->chh}, hout, s);
+        if (last && hout && !async_out) download_rect(p, Rect{0, 0, p->cw, p->chh}, hout, s);
     });
 }
 
@@ -1502,6 +1558,9 @@ void fs_plan_destroy(fs_plan p) {
     if (p->stage_out) cudaFree(p->stage_out);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
     if (p->shard.ev_hist) cudaEventDestroy(p->shard.ev_hist);
+    if (p->shard.ev_segend) cudaEventDestroy(p->shard.ev_segend);
+    if (p->shard.ev_place0) cudaEventDestroy(p->shard.ev_place0);
+    if (p->shard.ev_d2h) cudaEventDestroy(p->shard.ev_d2h);
     if (p->shard.hist) cudaFree(p->shard.hist);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete p;

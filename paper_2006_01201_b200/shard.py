@@ -171,7 +171,7 @@ class ShardedPlan:
         arg = None
         if view_ptrs is not None and segment == 0:
             arg = C.cast((C.c_void_p * self.plan.n)(*view_ptrs), N.PP)
-        outp = C.c_void_p(out_ptr) if (out_ptr and segment == self.n_segments - 1) else None
+        outp = C.c_void_p(out_ptr) if out_ptr else None  # rank 0 reads pieces as they finish
         _raise(N.lib.fs_plan_shard_execute(self.plan._h, segment, arg, outp,
                                            C.c_void_p(_stream_handle(stream))))
 
