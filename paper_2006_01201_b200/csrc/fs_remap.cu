@@ -18,53 +18,89 @@
 namespace fs {
 namespace {
 
+// byte -> float without the conversion pipe: 2^23 + b as a float's bits
+// (exact), minus 2^23; and back for an integer-valued float in [0, 255]
+constexpr float kMagic = 8388608.f;
+
+struct RemapTap {
+    bool ok;
+    size_t p[4];     // tap pixels 00, 10, 01, 11
+    float w[4];      // their bilinear weights
+};
+__device__ __forceinline__ RemapTap remap_tap(float2 m, int sw, int sh) {
+    RemapTap t;
+    t.ok = m.x >= 0.f && m.y >= 0.f && m.x <= (float)(sw - 1) && m.y <= (float)(sh - 1);
+    const float mx = t.ok ? m.x : 0.f, my = t.ok ? m.y : 0.f;
+    const int x0 = (int)floorf(mx), y0 = (int)floorf(my);
+    const int x1 = min(x0 + 1, sw - 1), y1 = min(y0 + 1, sh - 1);
+    const float fx = mx - (float)x0, fy = my - (float)y0;
+    t.w[0] = (1.f - fx) * (1.f - fy);
+    t.w[1] = fx * (1.f - fy);
+    t.w[2] = (1.f - fx) * fy;
+    t.w[3] = fx * fy;
+    t.p[0] = (size_t)y0 * sw + x0;
+    t.p[1] = (size_t)y0 * sw + x1;
+    t.p[2] = (size_t)y1 * sw + x0;
+    t.p[3] = (size_t)y1 * sw + x1;
+    return t;
+}
+__device__ __forceinline__ unsigned int remap_combine(const RemapTap& t, const float (&v)[4][3],
+                                                      const float (&g)[3]) {
+    if (!t.ok) return 0u;
+    unsigned int packed = 0xFF000000u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float s = ((t.w[0] * v[0][c] + t.w[1] * v[1][c]) + t.w[2] * v[2][c]) + t.w[3] * v[3][c];
+        float r = floorf(s * g[c] + 0.5f);
+        r = r < 255.f ? r : 255.f;
+        packed |= (__float_as_uint(r + kMagic) & 0xFFu) << (8 * c);
+    }
+    return packed;
+}
+
+// Two output pixels per thread (the loads of both issued before either is
+// combined).
 __global__ void __launch_bounds__(256) k_remap_rgba8(const uint8_t* __restrict__ src, int sw, int sh,
                                                      int channels, const float2* __restrict__ map,
                                                      int w, int h, float g0, float g1, float g2,
                                                      uchar4* __restrict__ out) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const int y = blockIdx.y;
     if (x >= w) return;
+    const bool two = x + 1 < w;
     const size_t o = (size_t)y * w + x;
-    const float2 m = map[o];
-    if (!(m.x >= 0.f && m.y >= 0.f && m.x <= (float)(sw - 1) && m.y <= (float)(sh - 1))) {
-        out[o] = make_uchar4(0, 0, 0, 0);
-        return;
-    }
-    const int x0 = (int)floorf(m.x), y0 = (int)floorf(m.y);
-    const int x1 = min(x0 + 1, sw - 1), y1 = min(y0 + 1, sh - 1);
-    const float fx = m.x - (float)x0, fy = m.y - (float)y0;
-    const float w00 = (1.f - fx) * (1.f - fy), w10 = fx * (1.f - fy);
-    const float w01 = (1.f - fx) * fy, w11 = fx * fy;
+    const float2 ma = map[o];
+    const float2 mb = two ? map[o + 1] : make_float2(-1.f, -1.f);
+    const RemapTap ta = remap_tap(ma, sw, sh), tb = remap_tap(mb, sw, sh);
     const float g[3] = {g0, g1, g2};
-    float t[4][3];  // the four taps' channels
-    const size_t p00 = (size_t)y0 * sw + x0, p10 = (size_t)y0 * sw + x1;
-    const size_t p01 = (size_t)y1 * sw + x0, p11 = (size_t)y1 * sw + x1;
+    float va[4][3], vb[4][3];
     if (channels == 4) {  // one 32-bit load per tap
-        const uchar4* s4 = reinterpret_cast<const uchar4*>(src);
-        const uchar4 a = __ldg(s4 + p00), b = __ldg(s4 + p10), c = __ldg(s4 + p01), d = __ldg(s4 + p11);
-        const uchar4 tp[4] = {a, b, c, d};
+        const unsigned int* s4 = reinterpret_cast<const unsigned int*>(src);
+        unsigned int qa[4], qb[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            t[k][0] = (float)tp[k].x;
-            t[k][1] = (float)tp[k].y;
-            t[k][2] = (float)tp[k].z;
+            qa[k] = __ldg(s4 + ta.p[k]);
+            qb[k] = __ldg(s4 + tb.p[k]);
         }
-    } else {
-        const size_t pk[4] = {p00, p10, p01, p11};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) t[k][c] = (float)__ldg(src + pk[k] * 3 + c);
-    }
-    uint8_t q[3];
+            for (int c = 0; c < 3; ++c) {
+                va[k][c] = __uint_as_float(__byte_perm(qa[k], 0x4B000000u, 0x7440u | c)) - kMagic;
+                vb[k][c] = __uint_as_float(__byte_perm(qb[k], 0x4B000000u, 0x7440u | c)) - kMagic;
+            }
+    } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const float v = ((w00 * t[0][c] + w10 * t[1][c]) + w01 * t[2][c]) + w11 * t[3][c];
-        const float r = floorf(v * g[c] + 0.5f);
-        q[c] = (uint8_t)(r < 255.f ? r : 255.f);
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                va[k][c] = (float)__ldg(src + ta.p[k] * 3 + c);
+                vb[k][c] = (float)__ldg(src + tb.p[k] * 3 + c);
+            }
     }
-    out[o] = make_uchar4(q[0], q[1], q[2], 255);
+    unsigned int* o32 = reinterpret_cast<unsigned int*>(out);
+    o32[o] = remap_combine(ta, va, g);
+    if (two) o32[o + 1] = remap_combine(tb, vb, g);
 }
 
 // Overlap channel sums of view k against the first covering earlier view:
@@ -125,7 +161,7 @@ void chroma_sums(const uint8_t* owner, int cw, const ViewU8& vk, const PanoViews
 void remap_rgba8(const uint8_t* src, int sw, int sh, int channels, const float2* map, int w, int h,
                  const float g[3], uchar4* out, cudaStream_t s) {
     if (w > 0 && h > 0)
-        k_remap_rgba8<<<dim3((w + 255) / 256, h), 256, 0, s>>>(src, sw, sh, channels, map, w, h,
+        k_remap_rgba8<<<dim3((w + 511) / 512, h), 256, 0, s>>>(src, sw, sh, channels, map, w, h,
                                                                g[0], g[1], g[2], out);
 }
 }  // namespace launch
