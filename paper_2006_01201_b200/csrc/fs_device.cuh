@@ -28,6 +28,12 @@ struct Canvas {
     int w, h, ch;
 };
 
+// (float)b of a byte without the conversion pipe: 2^23 + b is a float's
+// bits with b in the low mantissa byte (exact), minus 2^23.
+__device__ __forceinline__ float u8f(unsigned int word, int byte) {
+    return __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7440u | byte)) - 8388608.f;
+}
+
 // A placed view in 8-bit RGBA (alpha >= 128 is valid, src/image.cpp:38-39),
 // value = byte * (1/255) exactly as load_image (src/image.cpp:31-37).
 struct ViewU8 {
@@ -38,9 +44,10 @@ struct ViewU8 {
         return px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)].w >= 128;
     }
     __device__ __forceinline__ float4 value_at(int x, int y) const {
-        uchar4 p = px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)];
+        const unsigned int p =
+            reinterpret_cast<const unsigned int*>(px)[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)];
         const float s = 1.0f / 255.0f;
-        return make_float4(p.x * s, p.y * s, p.z * s, 0.f);
+        return make_float4(u8f(p, 0) * s, u8f(p, 1) * s, u8f(p, 2) * s, 0.f);
     }
 };
 
