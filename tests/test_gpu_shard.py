@@ -180,3 +180,22 @@ def test_sharded_host_io(fs, name):
     assert sp.status() == 0
     assert np.array_equal(out3, ref)
     plan.close()
+
+
+def test_sharded_host_io_rgb8(fs):
+    """The seam-sharded execution with RGB8 host views and canvas."""
+    import torch
+    from paper_2006_01201_b200.shard import ShardedPlan
+    lay = LAYOUTS["panorama"]()
+    params = fs.FlowParams(levels=3)
+    ref = _unsharded(fs, lay, params)
+    plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params, views_rgba=lay.views)
+    plan.set_host_format(3, 3)
+    sp = ShardedPlan(plan, 1, 0)
+    pin = [torch.from_numpy(np.ascontiguousarray(v[..., :3])).pin_memory() for v in lay.views]
+    out = torch.full((lay.canvas_h, lay.canvas_w, 3), 7, dtype=torch.uint8).pin_memory()
+    for _ in range(2):
+        out.fill_(7)
+        assert sp.run([t.data_ptr() for t in pin], out.data_ptr()) == "sharded"
+        assert np.array_equal(out.numpy(), ref[..., :3])
+    plan.close()
