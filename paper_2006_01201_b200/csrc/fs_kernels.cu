@@ -287,6 +287,137 @@ __global__ void __launch_bounds__(SM_TX* SM_TY, 3) k_smooth(SmoothArgs a) {
         smooth_tile<false>(a, src, p1);
 }
 
+// K4, column-sweep form: a CTA of S2_T threads owns S2_T - 4 output columns
+// and S2_OY output rows.  The (S2_OY + 4) x S2_T input tile is staged once;
+// each thread then walks one column down, carrying the two previous rows of
+// its 3x3 window in registers as doubles (every staged float is widened once
+// per window row instead of nine times), first for the pass-1 plane
+// ((S2_OY + 2) x (S2_T - 2), staged in shared memory) and then for the
+// output.  Out-of-image taps are staged as -0.0, the exact identity of
+// double addition, so the reference's skip-and-count (src/flow.cpp:113-130)
+// becomes a plain sum divided by (in-image rows) x (in-image columns).
+constexpr int S2_T = 128;
+#ifndef FS_SMOOTH_OY
+#define FS_SMOOTH_OY 8
+#endif
+constexpr int S2_OY = FS_SMOOTH_OY;
+#ifndef FS_SMOOTH2_MIN_PX
+#define FS_SMOOTH2_MIN_PX 100000
+#endif
+constexpr int S2_OX = S2_T - 4;
+
+// One column of 3x3 means: outputs q = 0..rows-1 read input rows q..q+2 at
+// columns t..t+2.  gx/gy0: global position of output (0, this column).
+template <bool INNER, class Sink>
+__device__ __forceinline__ void sweep3(const float2 (*in)[S2_T], int t, int rows, int gx,
+                                       int gy0, int w, int h, Sink sink) {
+    double x0[3], y0[3], x1[3], y1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float2 a = in[0][t + k], b = in[1][t + k];
+        x0[k] = a.x; y0[k] = a.y; x1[k] = b.x; y1[k] = b.y;
+    }
+    int ncol = 3;
+    if (!INNER) ncol = 3 - (gx - 1 < 0) - (gx + 1 >= w);
+#pragma unroll 4
+    for (int q = 0; q < rows; ++q) {
+        double x2[3], y2[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float2 c = in[q + 2][t + k];
+            x2[k] = c.x; y2[k] = c.y;
+        }
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { ax += x0[k]; ay += y0[k]; }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { ax += x1[k]; ay += y1[k]; }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { ax += x2[k]; ay += y2[k]; }
+        int n = 9;
+        if (!INNER) {
+            const int gy = gy0 + q;
+            n = ncol * (3 - (gy - 1 < 0) - (gy + 1 >= h));
+        }
+        sink(q, div_to_float(ax, n, kInvSmall[n]), div_to_float(ay, n, kInvSmall[n]));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            x0[k] = x1[k]; y0[k] = y1[k]; x1[k] = x2[k]; y1[k] = y2[k];
+        }
+    }
+}
+
+template <bool INNER>
+__device__ __forceinline__ void smooth2_tile(const SmoothArgs& a, float2 (*src)[S2_T],
+                                             float2 (*p1)[S2_T]) {
+    const int d = blockIdx.z;
+    const int w = a.w, h = a.h;
+    const int bx = blockIdx.x * S2_OX, by = blockIdx.y * S2_OY;
+    const int t = threadIdx.x;
+    const float2 nz = make_float2(-0.f, -0.f);
+    const float2(*last)[S2_T] = src;
+    int lastoff = 0;  // the last pass reads columns t..t+2 of `last` at offset lastoff
+    if (a.passes == 2) {
+        if (t < S2_T - 2) {
+            const int gx = bx - 1 + t;
+            const bool colin = gx >= 0 && gx < w;
+            sweep3<INNER>(src, t, S2_OY + 2, gx, by - 1, w, h, [&](int q, float vx, float vy) {
+                const int gy = by - 1 + q;
+                p1[q][t + 1] = (INNER || (colin && gy >= 0 && gy < h)) ? make_float2(vx, vy) : nz;
+            });
+        }
+        __syncthreads();
+        last = p1;
+        lastoff = 1;
+    }
+    if (t >= S2_OX) return;
+    const int gx = bx + t;
+    if (gx >= w) return;
+    float2* fo = d ? a.fout[1] : a.fout[0];
+    const uint8_t* ok = d ? a.ok[1] : a.ok[0];
+    uint8_t* vo = d ? a.valid_out[1] : a.valid_out[0];
+    const int rows = min(S2_OY, h - by);
+    sweep3<INNER>((const float2(*)[S2_T])(&last[0][lastoff]), t, rows, gx, by, w, h,
+                  [&](int q, float vx, float vy) {
+                      const size_t o = (size_t)(by + q) * w + gx;
+                      if (a.final_cap > 0.f) {
+                          final_cap(a.final_cap, vx, vy);
+                          vo[o] = ok[o];
+                      }
+                      fo[o] = make_float2(vx, vy);
+                  });
+}
+
+__global__ void __launch_bounds__(S2_T) k_smooth2(SmoothArgs a) {
+    __shared__ float2 src[S2_OY + 4][S2_T];
+    __shared__ float2 p1[S2_OY + 2][S2_T];
+    const int d = blockIdx.z;
+    const float2* fin = d ? a.fin[1] : a.fin[0];
+    const int w = a.w, h = a.h;
+    const int bx = blockIdx.x * S2_OX, by = blockIdx.y * S2_OY;
+    const int t = threadIdx.x;
+    // one pass reads the tile from row 1 (its outputs need rows by-1..)
+    const int gx = bx - 2 + t;
+    const bool colin = gx >= 0 && gx < w;
+#pragma unroll
+    for (int r = 0; r < S2_OY + 4; ++r) {
+        const int gy = by - 2 + r;
+        float2 v = make_float2(-0.f, -0.f);
+        if (colin && gy >= 0 && gy < h) v = fin[(size_t)gy * w + gx];
+        src[r][t] = v;
+    }
+    __syncthreads();
+    const bool inner = bx >= 2 && by >= 2 && bx + S2_OX + 2 <= w && by + S2_OY + 2 <= h;
+    if (a.passes == 2) {
+        if (inner) smooth2_tile<true>(a, src, p1);
+        else smooth2_tile<false>(a, src, p1);
+    } else {
+        // one pass: outputs read src rows q+1..q+3, columns t+1..t+3
+        if (inner) smooth2_tile<true>(a, (float2(*)[S2_T])&src[1][1], p1);
+        else smooth2_tile<false>(a, (float2(*)[S2_T])&src[1][1], p1);
+    }
+}
+
 // Level-0 finalisation when smoothing_passes == 0 (src/flow.cpp:300-313).
 __global__ void k_finalize_flow(SmoothArgs a) {
     const int d = blockIdx.z;
@@ -866,8 +997,19 @@ void downsample(const float* in0, const float* in1, float* out0, float* out1, in
 void init() { lk_init(); }
 
 void smooth(const SmoothArgs& a, cudaStream_t s) {
+#ifdef FS_SMOOTH_TILE2D
     dim3 g((a.w + SM_OX - 1) / SM_OX, (a.h + SM_OY - 1) / SM_OY, a.ndir);
     k_smooth<<<g, dim3(SM_TX, SM_TY), 0, s>>>(a);
+#else
+    // small (coarse) levels keep the 2-D tiles: more CTAs for the few pixels
+    if ((long long)a.w * a.h < FS_SMOOTH2_MIN_PX) {
+        dim3 g((a.w + SM_OX - 1) / SM_OX, (a.h + SM_OY - 1) / SM_OY, a.ndir);
+        k_smooth<<<g, dim3(SM_TX, SM_TY), 0, s>>>(a);
+        return;
+    }
+    dim3 g((a.w + S2_OX - 1) / S2_OX, (a.h + S2_OY - 1) / S2_OY, a.ndir);
+    k_smooth2<<<g, S2_T, 0, s>>>(a);
+#endif
 }
 void finalize_flow(const SmoothArgs& a, cudaStream_t s) {
     int n = a.w * a.h;

@@ -84,13 +84,30 @@ FS_HD void final_cap(float cap, float& x, float& y) {
 }
 
 // (float)(acc / n), as the reference rounds it (double division, then float
-// conversion).  The device double division is IEEE round-to-nearest (a
-// reciprocal seed plus DFMA refinement, ~10 instructions; its slow path only
-// for extreme exponents), so no cheaper exact form exists.  inv_n is unused
-// (kept for the call sites' signature).
+// conversion).  On the device without the double division: with inv_n =
+// RN(1/n), q = acc * inv_n lies within 2.5 double ulps of RN(acc / n), so both
+// round to the same float unless q's 29 bits below float precision are within
+// 4 of the float rounding midpoint, or q is outside the normal float range
+// (zero excepted); those rare cases divide exactly, out of line (a branch, not
+// predicated work).
+#ifdef __CUDACC__
+__device__ __noinline__ inline float div_exact_slow(double acc, double n) {
+    return static_cast<float>(acc / n);
+}
+#endif
 FS_HD float div_to_float(double acc, double n, double inv_n) {
+#if defined(__CUDA_ARCH__) && !defined(FS_EXACT_DIV)
+    const double q = acc * inv_n;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    const unsigned lo = (unsigned)b & 0x1FFFFFFFu;
+    const unsigned e = (unsigned)(b >> 52) & 0x7FFu;
+    if ((e - 897u <= 253u && lo - (0x10000000u - 4u) > 8u) || (b << 1) == 0)
+        return static_cast<float>(q);
+    return div_exact_slow(acc, n);
+#else
     (void)inv_n;
     return static_cast<float>(acc / n);
+#endif
 }
 
 // src/flow.cpp:267-291 — the 2x2 structure-tensor solve of one pixel.
