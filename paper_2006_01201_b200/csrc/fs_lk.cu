@@ -128,26 +128,68 @@ __device__ __forceinline__ TapF level_tap_f(int w, int h, float px, float py) {
     return t;
 }
 
-// ---- per-level start: flow, ever_ok and It ---------------------------------
+// ---- per-level start: flow and ever_ok --------------------------------------
+// A thread owns one column and LK_PREP_ROWS rows 8 apart: the column half of
+// the align-centres tap (src/flow.cpp:150-157: x0, x1, fx, nearest xn) is
+// computed once, the row half per row (uniform across the warp), and the four
+// bilinear weights once per pixel for both components — the same expressions
+// in the same order as src/flow.cpp:158-166, so the values are unchanged.
+#ifndef LK_PREP_ROWS
+#define LK_PREP_ROWS 4
+#endif
 template <int MODE>  // 0: zero flow (coarsest level), 2: upsample the coarser level
 __global__ void __launch_bounds__(256) k_lk_prep(LkArgs a) {
     const LkDir& D = a.d[blockIdx.z];
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (x >= a.w || y >= a.h) return;
-    float2 f = make_float2(0.f, 0.f);
-    uint8_t ok = 0;
+    if (x >= a.w) return;
+    const int yb = blockIdx.y * (8 * LK_PREP_ROWS) + (threadIdx.x >> 5);
+    int x0 = 0, x1 = 0, xn = 0;
+    double fx = 0.0;
     if (MODE == 2) {
-        UpTap t = up_tap(x, y, a.sx, a.sy, a.cw, a.ch);
-        float2 f00 = D.fin[(size_t)t.y0 * a.cw + t.x0], f10 = D.fin[(size_t)t.y0 * a.cw + t.x1];
-        float2 f01 = D.fin[(size_t)t.y1 * a.cw + t.x0], f11 = D.fin[(size_t)t.y1 * a.cw + t.x1];
-        f = make_float2(up_combine(t, f00.x, f10.x, f01.x, f11.x),
-                        up_combine(t, f00.y, f10.y, f01.y, f11.y));
-        ok = D.okin[(size_t)t.yn * a.cw + t.xn];
+        const double xc = clampd((x + 0.5) * a.sx - 0.5, 0.0, a.cw - 1.0);
+        x0 = static_cast<int>(xc);
+        x1 = imin(x0 + 1, a.cw - 1);
+        fx = xc - x0;
+        xn = clampi(static_cast<int>(lround(xc)), 0, a.cw - 1);
     }
-    const size_t o = (size_t)y * a.w + x;
-    D.fout[o] = f;
-    D.okout[o] = ok;
+#pragma unroll
+    for (int k = 0; k < LK_PREP_ROWS; ++k) {
+        const int y = yb + 8 * k;
+        if (y >= a.h) return;
+        float2 f = make_float2(0.f, 0.f);
+        uint8_t ok = 0;
+        if (MODE == 2) {
+            const double yc = clampd((y + 0.5) * a.sy - 0.5, 0.0, a.ch - 1.0);
+            const int y0 = static_cast<int>(yc);
+            const int y1 = imin(y0 + 1, a.ch - 1);
+            const double fy = yc - y0;
+            const int yn = clampi(static_cast<int>(lround(yc)), 0, a.ch - 1);
+            const float2* r0 = D.fin + (size_t)y0 * a.cw;
+            const float2* r1 = D.fin + (size_t)y1 * a.cw;
+            const float2 f00 = __ldg(r0 + x0), f10 = __ldg(r0 + x1);
+            const float2 f01 = __ldg(r1 + x0), f11 = __ldg(r1 + x1);
+            const double w00 = (1 - fx) * (1 - fy), w10 = fx * (1 - fy);
+            const double w01 = (1 - fx) * fy, w11 = fx * fy;
+            const double lx = w00 * f00.x + w10 * f10.x + w01 * f01.x + w11 * f11.x;
+            const double ly = w00 * f00.y + w10 * f10.y + w01 * f01.y + w11 * f11.y;
+            f = make_float2(static_cast<float>(2.0 * lx), static_cast<float>(2.0 * ly));
+            ok = __ldg(D.okin + (size_t)yn * a.cw + xn);
+        }
+        const size_t o = (size_t)y * a.w + x;
+        D.fout[o] = f;
+        D.okout[o] = ok;
+    }
+}
+
+// (v + a * b) for operands widened from float: the product is exact in double
+// (24 + 24 bits), so the fused form rounds once, like the separate multiply
+// and add it replaces (bit-identical, one instruction fewer).
+__device__ __forceinline__ double lk_fma(double a, double b, double v) {
+#ifdef FS_LK_NO_FMA
+    return v + a * b;
+#else
+    return __fma_rn(a, b, v);
+#endif
 }
 
 // ---- producer: sweep rows, stage vertical window sums ----------------------
@@ -279,20 +321,20 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 const double ogx = rs[0], ogy = rs[1];
                 rs[0] = (float)ix;
                 rs[1] = (float)iy;
-                V[0] = (V[0] + ix * ix) - ogx * ogx;
-                V[1] = (V[1] + ix * iy) - ogx * ogy;
-                V[2] = (V[2] + iy * iy) - ogy * ogy;
+                V[0] = lk_fma(-ogx, ogx, lk_fma(ix, ix, V[0]));
+                V[1] = lk_fma(-ogx, ogy, lk_fma(ix, iy, V[1]));
+                V[2] = lk_fma(-ogy, ogy, lk_fma(iy, iy, V[2]));
             } else if (FULL) {
                 float* rs = ringf + (slot * LK_IW + c) * 3;
                 const double ogx = rs[0], ogy = rs[1], odt = rs[2];
                 rs[0] = (float)ix;
                 rs[1] = (float)iy;
                 rs[2] = (float)tt;
-                V[0] = (V[0] + ix * ix) - ogx * ogx;
-                V[1] = (V[1] + ix * iy) - ogx * ogy;
-                V[2] = (V[2] + iy * iy) - ogy * ogy;
-                V[3] = (V[3] + ix * tt) - ogx * odt;
-                V[4] = (V[4] + iy * tt) - ogy * odt;
+                V[0] = lk_fma(-ogx, ogx, lk_fma(ix, ix, V[0]));
+                V[1] = lk_fma(-ogx, ogy, lk_fma(ix, iy, V[1]));
+                V[2] = lk_fma(-ogy, ogy, lk_fma(iy, iy, V[2]));
+                V[3] = lk_fma(-ogx, odt, lk_fma(ix, tt, V[3]));
+                V[4] = lk_fma(-ogy, odt, lk_fma(iy, tt, V[4]));
             } else {
                 double2* rp = ringd + (slot * LK_IW + c);
                 const double2 o = *rp;
@@ -466,7 +508,7 @@ int lk_tile_rows(int w, int h, int r, int ndir, int per_sm) {
 }
 
 cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
-    dim3 g((a.w + 31) / 32, (a.h + 7) / 8, a.ndir);
+    dim3 g((a.w + 31) / 32, (a.h + 8 * LK_PREP_ROWS - 1) / (8 * LK_PREP_ROWS), a.ndir);
     if (a.mode == 2)
         k_lk_prep<2><<<g, 256, 0, s>>>(a);
     else
