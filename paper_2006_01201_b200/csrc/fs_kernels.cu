@@ -444,6 +444,9 @@ __global__ void k_finalize_flow(SmoothArgs a) {
 // flagged and recomputed on the full domain by the host.
 // ============================================================================
 constexpr int EDT_SEG = 64;
+#ifndef EDT_BITS_RUN
+#define EDT_BITS_RUN 4
+#endif
 
 template <class M>
 __device__ __forceinline__ void edt_line_xy(const EdtJob<M>& J, int line, int p, int& x, int& y) {
@@ -466,29 +469,38 @@ __global__ void k_edt_bits(EdtJob<M> J0, EdtJob<M> J1) {
     const int nlines = J.vfirst ? J.W.w : J.W.h;
     const int len = J.vfirst ? J.W.h : J.W.w;
     const int nseg = (len + EDT_SEG - 1) / EDT_SEG;
-    const int seg = blockIdx.y;
-    if (seg >= nseg) return;
-    const int p0 = seg * EDT_SEG;
+    // rows-first: EDT_BITS_RUN consecutive segments of a row per warp (the job
+    // selection and index set-up paid once per run); columns-first: one
+    const int run = J.vfirst ? 1 : EDT_BITS_RUN;
+    const int seg0 = blockIdx.y * run;
+    const int seg1 = min(seg0 + run, nseg);
     if (J.vfirst) {
         const int line = blockIdx.x * blockDim.x + threadIdx.x;
         if (line >= nlines) return;
-        const int n = min(EDT_SEG, len - p0);
-        unsigned long long bits = 0;
+        for (int seg = seg0; seg < seg1; ++seg) {
+            const int p0 = seg * EDT_SEG;
+            const int n = min(EDT_SEG, len - p0);
+            unsigned long long bits = 0;
 #pragma unroll 16
-        for (int k = 0; k < EDT_SEG; ++k) {
-            if (k < n && J.mask(J.W.x0 + line, J.W.y0 + p0 + k)) bits |= 1ull << k;
+            for (int k = 0; k < EDT_SEG; ++k) {
+                if (k < n && J.mask(J.W.x0 + line, J.W.y0 + p0 + k)) bits |= 1ull << k;
+            }
+            J.bits[(size_t)seg * nlines + line] = bits;
         }
-        J.bits[(size_t)seg * nlines + line] = bits;
     } else {
         const int lane = threadIdx.x & 31;
         const int line = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         if (line >= nlines) return;
-        const int pa = p0 + lane, pb = p0 + 32 + lane;
-        bool a = pa < len && J.mask(J.W.x0 + pa, J.W.y0 + line);
-        bool b = pb < len && J.mask(J.W.x0 + pb, J.W.y0 + line);
-        unsigned lo = __ballot_sync(0xffffffffu, a), hi = __ballot_sync(0xffffffffu, b);
-        if (lane == 0)
-            J.bits[(size_t)seg * nlines + line] = (unsigned long long)lo | ((unsigned long long)hi << 32);
+        const int y = J.W.y0 + line;
+        for (int seg = seg0; seg < seg1; ++seg) {
+            const int pa = seg * EDT_SEG + lane, pb = pa + 32;
+            const bool a = pa < len && J.mask(J.W.x0 + pa, y);
+            const bool b = pb < len && J.mask(J.W.x0 + pb, y);
+            const unsigned lo = __ballot_sync(0xffffffffu, a), hi = __ballot_sync(0xffffffffu, b);
+            if (lane == 0)
+                J.bits[(size_t)seg * nlines + line] =
+                    (unsigned long long)lo | ((unsigned long long)hi << 32);
+        }
     }
 }
 
@@ -1039,7 +1051,7 @@ void edt(const EdtJob<M>& j0, const EdtJob<M>& j1, const FoldStats* st, cudaStre
     if (vf)
         k_edt_bits<M><<<dim3((max_lines + 127) / 128, max_seg, 2), 128, 0, s>>>(j0, j1);
     else
-        k_edt_bits<M><<<dim3((max_lines + 7) / 8, max_seg, 2), 256, 0, s>>>(j0, j1);
+        k_edt_bits<M><<<dim3((max_lines + 7) / 8, (max_seg + EDT_BITS_RUN - 1) / EDT_BITS_RUN, 2), 256, 0, s>>>(j0, j1);
     k_edt_line<M><<<dim3((max_lines + 127) / 128, max_oseg, 2), 128, 0, s>>>(j0, j1);
     k_edt_envelope<M><<<dim3((max_out + 7) / 8, 1, 2), 256, 0, s>>>(j0, j1, st);
 }
