@@ -523,7 +523,7 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
     if (p0 >= p1) return;
     const unsigned long long* B = J.bits + line;
     const unsigned long long mine = B[(size_t)seg * nlines];
-    long long prev = -(1LL << 40), next = 1LL << 40;  // nearest seed before / after the segment
+    int prev = -(1 << 30), next = 1 << 30;  // nearest seed before / after the segment
     // nearest seeds outside the segment: four segments' masks per round trip
     for (int s = seg - 1; s >= 0; s -= 4) {
         unsigned long long m[4];
@@ -534,7 +534,7 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
         for (int j = 3; j >= 0; --j)
             if (m[j]) hit = j;
         if (hit >= 0) {
-            prev = (long long)(s - hit) * EDT_SEG + 63 - __clzll((long long)m[hit]);
+            prev = (s - hit) * EDT_SEG + 63 - __clzll((long long)m[hit]);
             break;
         }
     }
@@ -547,19 +547,27 @@ __global__ void k_edt_line(EdtJob<M> J0, EdtJob<M> J1) {
         for (int j = 3; j >= 0; --j)
             if (m[j]) hit = j;
         if (hit >= 0) {
-            next = (long long)(s + hit) * EDT_SEG + __ffsll((long long)m[hit]) - 1;
+            next = (s + hit) * EDT_SEG + __ffsll((long long)m[hit]) - 1;
             break;
         }
     }
     const int gstride = J.vfirst ? J.W.w : J.W.h;  // pass-2 line length
-    for (int p = p0; p < p1; ++p) {
-        const int k = p - s0;
-        const unsigned long long upto = k == 63 ? ~0ull : ((2ull << k) - 1);
-        const unsigned long long lowm = mine & upto, highm = mine & ~((1ull << k) - 1);
-        const long long last = lowm ? (long long)s0 + 63 - __clzll((long long)lowm) : prev;
-        const long long nxt = highm ? (long long)s0 + __ffsll((long long)highm) - 1 : next;
-        const long long d = min((long long)p - last, nxt - (long long)p);
-        J.g[(size_t)(p - oa) * gstride + line] = d < 46341 ? (int)(d * d) : kInfSq;
+    // walk the outputs with the nearest seeds at or before (last) and at or
+    // after (nxt) p, advancing nxt past each seed it reaches
+    const int k0 = p0 - s0;
+    const unsigned long long below = k0 ? mine & ((1ull << k0) - 1) : 0ull;
+    int last = below ? s0 + 63 - __clzll((long long)below) : prev;
+    const unsigned long long from0 = mine & ~((1ull << k0) - 1);
+    int nxt = from0 ? s0 + __ffsll((long long)from0) - 1 : next;
+    int* gp = J.g + (size_t)(p0 - oa) * gstride + line;
+    for (int p = p0; p < p1; ++p, gp += gstride) {
+        if (p > nxt) {
+            const unsigned long long hm = mine & ~((1ull << (p - s0)) - 1);
+            nxt = hm ? s0 + __ffsll((long long)hm) - 1 : next;
+        }
+        if (nxt == p) last = p;
+        const int d = min(p - last, nxt - p);
+        *gp = d < 46341 ? d * d : kInfSq;
     }
 }
 
