@@ -672,13 +672,13 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st) 
             y = J.W.y0 + q;
         }
         J.out[(size_t)(y - J.C.y0) * J.C.w + (x - J.C.x0)] = dsq;
-        if (J.check && have) {
-            long long bnd = LLONG_MAX;
-            if (!J.e_left) bnd = min(bnd, (long long)(x - J.W.x0 + 1));
-            if (!J.e_right) bnd = min(bnd, (long long)(J.W.x1() - x));
-            if (!J.e_top) bnd = min(bnd, (long long)(y - J.W.y0 + 1));
-            if (!J.e_bottom) bnd = min(bnd, (long long)(J.W.y1() - y));
-            if (bnd != LLONG_MAX && (long long)dsq > bnd * bnd) fail = true;
+        if (J.check && have) {  // distances to W's open edges are < 46341: squares fit in int
+            int bnd = INT_MAX;
+            if (!J.e_left) bnd = min(bnd, x - J.W.x0 + 1);
+            if (!J.e_right) bnd = min(bnd, J.W.x1() - x);
+            if (!J.e_top) bnd = min(bnd, y - J.W.y0 + 1);
+            if (!J.e_bottom) bnd = min(bnd, J.W.y1() - y);
+            if (bnd < 46341 && dsq > bnd * bnd) fail = true;  // (no open edge: INT_MAX)
         }
     }
     if (__any_sync(0xffffffffu, fail) && lane == 0)
