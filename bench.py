@@ -47,13 +47,19 @@ def parse_args():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=["c2", "c1", "c3", "c4"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--shard", choices=["none", "seams"], default="none",
+    ap.add_argument("--shard", choices=["auto", "none", "seams"], default="auto",
                     help="seams: ONE panorama whose overlap pairs are sharded over the GPUs "
                          "(strong scaling, strips gathered to rank 0 over NCCL P2P); "
-                         "none: one independent panorama per GPU (weak scaling)")
+                         "none: one independent panorama per GPU (weak scaling); "
+                         "auto: seams when N > 1 (with the independent-panorama throughput "
+                         "as the secondary `dp` key)")
     ap.add_argument("--kernel-only", action="store_true",
                     help="only warmup + timed steps (for ncu launch lists)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: start the ranks over gloo, run the shard schedule and the "
+                         "strip-exchange protocol with host stand-ins, print one JSON line")
     return ap.parse_args()
 
 
@@ -64,8 +70,35 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_spawn(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) without a launcher: start the N
+    ranks ourselves (torchrun on 127.0.0.1, one process per GPU) and wait.
+    Returns True when this process was only the launcher."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NVLS / P2P transport lines in the log
+    rc = subprocess.call(cmd, env=env)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
 def make_layout(name: str, seed: int):
-    from paper_2006_01201_b200 import synthetic as S
+    import fs_synthetic as S  # numpy only: no torch, no product library
     return {"c1": S.c1_pair, "c2": S.c2_panorama, "c3": S.c3_large_parallax,
             "c4": S.c4_ring}[name](seed=seed)
 
@@ -75,12 +108,48 @@ def workload_name(lay, name):
             "c4": "C4 (configs[3]) "}[name] + lay.name
 
 
+def shard_mode(args, ws) -> str:
+    if args.shard == "auto":
+        return "seams" if ws > 1 else "none"
+    return args.shard
+
+
+def config_dict(args, lay, ws) -> dict:
+    """The workload; identical in the B200 and the reference arm's lines."""
+    mode = shard_mode(args, ws)
+    if ws == 1:
+        par = "dp1 (one panorama on one GPU)"
+    elif mode == "seams":
+        par = ("seam-sharded over %d GPUs: overlap pairs (folds) scheduled over the ranks, "
+               "Area3 strips gathered to rank 0 over NCCL P2P" % ws)
+    else:
+        par = "dp%d (one independent panorama per GPU)" % ws
+    return {"workload": workload_name(lay, args.config),
+            "canvas": [lay.canvas_w, lay.canvas_h],
+            "views": [list(d) for d in lay.dims], "folds": len(lay.views) - 1,
+            "flow_params": [lay.levels, 8, 3, 1e-4, 2], "blend_params": [10.0, 0.05],
+            "parallelism": par,
+            "l2": "inputs larger than L2 (views + canvas > 126 MB) and L2 flushed (256 MB "
+                  "write) between timed GPU steps"}
+
+
 def measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -136,81 +205,147 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference_run(lay, threads: int):
-    """One fold of `lay` through the compiled reference (oracle/_ref), metrics
-    excluded (pipeline.cpp:150-204 minus :184-187, :194-199). Returns (s, stage s)."""
-    import numpy as np
+def _ref_fold(ref, lay, flows=False):
+    """One whole stitch_placed of `lay` through the compiled reference
+    (oracle/_ref): the fold of proj/src/pipeline.cpp:150-204 minus the seam
+    metrics (:184-187, :194-199, which never write the panorama).  Returns
+    (pano, valid, per-fold flows or [], seconds of the fold on the host)."""
+    fv = lay.float_views()
+    return ref.stitch_placed_flows([d for d, _ in fv], [v for _, v in fv], lay.offsets,
+                                   lay.canvas_w, lay.canvas_h, (lay.levels, 8, 3, 1e-4, 2),
+                                   flows=flows)
+
+
+def cpu_baseline_leg(lay, config_name):
+    """The reference on this host, rank 0 at N = 1: the same whole-panorama
+    span as the GPU step, all host threads, best of 3; a
+    1-thread sample (fold 1 alone, FLOWSTITCH_THREADS=1 semantics,
+    src/parallel.cpp:14-20); returns (cpu_baseline dict, (pano, valid, folds))."""
     from oracle import reference
     ref = reference()
+    threads = os.cpu_count() or 1
     ref.set_threads(threads)
-    fv = lay.float_views()
-    timing = np.zeros(5, np.float64)
-    t0 = time.perf_counter()
-    ref.stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets, lay.canvas_w,
-                      lay.canvas_h, (lay.levels, 8, 3, 1e-4, 2), timing=timing)
-    return time.perf_counter() - t0, timing, ref.threads()
+    runs = []
+    keep = None
+    for i in range(3):
+        pano, valid, folds, secs = _ref_fold(ref, lay, flows=(i == 0))
+        runs.append(secs)
+        if i == 0:
+            keep = (pano, valid, folds)
+    used = ref.threads()
+    best = min(runs)
+    # 1-thread sample: fold 1 (views 0 and 1 alone) at 1 and at all threads
+    import fs_synthetic as S
+    pair = S.Layout(lay.name + " fold 1", lay.canvas_w, lay.canvas_h, lay.views[:2],
+                    lay.offsets[:2], lay.levels)
+    _, _, _, f1_all = _ref_fold(ref, pair)
+    ref.set_threads(1)
+    _, _, _, f1_one = _ref_fold(ref, pair)
+    ref.set_threads(threads)
+    cpu = {"value": round(lay.canvas_mpx / best, 4), "unit": UNIT, "cores": used,
+           "kind": "reference",
+           "sample": "whole %s stitch_placed (%d folds) through oracle/_ref (the reference "
+                     "compiled from /root/reference with its Release flags), %d threads, best "
+                     "of 3: %s s" % (config_name.upper(), len(lay.views) - 1, used,
+                                     [round(x, 2) for x in runs]),
+           "s_per_panorama": round(best, 3), "cpu_model": cpu_model(),
+           "threads1": {"sample": "fold 1 alone (views 0+1 on the full canvas)",
+                        "s_1_thread": round(f1_one, 3), "s_all_threads": round(f1_all, 3),
+                        "speedup_all_threads": round(f1_one / f1_all, 2),
+                        "est_s_per_panorama_1_thread": round(best * f1_one / f1_all, 2)}}
+    return cpu, keep
 
 
 def run_reference_arm(args, ws, rank):
-    """The reference's CPU fold (oracle/_ref, all host threads).  A step is
-    one fold of a continuously running fold chain over the panorama's views
-    (fold k = the reference's stitch of [panorama after fold k-1, view k],
-    which is exactly fold k of stitch_placed); after the last fold the chain
-    restarts from view 0.  value = canvas Mpx x (folds timed / folds per
-    panorama) / time, i.e. panoramas per second in canvas Mpx."""
+    """`--impl reference`: the reference's CPU implementation of the path
+    (oracle/_ref, all host threads) on the same workload.  A step is one
+    whole stitch_placed of the panorama's placed views — the span of the
+    GPU arm's step and of its cpu_baseline.  Rank 0 alone runs it; nothing
+    here imports torch or the B200 library."""
     if rank != 0:
         return
-    import numpy as np
     from oracle import reference
     lay = make_layout(args.config, 0)
     threads = os.cpu_count() or 1
     ref = reference()
     ref.set_threads(threads)
-    fv = lay.float_views()
-    nfold = len(fv) - 1
-    params = (lay.levels, 8, 3, 1e-4, 2)
-    pano = None
     times = []
     for i in range(args.warmup + args.steps):
-        k = i % nfold + 1
-        if k == 1:
-            d0, v0 = fv[0]
-            pano = ref.place_on_canvas(d0, v0, lay.offsets[0][0], lay.offsets[0][1], lay.canvas_w,
-                                       lay.canvas_h)
-        t0 = time.perf_counter()
-        pano = ref.stitch_placed([pano[0], fv[k][0]], [pano[1], fv[k][1]],
-                                 [(0, 0), lay.offsets[k]], lay.canvas_w, lay.canvas_h, params)
-        dt = time.perf_counter() - t0
+        _, _, _, secs = _ref_fold(ref, lay)
         if i >= args.warmup:
-            times.append(dt)
+            times.append(secs)
     used = ref.threads()
-    total = sum(times)
-    s = total / len(times) * nfold  # seconds per panorama
-    value = lay.canvas_mpx * (len(times) / nfold) / total
+    s = statistics.mean(times)  # seconds per panorama
+    value = lay.canvas_mpx / s
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(total / len(times) * 1e3, 1), "higher_is_better": True,
-        "scaling": "weak",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
+        "scaling": "strong" if shard_mode(args, ws) == "seams" else "weak",
         "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": workload_name(lay, args.config), "canvas": [lay.canvas_w, lay.canvas_h],
-                   "flow_params": [lay.levels, 8, 3, 1e-4, 2], "blend_params": [10.0, 0.05],
-                   "parallelism": "host threads (reference parallel_rows)"},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": used, "kind": "reference",
-                         "sample": "one fold per step of a running %d-fold %s chain (%d folds "
-                                   "timed), the reference compiled from /root/reference with its "
-                                   "Release flags" % (nfold, args.config.upper(), len(times))},
+        "config": config_dict(args, lay, ws),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": used,
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "sample": "one whole %s stitch_placed per step (%d folds), %d steps, "
+                                   "the reference compiled from /root/reference with its "
+                                   "Release flags (oracle/_ref), %d threads"
+                                   % (args.config.upper(), len(lay.views) - 1, len(times),
+                                      used)},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0, "s_per_panorama": round(s, 3)},
     }
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args, ws, rank):
+    """`--dry-run` (CPU): the N-rank launch, the gloo process group, the shard
+    schedule of the config's folds and one strip exchange with host tensors
+    in the schedule's order (paper_2006_01201_b200.shard's protocol)."""
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("gloo")
+    from paper_2006_01201_b200 import shard as SH
+    lay_boxes = {"c2": [(0, 0, 0, 0), (2083, 600, 667, 2800), (4166, 600, 584, 2800),
+                        (6250, 600, 500, 2800), (0, 600, 9000, 400), (0, 3000, 9000, 400)],
+                 "c4": [(0, 0, 0, 0)] + [(2048 * k, 1024, 512, 6144) for k in range(1, 8)],
+                 "c1": [(0, 0, 0, 0), (512, 0, 512, 1024)],
+                 "c3": [(0, 0, 0, 0), (1024, 0, 1024, 1024)]}[args.config]
+    sc = SH.shard_schedule(lay_boxes, ws)
+    strips = {k: torch.full((16,), k if sc.fold_rank[k] == rank else -1, dtype=torch.int64)
+              for k in range(1, len(lay_boxes))}
+    got = []
+    if ws > 1:
+        tr = SH.TorchDistTransport()
+        for seg in range(sc.n_segments):
+            xs = sc.xfers_after(seg, rank)
+            tr.exchange(rank, xs, lambda k: strips[k])
+            got += [x.fold for x in xs if x.dst == rank]
+        ok = all(int(strips[k][0]) == k for k in got)
+        status = tr.max_status(0 if ok else 1)
+    else:
+        status = 0
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "backend": "gloo" if ws > 1 else None,
+                          "config": args.config, "fold_rank": sc.fold_rank, "stage": sc.stage,
+                          "segments": sc.n_segments, "xfers": len(sc.xfers),
+                          "received_rank0": sorted(got), "status": status}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    if status:
+        sys.exit(1)
+
+
 def main():
     args = parse_args()
+    if maybe_spawn(args):
+        return
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
+        return
+    if args.dry_run:
+        run_dry(args, ws, rank)
         return
     import numpy as np
     import torch
@@ -221,7 +356,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2006_01201_b200 as fs
 
-    sharded = args.shard == "seams"
+    sharded = shard_mode(args, ws) == "seams"
     lay = make_layout(args.config, 0 if sharded else rank)
     params = fs.FlowParams(levels=lay.levels)
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params, device=local)
@@ -253,29 +388,33 @@ def main():
                                             "RGB8 (covered by the views)" if rgb_out else "RGBA8")
     # first execution: uploads the views, validates the plan's EDT domains
     plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
-    shard_mode = None
+    smode = None
     if sp is not None:
         if ws > 1:
-            shard_mode = sp.run()  # certified sharded, or unsharded on rank 0 from now on
+            smode = sp.run()  # certified sharded, or unsharded on rank 0 from now on
         else:
             sp.execute(sptr)
             torch.cuda.synchronize()
-            shard_mode = "sharded" if sp.status() == 0 else "unsharded"
-            if shard_mode == "unsharded":
+            smode = "sharded" if sp.status() == 0 else "unsharded"
+            if smode == "unsharded":
                 sp.unsharded = True
 
-    def run_step(host=False):
-        if sp is not None and not sp.unsharded:
+    def run_step(host=False, dp=False):
+        if dp or sp is None:
+            if host:
+                plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
+            else:
+                plan.execute(sptr)
+        elif not sp.unsharded:
             if host:
                 sp.execute(sptr, view_ptrs, host_out.data_ptr())
             else:
                 sp.execute(sptr)
-        elif sp is not None and rank != 0:
-            return  # unsharded fallback: rank 0 folds the panorama alone
-        elif host:
-            plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
-        else:
-            plan.execute(sptr)
+        elif rank == 0:  # unsharded fallback: rank 0 folds the panorama alone
+            if host:
+                plan.execute_ptrs(view_ptrs, host_out.data_ptr(), sptr)
+            else:
+                plan.execute(sptr)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -283,36 +422,42 @@ def main():
         if ws > 1:
             dist.barrier()
 
+    def max_over_ranks(v):
+        if ws > 1:
+            t = torch.tensor([v], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return v
+
+    def timed(steps, host=False, dp=False, flush_l2=True):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for a, b in ev:
+            if flush_l2:
+                flush.zero_()
+            a.record(stream)
+            run_step(host=host, dp=dp)
+            b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        wall = time.perf_counter() - w0
+        return max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev)), wall
+
     for _ in range(args.warmup):
         run_step()
     torch.cuda.synchronize()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     clocks = ClockSampler(local)
     with clocks:
-        barrier()
-        torch.cuda.synchronize()
-        wall0 = time.perf_counter()
-        for a, b in ev:
-            flush.zero_()
-            a.record(stream)
-            run_step()
-            b.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        wall = time.perf_counter() - wall0
+        ms, wall = timed(args.steps)
     if sp is not None and not sp.unsharded:
         if sp.status() != 0:
             raise RuntimeError("sharded execution not certified: " + fs._native.last_error())
     elif rank == 0 or sp is None:
         plan.check()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    ms = statistics.mean(step_ms)
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     units = 1 if sharded else ws  # panoramas per step over the job
     value = units * lay.canvas_mpx / (ms / 1e3)
     launches = plan.launch_count
@@ -328,22 +473,23 @@ def main():
             dist.destroy_process_group()
         return
 
+    # ---- secondary at N > 1 with sharding: independent panoramas per GPU
+    dp = None
+    if sharded and ws > 1:
+        for _ in range(args.warmup):
+            run_step(dp=True)
+        dms, _ = timed(args.steps, dp=True)
+        dp = {"value": round(ws * lay.canvas_mpx / (dms / 1e3), 2), "unit": UNIT,
+              "ms_per_step": round(dms, 4), "scaling": "weak",
+              "what": "every GPU folds its own panorama (BASELINE configs[4]-style "
+                      "throughput), no data-path collective"}
+
     # ---- end to end through the public call (host views in, host canvas out)
     e2e = None
     if not args.no_e2e:
-        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        barrier()
-        for a, b in ee:
-            a.record(stream)
+        for _ in range(2):
             run_step(host=True)
-            b.record(stream)
-        torch.cuda.synchronize()
-        e_ms = statistics.mean(a.elapsed_time(b) for a, b in ee)
-        if ws > 1:
-            t = torch.tensor([e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+        e_ms, _ = timed(args.steps, host=True, flush_l2=False)
         e2e = {"value": round(units * lay.canvas_mpx / (e_ms / 1e3), 2), "unit": UNIT,
                "h2d_bytes_per_step": h2d_bytes * ws, "d2h_bytes_per_step": d2h_bytes * units,
                "s_per_panorama": round(e_ms / 1e3, 5), "ms_per_step": round(e_ms, 4)}
@@ -365,43 +511,62 @@ def main():
     breakdown = {k: {"launches_per_step": v["launches"] // nrep,
                      "ms_per_step": round(v["ms"] / nrep, 4),
                      "share": round(v["ms"] / kern_ms_total, 4),
-                     "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+                     "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None,
+                     "frac": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9 / peak, 4)
+                     if v["ms"] else None}
                  for k, v in sorted(fam.items(), key=lambda kv: -kv[1]["ms"])}
     dom = max(fam, key=lambda k: fam[k]["ms"])
     lk = fam.get("lk_iter", fam[dom])
-    ach = lk["bytes"] / lk["launches"] / (lk["ms"] / lk["launches"] * 1e-3) / 1e9
+    per_launch = lk["bytes"] / lk["launches"]
+    ach = per_launch / (lk["ms"] / lk["launches"] * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             traffic = json.load(f).get("lk_iter_dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"kernel": "k_lk_sweep<false> (LK later iteration, level 0, both directions)",
+    roofline = {"kernel": "k_lk_sweep (LK later iteration, level 0, both directions)",
                 "bound": "hbm",
                 "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": round(lk["bytes"] / lk["launches"]),
+                "bytes_basis": "SURVEY.md §8(d) K3: 26 B per px, direction and iteration",
+                "algorithmic_bytes_per_launch": round(per_launch),
                 "avg_launch_us": round(lk["ms"] / lk["launches"] * 1e3, 2),
                 "peak_source": peak_src, "share_of_step": round(lk["ms"] / kern_ms_total, 4),
                 "dominant_kernel": dom, "kernels": breakdown,
+                "step_bytes_frac": round(sum(v["bytes"] for v in fam.values()) / nrep
+                                         / (statistics.mean(tot_ms) * 1e-3) / 1e9 / peak, 4),
                 "profiled_step_ms": round(statistics.mean(tot_ms), 4)}
 
-    # ---- CPU baseline: the compiled reference on this host (rank 0, N = 1)
+    # ---- CPU baseline (the compiled reference on this host, rank 0, N = 1)
+    # and parity of this run's output against it
     cpu = None
+    parity = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            cs, stages, used = cpu_reference_run(lay, threads)
-            cpu = {"value": round(lay.canvas_mpx / cs, 4), "unit": UNIT, "cores": used,
-                   "kind": "reference",
-                   "sample": "one full %s fold (%d folds, %.1f s), reference from "
-                             "/root/reference built by oracle/Makefile, %d threads; stages "
-                             "prep/flow/embed/blend_field/blend = %s s"
-                             % (args.config.upper(), len(lay.views) - 1, cs, used,
-                                [round(x, 2) for x in stages])}
+            cpu, (rp, rv, rfolds) = cpu_baseline_leg(lay, args.config)
         except Exception as e:  # checker missing: say so, never substitute
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": "unavailable: %s" % e}
+            rp = None
+        if rp is not None and not args.no_parity:
+            from oracle import parity as P
+            if not args.no_e2e:
+                gpu_canvas = host_out.numpy()
+            else:
+                gpu_canvas = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
+                plan.set_host_format(4, 4)
+                plan.execute_host(lay.views, gpu_canvas)
+            canvas = P.compare_canvas(gpu_canvas, rp, rv)
+            flow = P.fold_flow_stats(plan, rfolds)
+            parity = {"vs": "oracle/_ref (the reference compiled from /root/reference), same "
+                            "inputs, this run's output",
+                      "max_lsb": canvas["max_lsb"], "frac_le_1lsb": canvas["frac_le_1lsb"],
+                      "frac_exact": canvas["frac_exact"], "valid_equal": canvas["valid_equal"],
+                      "flow_mean_epe": flow["mean_epe"], "flow_max_epe": flow["max_epe"],
+                      "flow_frac_gt_0p5": flow["frac_gt_0p5"],
+                      "flow_valid_mismatch": flow["valid_mismatch"], "flow_px": flow["n"],
+                      "gates": P.gates(canvas, flow)}
 
     if rank == 0:
         line = {
@@ -410,25 +575,17 @@ def main():
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None,
             "dtype": "f32/f64", "data": "synthetic",
-            "config": {"workload": workload_name(lay, args.config),
-                       "canvas": [lay.canvas_w, lay.canvas_h],
-                       "views": [list(d) for d in lay.dims], "folds": len(lay.views) - 1,
-                       "flow_params": list(params.astuple()), "blend_params": [10.0, 0.05],
-                       "host_formats": host_formats,
-                       "parallelism": ("seam-sharded over %d GPU(s): folds on ranks %s, "
-                                       "stages %s, %d strip transfers (NCCL P2P), %s"
-                                       % (ws, sp.schedule.fold_rank, sp.schedule.stage,
-                                          len(sp.schedule.xfers), shard_mode)
-                                       if sharded else
-                                       "dp%d (one independent panorama per GPU)" % ws),
-                       "l2": "inputs larger than L2 (views %d MB + canvas %d MB) and L2 "
-                             "flushed (256 MB write) between timed steps"
-                             % (h2d_bytes >> 20, (lay.canvas_w * lay.canvas_h * 21) >> 20),
-                       "timing": "CUDA events per step on the launching stream, mean of %d, "
-                                 "max over ranks" % args.steps,
-                       "wall_s_timed_region": round(wall, 4)},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "clocks": clocks.summary(), "gpu_launches": launches * args.steps,
+            "config": config_dict(args, lay, ws),
+            "details": {"host_formats": host_formats,
+                        "timing": "CUDA events per step on the launching stream, mean of %d, "
+                                  "max over ranks" % args.steps,
+                        "wall_s_timed_region": round(wall, 4),
+                        "shard": ({"fold_rank": sp.schedule.fold_rank,
+                                   "stage": sp.schedule.stage,
+                                   "strip_transfers": len(sp.schedule.xfers), "mode": smode}
+                                  if sp is not None else None)},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
+            "dp": dp, "clocks": clocks.summary(), "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)
     plan.close()

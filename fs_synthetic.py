@@ -1,5 +1,9 @@
 """Synthetic, seeded stitching workloads (BASELINE.json configs).
 
+Input generation only: numpy, no torch, no GPU and no import of the product
+package, so the reference arm of bench.py and the CPU oracle legs build their
+inputs without touching the B200 library.  Every arm reads the same bytes.
+
 Texture is multi-octave value noise (octave o = 1..7: cell 2^o px, amplitude
 2^(o/2), smoothstep-bilinear lattice drawn from MT19937(seed) in U(-1,1)),
 normalised to [0.1, 0.9] and quantised to 8 bits; RGB channels use seeds s,
@@ -19,16 +23,7 @@ INV255 = np.float32(1.0) / np.float32(255.0)  # 1.0f/255.0f as the reference com
 
 
 def value_noise(h: int, w: int, seed: int, octaves=range(1, 8)) -> np.ndarray:
-    """Multi-octave smoothstep value noise in [0.1, 0.9], float32 (h, w).
-    Large rasters are interpolated with torch on the GPU when one is present
-    (same lattice, same formula; input generation only, outside any timed
-    region; bitwise results may differ from numpy by float rounding, which
-    only matters within one run, where every arm reads the same bytes)."""
-    if h * w >= (1 << 22):
-        try:
-            return _value_noise_torch(h, w, seed, octaves)
-        except ImportError:
-            pass
+    """Multi-octave smoothstep value noise in [0.1, 0.9], float32 (h, w)."""
     rng = np.random.RandomState(seed)
     acc = np.zeros((h, w), np.float32)
     for o in octaves:
@@ -41,36 +36,27 @@ def value_noise(h: int, w: int, seed: int, octaves=range(1, 8)) -> np.ndarray:
         # x: each lattice column pair feeds `cell` consecutive pixels
         t = (lat[:, :-1, None] * (1 - s) + lat[:, 1:, None] * s).reshape(ny + 1, nx * cell)
         t = t[:, :w]
-        # y: same per lattice row pair
-        v = (t[:-1, None, :] * (1 - s)[None, :, None] + t[1:, None, :] * s[None, :, None])
-        acc += amp * v.reshape(ny * cell, w)[:h]
+        # y: same per lattice row pair, in row blocks (bounded temporaries)
+        for r0 in range(0, ny, 64):
+            r1 = min(ny, r0 + 64)
+            v = (t[r0:r1, None, :] * (1 - s)[None, :, None]
+                 + t[r0 + 1:r1 + 1, None, :] * s[None, :, None]).reshape((r1 - r0) * cell, w)
+            y0 = r0 * cell
+            y1 = min(h, r1 * cell)
+            if y1 > y0:
+                acc[y0:y1] += amp * v[:y1 - y0]
     lo, hi = float(acc.min()), float(acc.max())
     return (0.1 + 0.8 * (acc - lo) / max(hi - lo, 1e-6)).astype(np.float32)
 
 
-def _value_noise_torch(h, w, seed, octaves):
-    import torch
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    rng = np.random.RandomState(seed)
-    acc = torch.zeros((h, w), dtype=torch.float32, device=dev)
-    for o in octaves:
-        cell = 2 ** o
-        amp = float(2.0 ** (o / 2.0))
-        ny, nx = h // cell + 1, w // cell + 1
-        lat = torch.from_numpy(
-            rng.uniform(-1.0, 1.0, size=(ny + 1, nx + 1)).astype(np.float32)).to(dev)
-        f = torch.arange(cell, dtype=torch.float32, device=dev) / cell
-        s = f * f * (3 - 2 * f)
-        t = (lat[:, :-1, None] * (1 - s) + lat[:, 1:, None] * s).reshape(ny + 1, nx * cell)[:, :w]
-        v = t[:-1, None, :] * (1 - s)[None, :, None] + t[1:, None, :] * s[None, :, None]
-        acc.add_(v.reshape(ny * cell, w)[:h], alpha=amp)
-    lo, hi = float(acc.min()), float(acc.max())
-    return (0.1 + 0.8 * (acc - lo) / max(hi - lo, 1e-6)).cpu().numpy().astype(np.float32)
-
-
 def rgb_scene(h: int, w: int, seed: int) -> np.ndarray:
     """(h, w, 3) uint8 scene."""
-    chans = [value_noise(h, w, seed + d) for d in (0, 101, 202)]
+    if h * w >= (1 << 20):  # numpy releases the GIL: one thread per channel
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(3) as ex:
+            chans = list(ex.map(lambda d: value_noise(h, w, seed + d), (0, 101, 202)))
+    else:
+        chans = [value_noise(h, w, seed + d) for d in (0, 101, 202)]
     return np.clip(np.rint(np.stack(chans, axis=-1) * 255.0), 0, 255).astype(np.uint8)
 
 

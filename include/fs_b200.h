@@ -254,6 +254,12 @@ fs_status fs_plan_set_host_format(fs_plan plan, int view_channels, int out_chann
 fs_status fs_plan_transfer_bytes(fs_plan plan, size_t* h2d, size_t* d2h);
 /* fold geometry: for fold k (1..n-1) the Area3 box {x0,y0,w,h} and depth */
 fs_status fs_plan_fold_info(fs_plan plan, int k, int* box, int* depth);
+/* fold k's crop flows of the last execution (the FlowFields bidirectional_flow
+ * returns inside stitch_placed, src/pipeline.cpp:171-172): interleaved (dx,dy)
+ * float + u8 valid, box w x h each; host or device destinations, any of the
+ * four may be NULL.  Synchronises the plan's device. */
+fs_status fs_plan_fold_flow(fs_plan plan, int k, float* ltor_vec, uint8_t* ltor_valid,
+                            float* rtol_vec, uint8_t* rtol_valid);
 /* one un-captured execution with CUDA events around every kernel launch on
  * `stream`; per kernel family: launches, summed device ms and algorithmic
  * bytes.  total_ms spans the whole execution. */

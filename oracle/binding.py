@@ -72,6 +72,8 @@ class Oracle:
             self.lib.fsref_resolved_threads.restype = I
             self.lib.fsref_stitch_placed_timed.restype = I
             self.lib.fsref_stitch_placed_timed.argtypes = _SIGS["stitch_placed"][1] + [P]
+            self.lib.fsref_stitch_placed_flows.restype = I
+            self.lib.fsref_stitch_placed_flows.argtypes = _SIGS["stitch_placed"][1] + [P, P, P]
             self.lib.fsref_stitch_placed_full.restype = I
             self.lib.fsref_stitch_placed_full.argtypes = _SIGS["stitch_placed"][1]
 
@@ -280,6 +282,32 @@ class Oracle:
             st = self._fn("stitch_placed")(*args)
         self._ok(st, "stitch_placed")
         return out, ov
+
+    def stitch_placed_flows(self, images, valids, offsets, cw, chh, params=None, k=10.0,
+                            coef=0.05, flows=True):
+        """The compiled reference's fold with every fold's crop flows.
+        Returns (pano, valid, folds, seconds): folds[k-1] = dict(box=(x, y, w, h),
+        lr=(vec, valid), rl=(vec, valid)); seconds = the whole fold's time on
+        the host, flow export excluded."""
+        if self.prefix != "fsref_":
+            raise NotImplementedError("per-fold flows come from the compiled reference")
+        args, out, ov, keep = self._stitch_args(images, valids, offsets, cw, chh, params, k, coef)
+        folds = []
+        CB = C.CFUNCTYPE(None, I, I, I, I, I, P, P, P, P, P)
+
+        def cb(kk, ox, oy, w, h, lr, lrv, rl, rlv, ctx):
+            def arr(ptr, shape, dt):
+                n = int(np.prod(shape)) * np.dtype(dt).itemsize
+                return np.frombuffer(C.string_at(ptr, n), dt).reshape(shape).copy()
+            folds.append({"k": kk, "box": (ox, oy, w, h),
+                          "lr": (arr(lr, (h, w, 2), np.float32), arr(lrv, (h, w), np.uint8)),
+                          "rl": (arr(rl, (h, w, 2), np.float32), arr(rlv, (h, w), np.uint8))})
+        cbf = CB(cb)
+        timing = np.zeros(6, np.float64)
+        st = self.lib.fsref_stitch_placed_flows(*args, _p(timing),
+                                                C.cast(cbf, C.c_void_p) if flows else None, None)
+        self._ok(st, "stitch_placed_flows")
+        return out, ov, folds, float(timing[5])
 
     def last_report_misalignment(self, max_pairs: int = 64) -> np.ndarray:
         """(before, after) per pair of the last stitch_placed(full=True)

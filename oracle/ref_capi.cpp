@@ -280,11 +280,20 @@ std::vector<PlacedImage> make_placed(int n, const float* const* imgs, const uint
 // in the same order, minus misalignment_score / warp_constituents (:184-187,
 // :194-199: metrics that never write the panorama).  `timing` (optional,
 // 5 doubles): prep (place/partition/crop), flow, embed, blend field, blend.
-int fsref_stitch_placed_timed(int n, const float* const* imgs, const uint8_t* const* valids,
+// `fold_cb` (optional) receives every fold's crop flows (the reference's own
+// bidirectional_flow output, proj/src/pipeline.cpp:171-172) and crop box;
+// the time it takes is excluded from `timing`.  timing[5] (when timing is
+// given) = seconds of the whole fold, the callbacks excluded.
+typedef void (*fsref_fold_cb)(int k, int ox, int oy, int w, int h, const float* lr,
+                              const uint8_t* lr_valid, const float* rl, const uint8_t* rl_valid,
+                              void* ctx);
+int fsref_stitch_placed_flows(int n, const float* const* imgs, const uint8_t* const* valids,
                               const int* dims, const int* offsets, int ch, int cw, int chh,
                               int levels, int radius, int iters, double eps, int smoothing,
                               double k, double coef, float* out, uint8_t* out_valid,
-                              double* timing) {
+                              double* timing, fsref_fold_cb fold_cb, void* ctx) {
+    auto t_start = Clock::now();
+    double cb_s = 0.0;
     std::vector<PlacedImage> placed = make_placed(n, imgs, valids, dims, offsets, ch);
     double t[5] = {0, 0, 0, 0, 0};
     int st = guarded([&] {
@@ -313,6 +322,14 @@ int fsref_stitch_placed_timed(int n, const float* const* imgs, const uint8_t* co
             auto b = Clock::now();
             auto [lr_c, rl_c] = bidirectional_flow(crop_l.image, crop_r.image, fp);
             auto c = Clock::now();
+            if (fold_cb) {
+                fold_cb(static_cast<int>(kk), crop_l.offset_x, crop_l.offset_y, lr_c.width,
+                        lr_c.height, lr_c.vec.data(), lr_c.valid.data(), rl_c.vec.data(),
+                        rl_c.valid.data(), ctx);
+                auto c2 = Clock::now();
+                cb_s += secs(c, c2);
+                c = c2;
+            }
             FlowField lr = embed_flow(lr_c, crop_l.offset_x, crop_l.offset_y, cw, chh);
             FlowField rl = embed_flow(rl_c, crop_l.offset_x, crop_l.offset_y, cw, chh);
             auto d = Clock::now();
@@ -331,8 +348,24 @@ int fsref_stitch_placed_timed(int n, const float* const* imgs, const uint8_t* co
         }
         export_image(pano, out, out_valid);
     });
-    if (timing)
+    if (timing) {
         for (int q = 0; q < 5; ++q) timing[q] = t[q];
+        timing[5] = secs(t_start, Clock::now()) - cb_s;
+    }
+    return st;
+}
+
+int fsref_stitch_placed_timed(int n, const float* const* imgs, const uint8_t* const* valids,
+                              const int* dims, const int* offsets, int ch, int cw, int chh,
+                              int levels, int radius, int iters, double eps, int smoothing,
+                              double k, double coef, float* out, uint8_t* out_valid,
+                              double* timing) {
+    double t6[6];
+    int st = fsref_stitch_placed_flows(n, imgs, valids, dims, offsets, ch, cw, chh, levels, radius,
+                                       iters, eps, smoothing, k, coef, out, out_valid, t6, nullptr,
+                                       nullptr);
+    if (timing)
+        for (int q = 0; q < 5; ++q) timing[q] = t6[q];
     return st;
 }
 

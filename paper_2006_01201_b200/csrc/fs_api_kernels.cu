@@ -2,6 +2,7 @@
 // API: interleaved float images, canvas-sized flows and fields).  The fold
 // engine uses the fused kernels in fs_kernels.cu; these serve the drop-in
 // entry points one call at a time.
+#include <algorithm>
 #include <climits>
 
 #include "fs_api_kernels.cuh"
@@ -65,47 +66,53 @@ __global__ void k_bilinear_batch(ImgSampler s, int h, const double* __restrict__
     for (int c = 0; c < s.ch; ++c) out[(size_t)k * s.ch + c] = o[c];
 }
 
+// Rows are grid-strided: gridDim.y is capped at 65535 (rows() below), any
+// image height works.
+#define FS_FOR_ROWS(j, h) for (int j = blockIdx.y; j < (h); j += gridDim.y)
+
 // src/image.cpp:115-132 (counts) and :140-148 (Area3 box)
 __global__ void k_partition_planes(const uint8_t* __restrict__ ml, const uint8_t* __restrict__ mr,
                                    int w, int h, uint8_t* __restrict__ label,
                                    unsigned long long* counts, int* box) {
     int x = blockIdx.x * blockDim.x + threadIdx.x;
-    int y = blockIdx.y;
-    uint8_t reg = 0;
-    bool in = x < w;
-    if (in) {
-        size_t p = (size_t)y * w + x;
-        bool l = ml[p] != 0, r = mr[p] != 0;
-        reg = l ? (r ? 3 : 1) : (r ? 2 : 0);
-        label[p] = reg;
-    }
-    for (int v = 0; v < 4; ++v) {
-        unsigned m = __ballot_sync(0xffffffffu, in && reg == v);
-        if ((threadIdx.x & 31) == 0 && m) atomicAdd(&counts[v], (unsigned long long)__popc(m));
-    }
-    bool a3 = in && reg == 3;
-    int mn = __reduce_min_sync(0xffffffffu, a3 ? x : INT_MAX);
-    int mx = __reduce_max_sync(0xffffffffu, a3 ? x : -1);
-    if ((threadIdx.x & 31) == 0 && mx >= 0) {
-        atomicMin(&box[0], mn);
-        atomicMin(&box[1], y);
-        atomicMax(&box[2], mx);
-        atomicMax(&box[3], y);
+    FS_FOR_ROWS(y, h) {
+        uint8_t reg = 0;
+        bool in = x < w;
+        if (in) {
+            size_t p = (size_t)y * w + x;
+            bool l = ml[p] != 0, r = mr[p] != 0;
+            reg = l ? (r ? 3 : 1) : (r ? 2 : 0);
+            label[p] = reg;
+        }
+        for (int v = 0; v < 4; ++v) {
+            unsigned m = __ballot_sync(0xffffffffu, in && reg == v);
+            if ((threadIdx.x & 31) == 0 && m) atomicAdd(&counts[v], (unsigned long long)__popc(m));
+        }
+        bool a3 = in && reg == 3;
+        int mn = __reduce_min_sync(0xffffffffu, a3 ? x : INT_MAX);
+        int mx = __reduce_max_sync(0xffffffffu, a3 ? x : -1);
+        if ((threadIdx.x & 31) == 0 && mx >= 0) {
+            atomicMin(&box[0], mn);
+            atomicMin(&box[1], y);
+            atomicMax(&box[2], mx);
+            atomicMax(&box[3], y);
+        }
     }
 }
 
 // Area3 box from a label plane (crop_overlap on a given partition)
 __global__ void k_label_box(const uint8_t* __restrict__ label, int w, int h, int* box) {
     int x = blockIdx.x * blockDim.x + threadIdx.x;
-    int y = blockIdx.y;
-    bool a3 = x < w && label[(size_t)y * w + x] == 3;
-    int mn = __reduce_min_sync(0xffffffffu, a3 ? x : INT_MAX);
-    int mx = __reduce_max_sync(0xffffffffu, a3 ? x : -1);
-    if ((threadIdx.x & 31) == 0 && mx >= 0) {
-        atomicMin(&box[0], mn);
-        atomicMin(&box[1], y);
-        atomicMax(&box[2], mx);
-        atomicMax(&box[3], y);
+    FS_FOR_ROWS(y, h) {
+        bool a3 = x < w && label[(size_t)y * w + x] == 3;
+        int mn = __reduce_min_sync(0xffffffffu, a3 ? x : INT_MAX);
+        int mx = __reduce_max_sync(0xffffffffu, a3 ? x : -1);
+        if ((threadIdx.x & 31) == 0 && mx >= 0) {
+            atomicMin(&box[0], mn);
+            atomicMin(&box[1], y);
+            atomicMax(&box[2], mx);
+            atomicMax(&box[3], y);
+        }
     }
 }
 
@@ -114,12 +121,13 @@ __global__ void k_crop(const float* __restrict__ img, const uint8_t* __restrict_
                        int ch, const uint8_t* __restrict__ label, int bx, int by, int bw, int bh,
                        float* __restrict__ out, uint8_t* __restrict__ out_valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= bw) return;
-    size_t s = (size_t)(j + by) * w + (i + bx), d = (size_t)j * bw + i;
-    bool v = valid[s] != 0;
-    for (int c = 0; c < ch; ++c) out[d * ch + c] = v ? img[s * ch + c] : 0.f;
-    out_valid[d] = (label[s] == 3 && v) ? 1 : 0;
+    FS_FOR_ROWS(j, bh) {
+        if (i >= bw) return;
+        size_t s = (size_t)(j + by) * w + (i + bx), d = (size_t)j * bw + i;
+        bool v = valid[s] != 0;
+        for (int c = 0; c < ch; ++c) out[d * ch + c] = v ? img[s * ch + c] : 0.f;
+        out_valid[d] = (label[s] == 3 && v) ? 1 : 0;
+    }
 }
 
 // src/image.cpp:169-175 (the canvas was zero-filled / invalidated first)
@@ -127,11 +135,12 @@ __global__ void k_place(const float* __restrict__ img, const uint8_t* __restrict
                         int h, int ch, int ox, int oy, int cw, float* __restrict__ out,
                         uint8_t* __restrict__ out_valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= w) return;
-    size_t s = (size_t)j * w + i, d = (size_t)(j + oy) * cw + (i + ox);
-    for (int c = 0; c < ch; ++c) out[d * ch + c] = img[s * ch + c];
-    out_valid[d] = valid ? valid[s] : 1;
+    FS_FOR_ROWS(j, h) {
+        if (i >= w) return;
+        size_t s = (size_t)j * w + i, d = (size_t)(j + oy) * cw + (i + ox);
+        for (int c = 0; c < ch; ++c) out[d * ch + c] = img[s * ch + c];
+        out_valid[d] = valid ? valid[s] : 1;
+    }
 }
 
 // src/flow.cpp:342-355 (canvas pre-filled with zero flow, valid = 1)
@@ -139,11 +148,12 @@ __global__ void k_embed(const float2* __restrict__ vec, const uint8_t* __restric
                         int h, int ox, int oy, int cw, float2* __restrict__ out,
                         uint8_t* __restrict__ out_valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= w) return;
-    size_t s = (size_t)j * w + i, d = (size_t)(j + oy) * cw + (i + ox);
-    out[d] = vec[s];
-    out_valid[d] = valid[s];
+    FS_FOR_ROWS(j, h) {
+        if (i >= w) return;
+        size_t s = (size_t)j * w + i, d = (size_t)(j + oy) * cw + (i + ox);
+        out[d] = vec[s];
+        out_valid[d] = valid[s];
+    }
 }
 
 __global__ void k_fill_flow(float2* __restrict__ v, uint8_t* __restrict__ ok, size_t n) {
@@ -199,57 +209,60 @@ __global__ void k_blend_pair(ImgSampler L, ImgSampler R, int w, int h, int ch,
                              double k, double coef, float* __restrict__ out,
                              uint8_t* __restrict__ out_valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= w) return;
-    size_t p = (size_t)j * w + i;
-    uint8_t reg = label[p];
-    float res[3] = {0.f, 0.f, 0.f};
-    uint8_t v = 1;
-    if (reg == 1) {
-        for (int c = 0; c < ch; ++c) res[c] = L.data[p * ch + c];
-    } else if (reg == 2) {
-        for (int c = 0; c < ch; ++c) res[c] = R.data[p * ch + c];
-    } else if (reg == 3) {
-        double blend_r = b[p];
-        double blend_l = 1.0 - blend_r;
-        float2 rl = frl[p], lr = flr[p];
-        float cl[3], cr[3];
-        sample(L, w, h, ch, i + rl.x * (1.0 - blend_l), j + rl.y * (1.0 - blend_l), cl);
-        sample(R, w, h, ch, i + lr.x * (1.0 - blend_r), j + lr.y * (1.0 - blend_r), cr);
-        double mag_rl = sqrt((double)rl.x * rl.x + (double)rl.y * rl.y);
-        double mag_lr = sqrt((double)lr.x * lr.x + (double)lr.y * lr.y);
-        double sl, sr;
-        softmax_weights(blend_l, blend_r, mag_rl, mag_lr, k, coef, sl, sr);
-        for (int c = 0; c < ch; ++c) res[c] = (float)clampd(cl[c] * sl + cr[c] * sr, 0.0, 1.0);
-    } else {
-        v = 0;
+    FS_FOR_ROWS(j, h) {
+        if (i >= w) return;
+        size_t p = (size_t)j * w + i;
+        uint8_t reg = label[p];
+        float res[3] = {0.f, 0.f, 0.f};
+        uint8_t v = 1;
+        if (reg == 1) {
+            for (int c = 0; c < ch; ++c) res[c] = L.data[p * ch + c];
+        } else if (reg == 2) {
+            for (int c = 0; c < ch; ++c) res[c] = R.data[p * ch + c];
+        } else if (reg == 3) {
+            double blend_r = b[p];
+            double blend_l = 1.0 - blend_r;
+            float2 rl = frl[p], lr = flr[p];
+            float cl[3], cr[3];
+            sample(L, w, h, ch, i + rl.x * (1.0 - blend_l), j + rl.y * (1.0 - blend_l), cl);
+            sample(R, w, h, ch, i + lr.x * (1.0 - blend_r), j + lr.y * (1.0 - blend_r), cr);
+            double mag_rl = sqrt((double)rl.x * rl.x + (double)rl.y * rl.y);
+            double mag_lr = sqrt((double)lr.x * lr.x + (double)lr.y * lr.y);
+            double sl, sr;
+            softmax_weights(blend_l, blend_r, mag_rl, mag_lr, k, coef, sl, sr);
+            for (int c = 0; c < ch; ++c) res[c] = (float)clampd(cl[c] * sl + cr[c] * sr, 0.0, 1.0);
+        } else {
+            v = 0;
+        }
+        for (int c = 0; c < ch; ++c) out[p * ch + c] = res[c];
+        out_valid[p] = v;
     }
-    for (int c = 0; c < ch; ++c) out[p * ch + c] = res[c];
-    out_valid[p] = v;
 }
 
 // src/blender.cpp:102-135
-__global__ void k_feather(const float* __restrict__ l, const float* __restrict__ r, int w, int ch,
+__global__ void k_feather(const float* __restrict__ l, const float* __restrict__ r, int w, int h,
+                          int ch,
                           const double* __restrict__ b, const uint8_t* __restrict__ label,
                           float* __restrict__ out, uint8_t* __restrict__ out_valid) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= w) return;
-    size_t p = (size_t)j * w + i;
-    uint8_t reg = label[p];
-    uint8_t v = 1;
-    for (int c = 0; c < ch; ++c) {
-        float res = 0.f;
-        if (reg == 1)
-            res = l[p * ch + c];
-        else if (reg == 2)
-            res = r[p * ch + c];
-        else if (reg == 3)
-            res = (float)clampd((1.0 - b[p]) * l[p * ch + c] + b[p] * r[p * ch + c], 0.0, 1.0);
-        out[p * ch + c] = res;
+    FS_FOR_ROWS(j, h) {
+        if (i >= w) return;
+        size_t p = (size_t)j * w + i;
+        uint8_t reg = label[p];
+        uint8_t v = 1;
+        for (int c = 0; c < ch; ++c) {
+            float res = 0.f;
+            if (reg == 1)
+                res = l[p * ch + c];
+            else if (reg == 2)
+                res = r[p * ch + c];
+            else if (reg == 3)
+                res = (float)clampd((1.0 - b[p]) * l[p * ch + c] + b[p] * r[p * ch + c], 0.0, 1.0);
+            out[p * ch + c] = res;
+        }
+        if (reg == 0) v = 0;
+        out_valid[p] = v;
     }
-    if (reg == 0) v = 0;
-    out_valid[p] = v;
 }
 
 // src/blender.cpp:137-163 (outputs pre-filled with copies of L and R)
@@ -260,19 +273,20 @@ __global__ void k_warp_constituents(ImgSampler L, ImgSampler R, int w, int h, in
                                     uint8_t* __restrict__ ovl, float* __restrict__ orr,
                                     uint8_t* __restrict__ ovr) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int j = blockIdx.y;
-    if (i >= w) return;
-    size_t p = (size_t)j * w + i;
-    if (label[p] != 3) return;
-    double blend_r = b[p];
-    double blend_l = 1.0 - blend_r;
-    float c[3];
-    sample(L, w, h, ch, i + frl[p].x * (1.0 - blend_l), j + frl[p].y * (1.0 - blend_l), c);
-    for (int q = 0; q < ch; ++q) ol[p * ch + q] = c[q];
-    ovl[p] = 1;
-    sample(R, w, h, ch, i + flr[p].x * (1.0 - blend_r), j + flr[p].y * (1.0 - blend_r), c);
-    for (int q = 0; q < ch; ++q) orr[p * ch + q] = c[q];
-    ovr[p] = 1;
+    FS_FOR_ROWS(j, h) {
+        if (i >= w) return;
+        size_t p = (size_t)j * w + i;
+        if (label[p] != 3) continue;
+        double blend_r = b[p];
+        double blend_l = 1.0 - blend_r;
+        float c[3];
+        sample(L, w, h, ch, i + frl[p].x * (1.0 - blend_l), j + frl[p].y * (1.0 - blend_l), c);
+        for (int q = 0; q < ch; ++q) ol[p * ch + q] = c[q];
+        ovl[p] = 1;
+        sample(R, w, h, ch, i + flr[p].x * (1.0 - blend_r), j + flr[p].y * (1.0 - blend_r), c);
+        for (int q = 0; q < ch; ++q) orr[p * ch + q] = c[q];
+        ovr[p] = 1;
+    }
 }
 
 // ImageBuf (interleaved ch) -> float4 + valid plane, for the fold's views
@@ -329,7 +343,9 @@ void count_nonfinite(const float* v, size_t n, unsigned long long* cnt, cudaStre
 }
 
 static inline unsigned nblk(size_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
-static inline dim3 rows(int w, int h, int b = 256) { return dim3((w + b - 1) / b, h); }
+static inline dim3 rows(int w, int h, int b = 256) {
+    return dim3((w + b - 1) / b, (unsigned)std::min(h, 65535));
+}
 
 void to_gray(const float* img, int n, int ch, float* out, cudaStream_t s) {
     k_to_gray<<<nblk(n), 256, 0, s>>>(img, n, ch, out);
@@ -382,7 +398,7 @@ void blend_pair(const float* l, const uint8_t* vl, const float* r, const uint8_t
 }
 void feather(const float* l, const float* r, int w, int h, int ch, const double* b,
              const uint8_t* label, float* out, uint8_t* out_valid, cudaStream_t s) {
-    k_feather<<<rows(w, h), 256, 0, s>>>(l, r, w, ch, b, label, out, out_valid);
+    k_feather<<<rows(w, h), 256, 0, s>>>(l, r, w, h, ch, b, label, out, out_valid);
 }
 void warp_constituents(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr, int w,
                        int h, int ch, const float2* flr, const float2* frl, const double* b,

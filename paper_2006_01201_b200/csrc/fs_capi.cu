@@ -465,6 +465,7 @@ fs_status fs_embed_flow(const float* vec, const uint8_t* valid, int w, int h, in
 fs_status fs_distance_transform(const uint8_t* mask, int w, int h, double* out, void* stream) {
     return guarded([&] {
         if (w <= 0 || h <= 0) raise(FS_ERR_CONTRACT, "distance_transform: empty canvas");
+        check_edt_extent(w, h, "distance_transform");
         Stage st(stream);
         size_t n = (size_t)w * h;
         const uint8_t* dm = st.in(mask, n);
@@ -486,6 +487,7 @@ fs_status fs_compute_blend(const uint8_t* label, const int64_t* counts, int w, i
                            void* stream) {
     return guarded([&] {
         check_dims(w, h);
+        check_edt_extent(w, h, "compute_blend");
         int64_t c[4];
         read_counts(counts, c);
         Stage st(stream);
@@ -658,6 +660,7 @@ fs_status fs_stitch_placed(int n, const float* const* images, const uint8_t* con
         validate_flow_params(*flow);
         validate_blend_params(*blend);
         check_ch(ch);
+        check_edt_extent(canvas_w, canvas_h, "stitch");
         Stage st(stream);
         const size_t nc = (size_t)canvas_w * canvas_h;
         Canvas cv;

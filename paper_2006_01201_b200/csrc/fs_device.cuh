@@ -2,11 +2,30 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "fs_math.cuh"
 
 namespace fs {
+
+// Run `fn` once per CUDA device (the current one) and per `flags` word:
+// kernel attributes such as the dynamic shared-memory opt-in belong to a
+// device's context, so a process driving several GPUs (or several threads)
+// must apply them for each device, exactly once.
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& flags, F&& fn) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (flags.load(std::memory_order_acquire) & bit) return;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (flags.load(std::memory_order_relaxed) & bit) return;
+    fn(dev);
+    flags.fetch_or(bit, std::memory_order_release);
+}
 
 constexpr int kInfSq = 0x3fffffff;  // "no seed" squared distance (exceeds any canvas d^2)
 

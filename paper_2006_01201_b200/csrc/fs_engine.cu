@@ -44,21 +44,33 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) raise(FS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Per device (the current one): is it an sm_100 part?  Checked once per
+// device, thread-safe; kernel attributes are applied per device (launch::init).
 void ensure_device() {
-    static int ok = -1;
-    if (ok < 0) {
-        int n = 0;
-        ok = 0;
-        if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0) {
-            int dev = 0, major = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-            ok = major == 10 ? 1 : 0;
-        }
+    static std::atomic<unsigned long long> checked{0}, good{0};
+    int n = 0, dev = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0 || cudaGetDevice(&dev) != cudaSuccess) {
         cudaGetLastError();
+        raise(FS_ERR_CUDA, "no sm_100 (B200) CUDA device available; the flow+blend path has no "
+                           "CPU fallback");
     }
-    if (!ok) raise(FS_ERR_CUDA, "no sm_100 (B200) CUDA device available; the flow+blend path has no CPU fallback");
+    once_per_device(checked, [&](int d) {
+        int major = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+        cudaGetLastError();
+        if (major == 10) good.fetch_or(1ull << (d & 63));
+    });
+    if (!(good.load() & (1ull << (dev & 63))))
+        raise(FS_ERR_CUDA, "CUDA device " + std::to_string(dev) + " is not an sm_100 (B200) "
+                           "part; the flow+blend path has no CPU fallback");
     launch::init();
+}
+
+void check_edt_extent(long long w, long long h, const char* what) {
+    if ((w - 1) * (w - 1) + (h - 1) * (h - 1) >= (long long)kInfSq)
+        raise(FS_ERR_UNSUPPORTED, std::string(what) + ": a " + std::to_string(w) + "x" +
+                                      std::to_string(h) + " canvas exceeds the distance "
+                                      "transform's exact range ((w-1)^2 + (h-1)^2 < 2^30 - 1)");
 }
 
 // src/flow.cpp:15-21 (same messages)
@@ -70,7 +82,8 @@ void validate_flow_params(const fs_flow_params& p) {
     if (!(p.min_eigen_eps > 0.0)) raise(FS_ERR_CONTRACT, "FlowParams: min_eigen_eps must be > 0");
     if (p.smoothing_passes < 0) raise(FS_ERR_CONTRACT, "FlowParams: smoothing_passes must be >= 0");
     if (p.window_radius > launch::lk_max_radius())
-        raise(FS_ERR_UNSUPPORTED, "FlowParams: window_radius above the kernel's maximum (48)");
+        raise(FS_ERR_UNSUPPORTED, "FlowParams: window_radius above the kernel's maximum (" +
+                                      std::to_string(launch::lk_max_radius()) + ")");
 }
 
 // src/blender.cpp:11-16
@@ -236,11 +249,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             }
             if (full && split) FS_CK(cudaStreamWaitEvent(s, ws.ev_tensor[l], 0));
             {
-                // per pixel and direction: F 4 + T 4 (It gather) + flow 8 in,
-                //  flow 8 out; first iteration: ok 1 in/out + coef 16 out (FULL)
-                //  or in (split); later: coef 16 in
-                double per = 24.0 + (full ? 2.0 + (a.d[0].coef ? 16.0 : 0.0) : 16.0);
-                ProfScope ps(kSweepNames[full && !split][std::min(l, 7)], per * npx, s);
+                // 26 B per px, direction and iteration
+                // (F 4 + T 4 + flow r/w 16 + ok r/w 2); the level-constant
+                // inverse tensor this design also moves (16 B) is not counted
+                ProfScope ps(kSweepNames[full && !split][std::min(l, 7)], 26.0 * npx, s);
                 FS_CK(launch::lk_sweep(a, full ? (split ? 3 : 1) : 0, s));
             }
             ++launches;
@@ -265,8 +277,9 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.valid_out[d] = out_valid[d];
             }
             {
+                // 16 B per px, direction and pass
                 ProfScope ps(l == 0 ? "smooth" : "smooth_coarse",
-                             (16.0 + (fin ? 2.0 : 0.0)) * L.w * L.h * ws.ndir, s);
+                             16.0 * passes * L.w * L.h * ws.ndir, s);
                 launch::smooth(a, s);
             }
             ++launches;

@@ -27,6 +27,10 @@ void validate_flow_params(const fs_flow_params& p);    // src/flow.cpp:15-21
 void validate_blend_params(const fs_blend_params& p);  // src/blender.cpp:11-16
 int pyramid_depth(int w, int h, int levels);           // src/flow.cpp:178-185
 void ensure_device();                                  // throws FS_ERR_CUDA without sm_100
+// Squared distances are int32 with the "no seed" sentinel kInfSq = 2^30 - 1:
+// every in-canvas squared distance (w-1)^2 + (h-1)^2 must stay below it
+// (e.g. 16384 x 16384 is fine, 32768 x 1 is not) -> FS_ERR_UNSUPPORTED.
+void check_edt_extent(long long w, long long h, const char* what);
 
 // Per-launch kernel timing (fs_plan_profile): when a profile run installs a
 // KernelProf, every launch site records CUDA events around its kernel on the

@@ -32,6 +32,7 @@
 // iterations form only the two mismatch sums and update by -(M^-1 b).
 // Products are exact in double (float x float) and all window sums are double,
 // agreeing with the reference's double prefix tables to ~1e-12 relative.
+#include <algorithm>
 #include <type_traits>
 
 #include "fs_device.cuh"
@@ -473,15 +474,33 @@ __global__ void __launch_bounds__(LK_THREADS, LkCfg<M>::MINB) k_lk_sweep(LkArgs 
 
 namespace launch {
 
-static bool lk_configured = false;
+// the largest dynamic shared memory any sweep mode needs at radius r
+static size_t lk_smem_max(int r) {
+    size_t m = lk_smem_bytes<LK_ITER>(r);
+    m = std::max(m, lk_smem_bytes<LK_FULL>(r));
+    m = std::max(m, lk_smem_bytes<LK_TENSOR>(r));
+    m = std::max(m, lk_smem_bytes<LK_FIRST>(r));
+    return m;
+}
+static int lk_optin_bytes() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+        cudaSuccess)
+        optin = 227 * 1024;  // sm_100
+    return optin;
+}
+static std::atomic<unsigned long long> lk_configured{0};
 void lk_init() {
-    if (lk_configured) return;
-    const int mx = 200 * 1024;
-    cudaFuncSetAttribute(k_lk_sweep<LK_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_sweep<LK_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_sweep<LK_TENSOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_lk_sweep<LK_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    lk_configured = true;
+    once_per_device(lk_configured, [](int) {
+        const int mx = lk_optin_bytes();
+        cudaFuncSetAttribute(k_lk_sweep<LK_ITER>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_lk_sweep<LK_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_lk_sweep<LK_TENSOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+        cudaFuncSetAttribute(k_lk_sweep<LK_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+    });
 }
 
 #ifndef LK_TH_MIN
@@ -537,8 +556,15 @@ cudaError_t lk_sweep(const LkArgs& a0, int mode, cudaStream_t s) {
 }
 
 // NB * nruns must fit the 128 consumer threads: tw = 128 - 2r, runs of 4
-// (FULL, NB = 4) or 8 (NB = 8) => any r <= 48 keeps tw >= 32.
-int lk_max_radius() { return 48; }
+// (FULL, NB = 4) or 8 (NB = 8) => any r <= 48 keeps tw >= 32; and every
+// sweep mode's ring + staging must fit the device's shared-memory opt-in
+// (r <= 45 on sm_100's 227 KB).
+int lk_max_radius() {
+    const size_t optin = (size_t)lk_optin_bytes();
+    int r = 48;
+    while (r > 1 && lk_smem_max(r) > optin) --r;
+    return r;
+}
 
 }  // namespace launch
 }  // namespace fs

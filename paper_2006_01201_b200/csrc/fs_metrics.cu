@@ -308,12 +308,11 @@ template <class GL, class GR, class RV, class A3>
 void launch_points(GL gl, GR gr, RV rv, A3 a3, int w, int h, int rad, int stride, int gx0,
                    int gy0, int ngx, int ngy, int* res, cudaStream_t s) {
     auto k = &k_misalign_point<GL, GR, RV, A3>;
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&](int) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)ms_smem(metrics::misalign_max_radius()));
-        configured = true;
-    }
+    });
     if (ngx > 0 && ngy > 0)
         k<<<dim3(ngx, ngy), MS_THREADS, ms_smem(rad), s>>>(gl, gr, rv, a3, w, h, rad, stride, gx0,
                                                             gy0, ngx, res);

@@ -1024,6 +1024,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         if (n < 2) raise(FS_ERR_CONTRACT, "stitch: at least two images required");
         validate_flow_params(*flow);
         validate_blend_params(*blend);
+        check_edt_extent(canvas_w, canvas_h, "plan");
         p->device = device;
         p->n = n;
         p->cw = canvas_w;
@@ -1185,6 +1186,23 @@ fs_status fs_plan_fold_info(fs_plan p, int k, int* box, int* depth) {
     box[3] = f.box.h;
     if (depth) *depth = f.depth;
     return FS_OK;
+}
+
+fs_status fs_plan_fold_flow(fs_plan p, int k, float* ltor_vec, uint8_t* ltor_valid,
+                            float* rtol_vec, uint8_t* rtol_valid) {
+    if (!p || k < 1 || k >= p->n) return FS_ERR_CONTRACT;
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        FS_CK(cudaDeviceSynchronize());
+        const FoldWS<ViewU8>& f = p->folds[k - 1];
+        size_t n = (size_t)f.box.w * f.box.h;
+        float* vec[2] = {ltor_vec, rtol_vec};
+        uint8_t* val[2] = {ltor_valid, rtol_valid};
+        for (int d = 0; d < 2; ++d) {
+            if (vec[d]) FS_CK(cudaMemcpy(vec[d], f.fvec[d], n * sizeof(float2), cudaMemcpyDefault));
+            if (val[d]) FS_CK(cudaMemcpy(val[d], f.fvalid[d], n, cudaMemcpyDefault));
+        }
+    });
 }
 
 fs_status fs_plan_execute(fs_plan p, void* stream) {

@@ -58,6 +58,15 @@ class Plan:
         _raise(N.lib.fs_plan_fold_info(self._h, k, box.ctypes.data_as(C.c_void_p), C.byref(depth)))
         return tuple(int(v) for v in box), depth.value
 
+    def fold_flow(self, k: int):
+        """Fold k's crop flows of the last execution: ((ltor vec, valid), (rtol vec, valid)),
+        box-sized, the FlowField layout."""
+        (x, y, w, h), _ = self.fold_info(k)
+        out = [np.empty((h, w, 2), np.float32), np.empty((h, w), np.uint8),
+               np.empty((h, w, 2), np.float32), np.empty((h, w), np.uint8)]
+        _raise(N.lib.fs_plan_fold_flow(self._h, k, *[o.ctypes.data_as(C.c_void_p) for o in out]))
+        return (out[0], out[1]), (out[2], out[3])
+
     def set_host_format(self, view_channels: int = 4, out_channels: int = 4) -> None:
         """Host views RGB8 (3, all valid) or RGBA8 (4); host canvas RGB8 or RGBA8."""
         _raise(N.lib.fs_plan_set_host_format(self._h, view_channels, out_channels))

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import reference  # noqa: E402
-from paper_2006_01201_b200 import synthetic as S  # noqa: E402
+import fs_synthetic as S  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_v1.npz")
 

@@ -13,7 +13,7 @@ Tolerances (BASELINE.json north_star):
 import numpy as np
 import pytest
 
-from paper_2006_01201_b200 import synthetic as S
+import fs_synthetic as S
 
 pytestmark = pytest.mark.gpu
 
@@ -792,3 +792,33 @@ def test_plan_rgb8_host_formats(fs, which):
     plan.execute_host(lay.views, again)
     assert np.array_equal(again, ref)
     plan.close()
+
+
+def test_lk_max_radius(fs, oracle):
+    """the largest accepted window radius runs every sweep mode
+    (ring + staging within the device's 227 KB opt-in, now requested in full:
+    r = 48, 215 KB for later iterations); r = 49 is refused up front
+    (FS_ERR_UNSUPPORTED -> ContractError), not at launch."""
+    h, w = 112, 120
+    base = S.value_noise(h + 8, w + 8, seed=45)
+    frm, to = base[4:4 + h, 4:4 + w], base[3:3 + h, 6:6 + w]
+    p = fs.FlowParams(levels=2, window_radius=48, iterations_per_level=2)
+    f = fs.dense_pyr_lk(_img(fs, frm), _img(fs, to), p)
+    vec, valid = oracle.dense_pyr_lk(frm, to, p)
+    assert np.array_equal(f.valid, valid)
+    assert _epe(f.vec, vec) <= EPE_TOL
+    with pytest.raises(fs.ContractError, match="maximum"):
+        fs.dense_pyr_lk(_img(fs, frm), _img(fs, to), fs.FlowParams(levels=2, window_radius=49))
+
+
+def test_edt_extent_limit(fs, oracle):
+    """squared distances are int32 with a 2^30 - 1 sentinel; the
+    widest exact canvas row (32768 px: 32767^2 < 2^30 - 1) matches the
+    oracle, one pixel more is refused up front (FS_ERR_UNSUPPORTED)."""
+    m = np.zeros((1, 32768), np.uint8)
+    m[0, 0] = 1
+    d = fs.distance_transform(fs.Mask(m)).d
+    assert np.array_equal(d, oracle.distance_transform(m))
+    assert d[0, -1] == 32767.0
+    with pytest.raises(fs.ContractError, match="exact range"):
+        fs.distance_transform(fs.Mask(np.ones((1, 32769), np.uint8)))

@@ -6,7 +6,7 @@ the region its GPU holds final (FS_ERR_SHARD_REACH) and fall back."""
 import numpy as np
 import pytest
 
-from paper_2006_01201_b200 import synthetic as S
+import fs_synthetic as S
 
 pytestmark = pytest.mark.gpu
 

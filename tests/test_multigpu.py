@@ -22,7 +22,7 @@ def _free_port():
 
 def _fold(seed):
     from oracle import restatement
-    from paper_2006_01201_b200 import synthetic as S
+    import fs_synthetic as S
     lay = S.small_strip(seed=seed, n=3, vw=48, vh=32, step=32, parallax=2)
     fv = lay.float_views()
     out, _ = restatement().stitch_placed([d for d, _ in fv], [v for _, v in fv], lay.offsets,
@@ -68,3 +68,54 @@ def test_two_rank_gloo_matches_single_process():
         assert res == single
         assert mx == 2.5  # max over ranks of (1.5 + rank)
         assert tot == 5
+
+
+def _bench(*args, timeout=600):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", 2), ("c4", 3)])
+def test_bench_spawns_ranks_dry_run(cfg, n):
+    """`bench.py --gpus N` without a launcher starts N ranks itself (torchrun on
+    127.0.0.1); --dry-run exchanges the shard schedule's strips over gloo."""
+    lines = _bench("--gpus", str(n), "--dry-run", "--config", cfg)
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == n and d["backend"] == "gloo" and d["status"] == 0
+    assert set(d["fold_rank"]) == set(range(n))
+    assert d["received_rank0"] == sorted(k for k in range(1, len(d["fold_rank"]))
+                                         if d["fold_rank"][k] != 0)
+
+
+def test_reference_arm_is_clean():
+    """--impl reference imports neither torch nor the B200 package and times
+    whole stitch_placed calls with the B200 arm's config dict."""
+    from oracle import ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import runpy, sys, json; sys.argv = ['bench.py', '--impl', 'reference', '--config', "
+            "'c1', '--steps', '1', '--warmup', '0']; runpy.run_path('bench.py', "
+            "run_name='__main__'); print(json.dumps({'mods': sorted(m for m in sys.modules "
+            "if m.split('.')[0] in ('torch', 'paper_2006_01201_b200'))}))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    line, mods = lines[0], lines[1]["mods"]
+    assert mods == []
+    assert line["impl"] == "reference" and line["steps"] == 1
+    assert line["config"]["workload"].startswith("C1") and line["config"]["folds"] == 1
+    assert "whole C1 stitch_placed" in line["cpu_baseline"]["sample"]

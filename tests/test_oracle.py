@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from oracle import ref_available, reference, restatement
-from paper_2006_01201_b200 import synthetic as S
+import fs_synthetic as S
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz")
 

@@ -6,7 +6,7 @@ GPU remap bit-exact on the same table) and by a render -> remap round trip."""
 import numpy as np
 import pytest
 
-from paper_2006_01201_b200 import synthetic as S
+import fs_synthetic as S
 
 
 def _cam(fs, **kw):

@@ -2,7 +2,7 @@
 §8(d) specify and are deterministic."""
 import numpy as np
 
-from paper_2006_01201_b200 import synthetic as S
+import fs_synthetic as S
 
 
 def test_value_noise_range_and_determinism():

@@ -25,7 +25,7 @@ CASES = [((64, 64), dict(levels=3, window_radius=5, iterations_per_level=3)),
 
 def dump(path):
     import paper_2006_01201_b200.api as fs
-    from paper_2006_01201_b200 import synthetic as S
+    import fs_synthetic as S
     out = {}
     for k, ((h, w), kw) in enumerate(CASES):
         base = S.value_noise(h + 40, w + 40, seed=w + k)

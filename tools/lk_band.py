@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 import paper_2006_01201_b200 as fs  # noqa: E402
-from paper_2006_01201_b200 import synthetic as S  # noqa: E402
+import fs_synthetic as S  # noqa: E402
 
 h, w = 400, 9000
 a = S.value_noise(h, w + 16, 3).astype(np.float32)

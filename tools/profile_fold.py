@@ -14,7 +14,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2006_01201_b200 as fs  # noqa: E402
-from paper_2006_01201_b200 import synthetic as S  # noqa: E402
+import fs_synthetic as S  # noqa: E402
 
 
 def main():
