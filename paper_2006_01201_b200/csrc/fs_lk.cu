@@ -53,6 +53,15 @@ enum { LK_ITER = 0, LK_FULL = 1, LK_TENSOR = 2, LK_FIRST = 3 };
 #ifndef LK_MINB_ITER
 #define LK_MINB_ITER 3
 #endif
+#ifndef LK_MINB_F32
+#define LK_MINB_F32 3
+#endif
+#ifndef LK_NS_F32
+#define LK_NS_F32 2
+#endif
+#ifndef LK_IW_F32
+#define LK_IW_F32 128
+#endif
 
 template <int M>
 struct LkCfg {
@@ -67,44 +76,75 @@ struct LkCfg {
     static constexpr int NB = FULL ? LK_NB_FULL : LK_NB_ITER;  // rows per staged batch
     static constexpr int S = FULL ? LK_S_FULL : LK_S_ITER;     // outputs per horizontal run
     static constexpr bool GATHER = M != LK_TENSOR;              // It = T(p + d) - F(p)
+    // Accumulation type.  FULL and TENSOR decide the level's valid bits (the
+    // eigenvalue test) and keep the reference's double window sums; the
+    // later iterations (ITER/FIRST) only refine a flow whose validity is
+    // settled, and run in fp32: It by a float bilinear, products, window sums
+    // and the update in float (well inside the 0.05 px mean-EPE budget;
+    // -DFS_LK_ITER_F64 restores the double sweep).
+#ifdef FS_LK_ITER_F64
+    using Acc = double;
+#else
+    using Acc = std::conditional_t<M == LK_ITER || M == LK_FIRST, float, double>;
+#endif
+    static constexpr bool F32 = std::is_same<Acc, float>::value;
     // ring entries per column and row: FULL (Ix, Iy, It) and TENSOR (Ix, Iy)
-    // as floats (products re-formed), ITER/FIRST the two double products
+    // as floats (products re-formed), ITER/FIRST the two products themselves
     static constexpr size_t RING = M == LK_FULL ? 3 * sizeof(float)
-                                 : M == LK_TENSOR ? 2 * sizeof(float) : 2 * sizeof(double);
-    static constexpr int MINB = M == LK_FULL ? LK_MINB_FULL : LK_MINB_ITER;
+                                 : M == LK_TENSOR ? 2 * sizeof(float) : 2 * sizeof(Acc);
+    static constexpr int MINB = F32 ? LK_MINB_F32 : M == LK_FULL ? LK_MINB_FULL : LK_MINB_ITER;
+    // producer threads = input columns per CTA; 4 consumer warps.  The fp32
+    // sweeps take 256 columns (240 outputs at r = 8: 7% halo columns, not
+    // 14%) and run 2 CTAs/SM = 16 producer warps per SM.
+    static constexpr int IW = F32 ? LK_IW_F32 : 128;
+    static constexpr int THREADS = IW + 128;
+    // staging buffers between producers and consumers (named barriers
+    // 1..NS "staged", NS+1..2NS "released")
+    static constexpr int NS = F32 ? LK_NS_F32 : 2;
 };
 
 #ifndef LK_CARRY_FULL
 #define LK_CARRY_FULL 1
 #endif
-constexpr int LK_IW = 128;  // producer threads = input columns per CTA
-constexpr int LK_THREADS = 2 * LK_IW;
 
-// Staged sums: plane [q][batch row][column] with an odd row stride, so the
-// consumers (consecutive threads = consecutive batch rows, then runs) read
-// without bank conflicts and with plain column offsets.
-__host__ __device__ inline int lk_iwp(int iw) { return iw + 1; }
+// Staged sums: plane [q][batch row][column].  Double modes: an odd row
+// stride, so the consumers (consecutive threads = consecutive batch rows,
+// then runs) read without bank conflicts and with plain column offsets.
+// fp32 modes: one consumer warp per batch row reads its row as float4s (row
+// stride 128, 16-byte aligned).
+template <int M>
+__host__ __device__ constexpr int lk_iwp() { return LkCfg<M>::F32 ? LkCfg<M>::IW : LkCfg<M>::IW + 1; }
 // Ring of the last 2r+1 rows per column, so the row leaving the window is
 // subtracted exactly: FULL keeps (Ix, Iy, It) as floats (five products are
 // re-formed), later iterations keep the two double products themselves.
 template <int M>
 __host__ __device__ inline size_t lk_ring_bytes(int r) {
-    return ((size_t)(2 * r + 1) * LK_IW * LkCfg<M>::RING + 15) & ~size_t(15);
+    return ((size_t)(2 * r + 1) * LkCfg<M>::IW * LkCfg<M>::RING + 15) & ~size_t(15);
 }
 template <int M>
-__host__ __device__ inline size_t lk_stage_doubles() {
-    return (size_t)LkCfg<M>::NB * LkCfg<M>::NQ * lk_iwp(LK_IW);
+__host__ __device__ inline size_t lk_stage_elems() {
+    return (size_t)LkCfg<M>::NB * LkCfg<M>::NQ * lk_iwp<M>();
+}
+// fp32 sweeps: the four bilinear taps of every window pixel are copied
+// (cp.async) into shared memory one batch ahead: [buffer][row][tap][column]
+template <int M>
+__host__ __device__ inline size_t lk_tap_bytes() {
+    return LkCfg<M>::F32 ? (size_t)2 * LkCfg<M>::NB * 4 * LkCfg<M>::IW * sizeof(float) : 0;
 }
 template <int M>
 __host__ inline size_t lk_smem_bytes(int r) {
-    return lk_ring_bytes<M>(r) + 2 * lk_stage_doubles<M>() * sizeof(double);
+    return lk_ring_bytes<M>(r) +
+           LkCfg<M>::NS * lk_stage_elems<M>() * sizeof(typename LkCfg<M>::Acc) +
+           lk_tap_bytes<M>();
 }
 
+template <int NT>
 __device__ __forceinline__ void bar_sync(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
 }
+template <int NT>
 __device__ __forceinline__ void bar_arrive(int id) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(LK_THREADS) : "memory");
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(NT) : "memory");
 }
 
 // sample_level's clamp and taps (src/flow.cpp:100-111) at the float position
@@ -203,13 +243,16 @@ __device__ __forceinline__ double lk_fma(double a, double b, double v) {
 // ahead).  All indices are 32-bit (levels hold < 2^31 pixels).
 template <int M>
 __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void* ringv,
-                                           double* stage, int x0, int ystart, int yend, int nbat) {
+                                           typename LkCfg<M>::Acc* stage, int x0, int ystart,
+                                           int yend, int nbat) {
     using Cfg = LkCfg<M>;
+    using Acc = typename Cfg::Acc;
+    using Acc2 = std::conditional_t<Cfg::F32, float2, double2>;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ;
     constexpr bool FULL = Cfg::FULL, GATHER = Cfg::GATHER, TENSOR = M == LK_TENSOR;
     const int r = a.r, K = 2 * r + 1, w = a.w, h = a.h;
-    const int IWP = lk_iwp(LK_IW);
-    const int c = threadIdx.x;
+    constexpr int IWP = lk_iwp<M>(), IW = Cfg::IW, NT = Cfg::THREADS;
+    const int c = threadIdx.x, lane = c & 31;
     const int x = x0 - r + c;
     const bool xin = x >= 0 && x < w;
     const int xc = clampi(x, 0, w - 1);
@@ -218,19 +261,19 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     const float2* __restrict__ Uc = D.fin + xc;
     const float* __restrict__ T = D.T;
     float* ringf = static_cast<float*>(ringv);
-    double2* ringd = static_cast<double2*>(ringv);
+    Acc2* ringd = static_cast<Acc2*>(ringv);
     for (int k = 0; k < K; ++k) {
         if (FULL) {
-            float* rs = ringf + (k * LK_IW + c) * 3;
+            float* rs = ringf + (k * IW + c) * 3;
             rs[0] = rs[1] = rs[2] = 0.f;
         } else if (TENSOR) {
-            float* rs = ringf + (k * LK_IW + c) * 2;
+            float* rs = ringf + (k * IW + c) * 2;
             rs[0] = rs[1] = 0.f;
         } else {
-            ringd[k * LK_IW + c] = make_double2(0.0, 0.0);
+            ringd[k * IW + c] = Acc2{0, 0};
         }
     }
-    double V[NQ];
+    Acc V[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) V[q] = 0.0;
     auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
@@ -239,10 +282,11 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
 #pragma unroll
         for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
     }
-    // FULL (128 registers): the column of `from` walks down in registers,
-    // cen[j] = F(x, clamp(y)) for y = ybase - 1 .. ybase + NB (the vertical
-    // gradient's rows); later iterations (80 registers) reload them
-    constexpr bool CARRY = FULL && LK_CARRY_FULL;
+    // The column of `from` walks down in registers: cen[j] = F(x, clamp(y))
+    // for y = ybase - 1 .. ybase + NB (the vertical gradient's rows), the
+    // next batch's rows loaded one batch ahead.  (The double later-iteration
+    // build, at 80 registers, reloads them instead.)
+    constexpr bool CARRY = FULL ? LK_CARRY_FULL != 0 : (Cfg::F32 || TENSOR);
     float cen[CARRY ? NB + 2 : 1];
     if (CARRY) {
 #pragma unroll
@@ -252,7 +296,7 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     for (int i = 0; i < nbat; ++i) {
         const int buf = i & 1;
         const int ybase = ystart + i * NB;
-        float gxs[NB], gys[NB], dts[NB], tap[NB][4], tfx[NB], tfy[NB], ctr[NB];
+        float gxs[NB], gys[NB], dts[NB], tap[NB][4], tfx[NB], tfy[NB], ctr[NB], edge[NB];
         bool in[NB];
         // batches whose rows (and rows -1, +1) lie inside the level and the
         // band need no row clamps or row tests
@@ -265,7 +309,11 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 in[b] = INNER ? xin : (xin && y >= 0 && y < h && y < yend);
                 const int yy = INNER ? y : clampi(y, 0, h - 1);
                 const float* Fr = INNER ? Fb + b * w : Fc + yy * w;
-                gxs[b] = 0.5f * (__ldg(Fr + dxr) - __ldg(Fr + dxl));  // src/flow.cpp:230-235
+                // F(clamp(x -/+ 1), y) are the adjacent lanes' centres (their
+                // columns are x -/+ 1, clamped alike); the warp's edge lanes
+                // load theirs (the horizontal gradient is formed below)
+                edge[b] = 0.f;
+                if (lane == 0 || lane == 31) edge[b] = __ldg(Fr + (lane == 0 ? dxl : dxr));
                 if (CARRY) {
                     gys[b] = 0.5f * (cen[b + 2] - cen[b]);
                     ctr[b] = cen[b + 1];
@@ -302,23 +350,37 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
             }
         }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {  // src/flow.cpp:230-235, 0.5f * (F[i+1] - F[i-1])
+            float lf = __shfl_up_sync(0xffffffffu, ctr[b], 1);
+            float rt = __shfl_down_sync(0xffffffffu, ctr[b], 1);
+            if (lane == 0) lf = edge[b];
+            if (lane == 31) rt = edge[b];
+            gxs[b] = 0.5f * (rt - lf);
+        }
         if (GATHER) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                LevelTap t;
-                t.fx = tfx[b];
-                t.fy = tfy[b];
-                dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - ctr[b];
+                if (Cfg::F32) {  // float bilinear (lerp form) of the same taps
+                    const float u = __fmaf_rn(tfx[b], tap[b][1] - tap[b][0], tap[b][0]);
+                    const float v = __fmaf_rn(tfx[b], tap[b][3] - tap[b][2], tap[b][2]);
+                    dts[b] = __fmaf_rn(tfy[b], v - u, u) - ctr[b];
+                } else {
+                    LevelTap t;
+                    t.fx = tfx[b];
+                    t.fy = tfy[b];
+                    dts[b] = level_combine(t, tap[b][0], tap[b][1], tap[b][2], tap[b][3]) - ctr[b];
+                }
             }
         }
-        if (i >= 2) bar_sync(3 + buf);  // consumers released this buffer
-        double* st = stage + (size_t)buf * lk_stage_doubles<M>();
+        if (i >= 2) bar_sync<NT>(3 + buf);  // consumers released this buffer
+        Acc* st = stage + (size_t)buf * lk_stage_elems<M>();
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             const double ix = in[b] ? gxs[b] : 0.f, iy = in[b] ? gys[b] : 0.f;
             const double tt = (GATHER && in[b]) ? dts[b] : 0.f;
             if (TENSOR) {
-                float* rs = ringf + (slot * LK_IW + c) * 2;
+                float* rs = ringf + (slot * IW + c) * 2;
                 const double ogx = rs[0], ogy = rs[1];
                 rs[0] = (float)ix;
                 rs[1] = (float)iy;
@@ -326,7 +388,7 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 V[1] = lk_fma(-ogx, ogy, lk_fma(ix, iy, V[1]));
                 V[2] = lk_fma(-ogy, ogy, lk_fma(iy, iy, V[2]));
             } else if (FULL) {
-                float* rs = ringf + (slot * LK_IW + c) * 3;
+                float* rs = ringf + (slot * IW + c) * 3;
                 const double ogx = rs[0], ogy = rs[1], odt = rs[2];
                 rs[0] = (float)ix;
                 rs[1] = (float)iy;
@@ -337,33 +399,309 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
                 V[3] = lk_fma(-ogx, odt, lk_fma(ix, tt, V[3]));
                 V[4] = lk_fma(-ogy, odt, lk_fma(iy, tt, V[4]));
             } else {
-                double2* rp = ringd + (slot * LK_IW + c);
-                const double2 o = *rp;
-                const double px = ix * tt, py = iy * tt;
-                *rp = make_double2(px, py);
+                Acc2* rp = ringd + (slot * IW + c);
+                const Acc2 o = *rp;
+                const float fxx = in[b] ? gxs[b] : 0.f, fyy = in[b] ? gys[b] : 0.f;
+                const float ftt = in[b] ? dts[b] : 0.f;
+                const Acc px = (Acc)fxx * (Acc)ftt, py = (Acc)fyy * (Acc)ftt;  // double: exact
+                *rp = Acc2{px, py};
                 V[0] = (V[0] + px) - o.x;
                 V[1] = (V[1] + py) - o.y;
             }
             slot = slot + 1 == K ? 0 : slot + 1;
-            double* vb = st + b * IWP + c;
+            Acc* vb = st + b * IWP + c;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) vb[q * NB * IWP] = V[q];
         }
-        bar_arrive(1 + buf);  // batch staged
+        bar_arrive<NT>(1 + buf);  // batch staged
+    }
+}
+
+// ---- producer (fp32 later iterations): a software pipeline ---------------
+// Batch i's taps were issued (cp.async into shared memory) during batch i-1,
+// from the flow loaded during batch i-2; its `from` rows (cen) and the warp
+// edge lanes' horizontal neighbours were loaded during batch i-1.  So a batch
+// starts with its data on chip: gradients, It (float bilinear of the staged
+// taps), the two products, the column's running window sums (the row leaving
+// the window comes from the ring of the last 2r + 1 products), staging.
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int M>
+__device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, float2* ring,
+                                               float* stage, float* tapb, int x0, int ystart,
+                                               int yend, int nbat) {
+    using Cfg = LkCfg<M>;
+    constexpr int NB = Cfg::NB, IW = Cfg::IW, NT = Cfg::THREADS, IWP = lk_iwp<M>(), NS = Cfg::NS;
+    const int r = a.r, K = 2 * r + 1, w = a.w, h = a.h;
+    const int c = threadIdx.x, lane = c & 31;
+    const int x = x0 - r + c;
+    const bool xin = x >= 0 && x < w;
+    const int xc = clampi(x, 0, w - 1);
+    // warp edge lanes: the horizontal neighbour outside the warp (others: own column)
+    const int eoff = lane == 0 ? clampi(x - 1, 0, w - 1) - xc
+                   : lane == 31 ? clampi(x + 1, 0, w - 1) - xc : 0;
+    const float* __restrict__ Fc = D.F + xc;
+    const float2* __restrict__ Uc = D.fin + xc;
+    const float* __restrict__ T = D.T;
+    for (int k = 0; k < K; ++k) ring[k * IW + c] = make_float2(0.f, 0.f);
+    float V0 = 0.f, V1 = 0.f;
+    auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
+    const uint32_t tap0 = (uint32_t)__cvta_generic_to_shared(tapb + c);
+    // issue batch bi's taps (src/flow.cpp:100-111 at (i + dx, j + dy), :248)
+    auto stage_taps = [&](int bi, const float2* fl, float* fx, float* fy) {
+        const int yb = ystart + bi * NB;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int yy = clampi(yb + b, 0, h - 1);
+            const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
+            fx[b] = t.fx;
+            fy[b] = t.fy;
+            const float* p = T + t.off;
+            const uint32_t d = tap0 + (uint32_t)(((bi & 1) * NB + b) * 4 * IW) * 4u;
+            cp_async4(d, p);
+            cp_async4(d + IW * 4, p + t.dx);
+            cp_async4(d + 2 * IW * 4, p + t.dy);
+            cp_async4(d + 3 * IW * 4, p + (t.dy + t.dx));
+        }
+        cp_async_commit();
+    };
+    float2 fl[NB];
+    float tfx[NB], tfy[NB], cen[NB + 2], edg[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
+    stage_taps(0, fl, tfx, tfy);
+    if (nbat > 1) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + NB + b)];
+    }
+#pragma unroll
+    for (int j = 0; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ystart - 1 + j));
+#pragma unroll
+    for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ystart + b) + eoff);
+    int slot = 0;
+    for (int i = 0; i < nbat; ++i) {
+        const int buf = i % NS, tb = i & 1;
+        const int ybase = ystart + i * NB;
+        const bool more = i + 1 < nbat;
+        // gradients of this batch from the carried rows (src/flow.cpp:225-237),
+        // before any load of this iteration is issued (a fresh load sharing
+        // the carried values' scoreboard would make them wait for it)
+        float ctr[NB], gxs[NB], gys[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            ctr[b] = cen[b + 1];
+            gys[b] = 0.5f * (cen[b + 2] - cen[b]);
+            float lf = __shfl_up_sync(0xffffffffu, ctr[b], 1);
+            float rt = __shfl_down_sync(0xffffffffu, ctr[b], 1);
+            if (lane == 0) lf = edg[b];
+            if (lane == 31) rt = edg[b];
+            gxs[b] = 0.5f * (rt - lf);
+        }
+        float nfx[NB], nfy[NB];
+        if (more) {  // next batch's taps, then the flow two batches ahead
+            stage_taps(i + 1, fl, nfx, nfy);
+            if (i + 2 < nbat) {
+#pragma unroll
+                for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + 2 * NB + b)];
+            }
+        }
+        if (more) {  // next batch's `from` rows and edge neighbours
+            cen[0] = cen[NB];
+            cen[1] = cen[NB + 1];
+#pragma unroll
+            for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
+#pragma unroll
+            for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ybase + NB + b) + eoff);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        float dts[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {  // float bilinear (lerp form) of the staged taps
+            const float* tp = tapb + ((tb * NB + b) * 4) * IW + c;
+            const float t00 = tp[0], t10 = tp[IW], t01 = tp[2 * IW], t11 = tp[3 * IW];
+            const float u = __fmaf_rn(tfx[b], t10 - t00, t00);
+            const float v = __fmaf_rn(tfx[b], t11 - t01, t01);
+            dts[b] = __fmaf_rn(tfy[b], v - u, u) - ctr[b];
+        }
+        if (i >= NS) bar_sync<NT>(1 + NS + buf);  // consumers released this buffer
+        float* st = stage + (size_t)buf * lk_stage_elems<M>();
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int y = ybase + b;
+            const bool in = xin && y >= 0 && y < h && y < yend;
+            const float px = in ? gxs[b] * dts[b] : 0.f, py = in ? gys[b] * dts[b] : 0.f;
+            float2* rp = ring + (slot * IW + c);
+            const float2 o = *rp;
+            *rp = make_float2(px, py);
+            V0 = (V0 + px) - o.x;
+            V1 = (V1 + py) - o.y;
+            slot = slot + 1 == K ? 0 : slot + 1;
+            st[b * IWP + c] = V0;
+            st[NB * IWP + b * IWP + c] = V1;
+        }
+        bar_arrive<NT>(1 + buf);  // batch staged
+        if (more) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                tfx[b] = nfx[b];
+                tfy[b] = nfy[b];
+            }
+        }
+    }
+}
+
+// ---- consumer (fp32 later iterations): horizontal sums by row prefix sums -
+// Consumer warp b takes batch row b: an exclusive-scan of the row's 128
+// staged column sums (a float4 per lane, then a warp scan of the lane
+// totals), written back in place; output column j's (2r+1)-wide sum is then
+// P[j + 2r] - P[j - 1].  Lane l owns output columns l, l + 32, l + 64, l + 96,
+// so the flow / coefficient loads and the flow stores are coalesced.
+template <int M>
+__device__ __forceinline__ void lk_consume_scan(const LkArgs& a, const LkDir& D, float* stage,
+                                                int x0, int y0, int ystart, int yo_end,
+                                                int nbat) {
+    using Cfg = LkCfg<M>;
+    constexpr int NB = Cfg::NB, IW = Cfg::IW, NT = Cfg::THREADS, NS = Cfg::NS;
+    constexpr int CPL = IW / 32;  // staged columns per lane (consecutive)
+    static_assert(NB == 4 && NT == IW + 32 * NB && CPL % 4 == 0, "one consumer warp per row");
+    constexpr bool FIRST = M == LK_FIRST;
+    constexpr int IWP = lk_iwp<M>(), QS = NB * IWP;
+    const int r = a.r, w = a.w, tw = a.tw;
+    const int t = threadIdx.x - IW;
+    const int b = t >> 5, lane = t & 31;
+    const int nact = min(tw, w - x0);  // output columns of this tile
+    for (int i = 0; i < nbat; ++i) {
+        const int buf = i % NS;
+        const int yo = ystart + i * NB + b - r;
+        const bool rowact = yo >= y0 && yo < yo_end;  // warp-uniform
+        // lane's outputs: row yo, columns x0 + lane + 32 k (immediate offsets)
+        const size_t ro = (size_t)yo * w + x0 + lane;
+        const float2* __restrict__ fin = D.fin + ro;
+        const float4* __restrict__ cfp = D.coef + ro;
+        // CPL == 4: the row's flow / ok / coefficients prefetched before the wait
+        float2 pfo[4];
+        float4 pcf[4];
+        uint8_t pok[4];
+        if (CPL == 4 && rowact) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (lane + 32 * k < nact) {
+                    pfo[k] = fin[32 * k];
+                    pcf[k] = cfp[32 * k];
+                    if (FIRST) pok[k] = D.okin[ro + 32 * k];
+                }
+            }
+        }
+        bar_sync<NT>(1 + buf);
+        if (rowact) {
+            float* vb = stage + (size_t)buf * lk_stage_elems<M>() + b * IWP;
+            float H[2][CPL];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                float4 v[CPL / 4];
+#pragma unroll
+                for (int u = 0; u < CPL / 4; ++u)
+                    v[u] = *reinterpret_cast<const float4*>(vb + q * QS + CPL * lane + 4 * u);
+                float run = 0.f;
+#pragma unroll
+                for (int u = 0; u < CPL / 4; ++u) {
+                    v[u].x += run;
+                    v[u].y += v[u].x;
+                    v[u].z += v[u].y;
+                    v[u].w += v[u].z;
+                    run = v[u].w;
+                }
+                float s = run;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float n = __shfl_up_sync(0xffffffffu, s, o);
+                    if (lane >= o) s += n;
+                }
+                float ex = __shfl_up_sync(0xffffffffu, s, 1);
+                if (lane == 0) ex = 0.f;
+#pragma unroll
+                for (int u = 0; u < CPL / 4; ++u) {
+                    v[u].x += ex;
+                    v[u].y += ex;
+                    v[u].z += ex;
+                    v[u].w += ex;
+                    *reinterpret_cast<float4*>(vb + q * QS + CPL * lane + 4 * u) = v[u];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int j = lane + 32 * k;
+                    if (j < tw) {
+                        const float hi = vb[q * QS + j + 2 * r];
+                        H[q][k] = j > 0 ? hi - vb[q * QS + j - 1] : hi;
+                    }
+                }
+            }
+            // the outputs in groups of 4 columns: the group's flow / ok /
+            // coefficient loads in flight together, then solve and store
+#pragma unroll
+            for (int k0 = 0; k0 < CPL; k0 += 4) {
+                float2 fo[4];
+                float4 cf[4];
+                uint8_t okv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = lane + 32 * (k0 + k);
+                    if (CPL == 4) {
+                        fo[k] = pfo[k];
+                        cf[k] = pcf[k];
+                        okv[k] = pok[k];
+                    } else if (j < nact) {
+                        fo[k] = fin[j - lane];
+                        cf[k] = cfp[j - lane];
+                        if (FIRST) okv[k] = D.okin[ro + j - lane];
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = lane + 32 * (k0 + k);
+                    if (j >= nact) continue;
+                    const size_t oi = ro + (j - lane);
+                    float2 f = fo[k];
+                    if (FIRST) D.okout[oi] = (okv[k] || cf[k].w != 0.f) ? 1 : 0;
+                    if (cf[k].w != 0.f) {  // -(M^-1 b) in float
+                        const float bx = H[0][k0 + k], by = H[1][k0 + k];
+                        float ndx = f.x + -__fmaf_rn(cf[k].x, bx, -(cf[k].y * by));
+                        float ndy = f.y + -__fmaf_rn(cf[k].z, by, -(cf[k].y * bx));
+                        final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
+                        f = make_float2(ndx, ndy);
+                    }
+                    D.fout[oi] = f;
+                }
+            }
+        }
+        if (i + NS < nbat) bar_arrive<NT>(1 + NS + buf);  // buffer free for batch i + NS
     }
 }
 
 // ---- consumer: horizontal sums, solve, update, next It ---------------------
 template <int M>
-__device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, const double* stage,
-                                           int x0, int y0, int ystart, int yo_end, int nbat) {
+__device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D,
+                                           const typename LkCfg<M>::Acc* stage, int x0, int y0,
+                                           int ystart, int yo_end, int nbat) {
     using Cfg = LkCfg<M>;
+    using Acc = typename Cfg::Acc;
     constexpr int NB = Cfg::NB, NQ = Cfg::NQ, S = Cfg::S;
     constexpr bool FULL = Cfg::FULL, TENSOR = M == LK_TENSOR, FIRST = M == LK_FIRST;
     const int r = a.r, w = a.w;
-    const int IWP = lk_iwp(LK_IW);
+    constexpr int IWP = lk_iwp<M>();
     const int nruns = (a.tw + S - 1) / S;
-    const int t = threadIdx.x - LK_IW;
+    constexpr int NT = Cfg::THREADS;
+    const int t = threadIdx.x - Cfg::IW;
     const int b = t % NB, run = t / NB;  // NB * nruns <= 128 by construction
     const int cs = run * S;
     for (int i = 0; i < nbat; ++i) {
@@ -384,11 +722,11 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                 if (!FULL) cf[o] = D.coef[oi];
             }
         }
-        bar_sync(1 + buf);
+        bar_sync<NT>(1 + buf);
         if (active) {
-            const double* vb = stage + (size_t)buf * lk_stage_doubles<M>() + b * IWP + cs;
+            const Acc* vb = stage + (size_t)buf * lk_stage_elems<M>() + b * IWP + cs;
             const int QS = NB * IWP;  // plane stride
-            double s[NQ], s2[NQ];
+            Acc s[NQ], s2[NQ];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) s[q] = s2[q] = 0.0;
             int k = 0;
@@ -405,7 +743,7 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
             }
 #pragma unroll
             for (int q = 0; q < NQ; ++q) s[q] += s2[q];
-            const double* va = vb + 2 * r;  // column entering the window at o
+            const Acc* va = vb + 2 * r;  // column entering the window at o
 #pragma unroll
             for (int o = 0; o < S; ++o) {
                 if (o >= nout) break;
@@ -440,10 +778,18 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                     D.okout[oi] = ok;
                     if (D.coef) D.coef[oi] = coef;
                 } else if (cf[o].w != 0.f) {
-                    const double bx = s[0], by = s[1];
-                    const double ux = -((double)cf[o].x * bx - (double)cf[o].y * by);
-                    const double uy = -((double)cf[o].z * by - (double)cf[o].y * bx);
-                    float ndx = f.x + (float)ux, ndy = f.y + (float)uy;
+                    float ndx, ndy;
+                    if (Cfg::F32) {  // -(M^-1 b) in float
+                        const float bx = s[0], by = s[1];
+                        ndx = f.x + -__fmaf_rn(cf[o].x, bx, -(cf[o].y * by));
+                        ndy = f.y + -__fmaf_rn(cf[o].z, by, -(cf[o].y * bx));
+                    } else {
+                        const double bx = s[0], by = s[1];
+                        const double ux = -((double)cf[o].x * bx - (double)cf[o].y * by);
+                        const double uy = -((double)cf[o].z * by - (double)cf[o].y * bx);
+                        ndx = f.x + (float)ux;
+                        ndy = f.y + (float)uy;
+                    }
                     final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
                     f = make_float2(ndx, ndy);
                 }
@@ -451,22 +797,30 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D, cons
                 D.fout[oi] = f;
             }
         }
-        if (i + 2 < nbat) bar_arrive(3 + buf);  // buffer free for batch i + 2
+        if (i + 2 < nbat) bar_arrive<NT>(3 + buf);  // buffer free for batch i + 2
     }
 }
 
 template <int M>
-__global__ void __launch_bounds__(LK_THREADS, LkCfg<M>::MINB) k_lk_sweep(LkArgs a) {
+__global__ void __launch_bounds__(LkCfg<M>::THREADS, LkCfg<M>::MINB) k_lk_sweep(LkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     void* ring = smem;
-    double* stage = reinterpret_cast<double*>(smem + lk_ring_bytes<M>(a.r));
+    auto* stage = reinterpret_cast<typename LkCfg<M>::Acc*>(smem + lk_ring_bytes<M>(a.r));
     const LkDir& D = a.d[blockIdx.z];
     const int x0 = blockIdx.x * a.tw, y0 = blockIdx.y * a.th;
     const int yo_end = min(y0 + a.th, a.h);
     const int ystart = y0 - a.r;
     const int yend = yo_end + a.r;
     const int nbat = (yend - ystart + LkCfg<M>::NB - 1) / LkCfg<M>::NB;
-    if (threadIdx.x < LK_IW)
+    if constexpr (LkCfg<M>::F32) {
+        float* tapb = reinterpret_cast<float*>(smem + lk_ring_bytes<M>(a.r) +
+                                               LkCfg<M>::NS * lk_stage_elems<M>() * sizeof(float));
+        if (threadIdx.x < LkCfg<M>::IW)
+            lk_produce_f32<M>(a, D, static_cast<float2*>(ring), stage, tapb, x0, ystart, yend,
+                              nbat);
+        else
+            lk_consume_scan<M>(a, D, stage, x0, y0, ystart, yo_end, nbat);
+    } else if (threadIdx.x < LkCfg<M>::IW)
         lk_produce<M>(a, D, ring, stage, x0, ystart, yend, nbat);
     else
         lk_consume<M>(a, D, stage, x0, y0, ystart, yo_end, nbat);
@@ -506,10 +860,9 @@ void lk_init() {
 #ifndef LK_TH_MIN
 #define LK_TH_MIN 16  // smallest tile height (smaller: faster alone, slower in the DAG)
 #endif
-int lk_tile_rows(int w, int h, int r, int ndir, int per_sm) {
+static int lk_tile_rows(int w, int h, int r, int ndir, int per_sm, int tw) {
     // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x per_sm.  Pick th
     // minimising waves x rows per CTA (wave quantisation vs. halo rows).
-    const int tw = LK_IW - 2 * r;
     const long cols = (w + tw - 1) / tw;
     const long slots = 148L * per_sm;
     int best = LK_TH_MIN;
@@ -537,14 +890,14 @@ cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
 
 template <int M>
 static void sweep_launch(LkArgs a, cudaStream_t s) {
-    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB);
+    a.tw = LkCfg<M>::IW - 2 * a.r;
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB, a.tw);
     dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
-    k_lk_sweep<M><<<g, LK_THREADS, lk_smem_bytes<M>(a.r), s>>>(a);
+    k_lk_sweep<M><<<g, LkCfg<M>::THREADS, lk_smem_bytes<M>(a.r), s>>>(a);
 }
 
 cudaError_t lk_sweep(const LkArgs& a0, int mode, cudaStream_t s) {
     LkArgs a = a0;
-    a.tw = LK_IW - 2 * a.r;
     lk_init();
     switch (mode) {
         case LK_FULL: sweep_launch<LK_FULL>(a, s); break;
