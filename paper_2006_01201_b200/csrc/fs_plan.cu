@@ -20,7 +20,7 @@ constexpr size_t kMaxStamps = 512;
 
 // LK structure tensors off the coarse-to-fine chain (FlowWS split schedule)
 #ifndef FS_LK_SPLIT
-#define FS_LK_SPLIT 0  // measured: C2 4.28 -> 4.45 ms device, C4 e2e 14.5 -> 14.2 ms
+#define FS_LK_SPLIT 1  // the level tensors off the chain (TENSOR), then fp32 FIRST + ITER
 #endif
 constexpr bool kLkSplit = FS_LK_SPLIT != 0;
 
@@ -315,7 +315,9 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             launch::snapshot_count(f.st, p->cc, s);
             launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr,
                                                   nullptr, nullptr, nullptr, true,
-                                                  kLkSplit ? s : nullptr);
+                                                  // (the legacy stream's non-null handle
+                                                  // when s is the default stream)
+                                                  kLkSplit ? (s ? s : cudaStreamLegacy) : nullptr);
             launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
         }
         {
