@@ -259,6 +259,10 @@ void stamp(unsigned long long* slot, cudaStream_t);  // %globaltimer (ns) into *
 // RGB8 host formats: n RGB8 pixels -> RGBA8 (alpha 255); canvas rect -> RGB8
 // (canvas-indexed: out + 3 * (y * cw + x)); `in` of expand_rgb 4-byte aligned
 void expand_rgb(const uint8_t* in, uchar4* out, size_t n, cudaStream_t);
+// rectangle r (view-local) of a w-wide RGB8 image -> RGBA8 (alpha 255)
+void expand_rgb_rect(const uint8_t* in, uchar4* out, int w, const Rect& r, cudaStream_t);
+// alpha of n RGBA8 pixels := 255 (RGB kept)
+void set_alpha(uchar4* px, size_t n, cudaStream_t);
 void pack_rgb(const uchar4* in, int cw, const Rect& r, uint8_t* out, cudaStream_t);
 // fs_remap.cu: overlap channel sums of view k against its first covering views
 void chroma_sums(const uint8_t* owner, int cw, const ViewU8& vk, const PanoViews& pv, int k,

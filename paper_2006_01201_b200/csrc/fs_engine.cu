@@ -413,7 +413,8 @@ template <class V, class P, class PC>
 int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const V& view, int ch,
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1, cudaStream_t es, cudaEvent_t ev_fork,
-                          cudaEvent_t ev_join, bool with_edt, cudaStream_t ts) {
+                          cudaEvent_t ev_join, bool with_edt, cudaStream_t ts,
+                          cudaEvent_t ev_data) {
     int launches = 0;
     // the distance transforms need only the masks and the fold's counts: with
     // a second stream they run concurrently with the flow
@@ -424,6 +425,7 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
         FS_CK(cudaStreamWaitEvent(es, ev_fork, 0));
         se = es;
     }
+    if (ev_data) FS_CK(cudaStreamWaitEvent(s, ev_data, 0));  // the crop's pixels landed
     launch::check_box(f.st, f.box, s);
     {
         // pano rgb 16 + valid 1 + view 4 in, two gray planes 8 out
@@ -515,19 +517,19 @@ template int fold_enqueue_pre<ViewF4, PanoPlane>(FoldWS<ViewF4>&, const PanoPlan
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoViews>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoViews&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t, cudaEvent_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoViews, PanoHybrid>(
     FoldWS<ViewU8>&, const PanoViews&, const PanoHybrid&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t, cudaEvent_t);
 template int fold_enqueue_flow_edt<ViewU8, PanoPlane, PanoPlane>(
     FoldWS<ViewU8>&, const PanoPlane&, const PanoPlane&, const ViewU8&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t, cudaEvent_t);
 template int fold_enqueue_flow_edt<ViewF4, PanoPlane, PanoPlane>(
     FoldWS<ViewF4>&, const PanoPlane&, const PanoPlane&, const ViewF4&, int,
     const fs_flow_params&, cudaStream_t, cudaEvent_t, cudaEvent_t, cudaStream_t,
-    cudaEvent_t, cudaEvent_t, bool, cudaStream_t);
+    cudaEvent_t, cudaEvent_t, bool, cudaStream_t, cudaEvent_t);
 template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoViews&, const ViewU8&,
                                                  cudaStream_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,

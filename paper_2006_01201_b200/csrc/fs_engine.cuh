@@ -139,7 +139,8 @@ int fold_enqueue_flow_edt(FoldWS<V>& f, const P& pano, const PC& crop_src, const
                           const fs_flow_params& fp, cudaStream_t s, cudaEvent_t ev_flow0,
                           cudaEvent_t ev_flow1, cudaStream_t es = nullptr,
                           cudaEvent_t ev_fork = nullptr, cudaEvent_t ev_join = nullptr,
-                          bool with_edt = true, cudaStream_t ts = nullptr);
+                          bool with_edt = true, cudaStream_t ts = nullptr,
+                          cudaEvent_t ev_data = nullptr);  // s waits for it before the crop
 template <class V, class P>
 int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s);
 // Code 1 blend on Area3 + composition of the view onto the canvas

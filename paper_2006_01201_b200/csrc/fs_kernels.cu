@@ -1171,6 +1171,26 @@ __global__ void __launch_bounds__(256) k_pack_rgb(const uchar4* __restrict__ in,
         }
     }
 }
+__global__ void __launch_bounds__(256) k_expand_rgb_rect(const uint8_t* __restrict__ in,
+                                                         uchar4* __restrict__ out, int w, Rect r) {
+    const int x = r.x0 + blockIdx.x * 64 + (threadIdx.x & 63);
+    const int y = r.y0 + blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (x >= r.x1() || y >= r.y1()) return;
+    const size_t i = (size_t)y * w + x;
+    out[i] = make_uchar4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 255);
+}
+__global__ void __launch_bounds__(256) k_set_alpha(uchar4* __restrict__ px, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        px[i].w = 255;
+}
+void expand_rgb_rect(const uint8_t* in, uchar4* out, int w, const Rect& r, cudaStream_t s) {
+    if (r.w > 0 && r.h > 0)
+        k_expand_rgb_rect<<<dim3((r.w + 63) / 64, (r.h + 3) / 4), 256, 0, s>>>(in, out, w, r);
+}
+void set_alpha(uchar4* px, size_t n, cudaStream_t s) {
+    if (n) k_set_alpha<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(px, n);
+}
 void expand_rgb(const uint8_t* in, uchar4* out, size_t n, cudaStream_t s) {
     if (n) k_expand_rgb<<<(unsigned)((n / 4 + 1 + 255) / 256), 256, 0, s>>>(in, out, n);
 }

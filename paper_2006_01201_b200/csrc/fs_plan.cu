@@ -23,6 +23,14 @@ constexpr size_t kMaxStamps = 512;
 #define FS_LK_SPLIT 1  // the level tensors off the chain (TENSOR), then fp32 FIRST + ITER
 #endif
 constexpr bool kLkSplit = FS_LK_SPLIT != 0;
+// RGB8 upload order: whole views in fold order (default), or every fold's
+// Area3 box parts first (pitched copies), then the rest.  Measured C2 e2e:
+// boxes first 5.81 ms vs whole views 4.97 ms (the pitched copies run at
+// ~36 GB/s, and the first-cover read-backs wait for the late "rest" chunks).
+#ifndef FS_UPLOAD_BOXES
+#define FS_UPLOAD_BOXES 0
+#endif
+constexpr bool kUploadBoxesFirst = FS_UPLOAD_BOXES != 0;
 
 // first-cover copies a sharded rank keeps around each own fold's Area3 box:
 // a blend tap farther out is refused (ReachCheck) and the panorama runs unsharded
@@ -92,6 +100,20 @@ struct fs_plan_s {
     // host formats (fs_plan_set_host_format): RGB8 views are expanded on
     // arrival, the canvas packed to RGB8 before its read-backs
     int hv_ch = 4, ho_ch = 4;
+    // RGB8 views (every pixel valid, alpha preset to 255 on the device) cross
+    // PCIe in chunks ordered by need: first each fold's Area3 box parts of the
+    // views it crops (fold order), then the rest of every view (view order).
+    // Validity needs no data, so claims, partitions and distance transforms
+    // start at once; a fold's crop waits for its box chunks only.
+    struct Chunk {
+        int view;
+        Rect r;  // canvas coordinates
+    };
+    std::vector<Chunk> chunks;
+    std::vector<int> crop_chunk;  // per fold: last chunk its crop reads (-1: none)
+    std::vector<int> done_chunk;  // per view k: last chunk of views 0..k
+    std::vector<cudaEvent_t> ev_chunk, ev_copied;  // expanded / landed
+    cudaStream_t xst = nullptr;  // expands chunks as they land (the copy engine never waits)
     uint8_t* stage_in = nullptr;   // RGB8 views, 4-byte aligned each
     std::vector<size_t> stage_off;
     uint8_t* stage_out = nullptr;  // RGB8 canvas
@@ -146,6 +168,7 @@ Rect rect_union(const Rect& a, const Rect& b) {
     int x1 = std::max(a.x1(), b.x1()), y1 = std::max(a.y1(), b.y1());
     return Rect{x0, y0, x1 - x0, y1 - y0};
 }
+bool rects_meet(const Rect& a, const Rect& b);
 Rect rect_inter(const Rect& a, const Rect& b) {
     int x0 = std::max(a.x0, b.x0), y0 = std::max(a.y0, b.y0);
     int x1 = std::min(a.x1(), b.x1()), y1 = std::min(a.y1(), b.y1());
@@ -174,6 +197,73 @@ void upload_view(fs_plan_s* p, int k, const uint8_t* src, cudaStream_t st) {
     FS_CK(cudaMemcpyAsync(stg, src, np * 3, cudaMemcpyDefault, st));
     launch::expand_rgb(stg, p->views[k], np, st);
 }
+// Part of an RGB8 view (canvas rectangle r inside view k) host -> device:
+// a pitched copy into the view's staging image on st; expand_chunk turns it
+// into RGBA8 (on another stream, so the copies run back to back).
+void expand_chunk(fs_plan_s* p, int k, const Rect& r, cudaStream_t st) {
+    const Rect& v = p->rects[k];
+    launch::expand_rgb_rect(p->stage_in + p->stage_off[k], p->views[k], v.w,
+                            Rect{r.x0 - v.x0, r.y0 - v.y0, r.w, r.h}, st);
+}
+void upload_chunk(fs_plan_s* p, int k, const Rect& r, const uint8_t* src, cudaStream_t st) {
+    const Rect& v = p->rects[k];
+    const Rect l{r.x0 - v.x0, r.y0 - v.y0, r.w, r.h};
+    const size_t pitch = (size_t)v.w * 3, off = ((size_t)l.y0 * v.w + l.x0) * 3;
+    uint8_t* stg = p->stage_in + p->stage_off[k];
+    if (l.w == v.w)
+        FS_CK(cudaMemcpyAsync(stg + off, src + off, pitch * l.h, cudaMemcpyDefault, st));
+    else
+        FS_CK(cudaMemcpy2DAsync(stg + off, pitch, src + off, pitch, (size_t)l.w * 3, l.h,
+                                cudaMemcpyDefault, st));
+}
+// The chunk order of the RGB8 upload (fs_plan_s::chunks).
+void plan_chunks(fs_plan_s* p) {
+    const int n = p->n;
+    std::vector<std::vector<Rect>> rem(n);
+    for (int m = 0; m < n; ++m) rem[m] = {p->rects[m]};
+    p->chunks.clear();
+    auto carve = [&](int m, const Rect& x) {  // move rem[m] ∩ x into chunks
+        std::vector<Rect> keep;
+        for (const Rect& r : rem[m]) {
+            const Rect i = rect_inter(r, x);
+            if (i.w <= 0 || i.h <= 0) {
+                keep.push_back(r);
+                continue;
+            }
+            p->chunks.push_back({m, i});
+            if (i.y0 > r.y0) keep.push_back({r.x0, r.y0, r.w, i.y0 - r.y0});
+            if (i.y1() < r.y1()) keep.push_back({r.x0, i.y1(), r.w, r.y1() - i.y1()});
+            if (i.x0 > r.x0) keep.push_back({r.x0, i.y0, i.x0 - r.x0, i.h});
+            if (i.x1() < r.x1()) keep.push_back({i.x1(), i.y0, r.x1() - i.x1(), i.h});
+        }
+        rem[m] = keep;
+    };
+    if (kUploadBoxesFirst)
+        for (int k = 1; k < n; ++k)
+            for (int m = k; m >= 0; --m) carve(m, p->boxes[k]);
+    for (int m = 0; m < n; ++m)
+        for (const Rect& r : rem[m])
+            if (r.w > 0 && r.h > 0) p->chunks.push_back({m, r});
+    const int nc = (int)p->chunks.size();
+    p->crop_chunk.assign(n, -1);
+    p->done_chunk.assign(n, -1);
+    for (int i = 0; i < nc; ++i) {
+        const auto& c = p->chunks[i];
+        for (int k = std::max(1, c.view); k < n; ++k)
+            if (rects_meet(c.r, p->boxes[k])) p->crop_chunk[k] = std::max(p->crop_chunk[k], i);
+        for (int k = c.view; k < n; ++k) p->done_chunk[k] = std::max(p->done_chunk[k], i);
+    }
+    for (auto e : p->ev_chunk) cudaEventDestroy(e);
+    for (auto e : p->ev_copied) cudaEventDestroy(e);
+    p->ev_chunk.assign(nc, nullptr);
+    p->ev_copied.assign(nc, nullptr);
+    for (int i = 0; i < nc; ++i) {
+        FS_CK(cudaEventCreateWithFlags(&p->ev_chunk[i], cudaEventDisableTiming));
+        FS_CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
+    }
+    if (!p->xst) FS_CK(cudaStreamCreateWithFlags(&p->xst, cudaStreamNonBlocking));
+}
+
 // A canvas rectangle device -> host in the plan's host format.
 void download_rect(fs_plan_s* p, const Rect& r, uint8_t* dst, cudaStream_t st) {
     const int c = p->ho_ch;
@@ -275,6 +365,17 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     const PanoPlane plane{p->cv.valid, p->cv.rgb, p->cv.w};
     const bool hin = io && io->views, hout = io && io->out;
     const bool hfill = dag && hout && !p->empty_rects.empty();
+    // RGB8 views in chunks (validity needs no data): ev_view[k] = views 0..k
+    // complete, ev_crop[k] = fold k's crop inputs in
+    const bool chunked = dag && hin && p->hv_ch == 3 && !p->chunks.empty();
+    std::vector<cudaEvent_t> ev_view(p->n, nullptr), ev_crop(p->n, nullptr);
+    if (hin) {
+        for (int k = 0; k < p->n; ++k) {
+            ev_view[k] = chunked ? p->ev_chunk[p->done_chunk[k]] : p->ev_h2d[k];
+            ev_crop[k] = chunked ? (p->crop_chunk[k] >= 0 ? p->ev_chunk[p->crop_chunk[k]] : nullptr)
+                                 : p->ev_h2d[k];
+        }
+    }
     if (dag) {
         FS_CK(cudaEventRecord(p->ev_start, s));
         if (hfill) {  // uncovered canvas: zeroed by the host, concurrently
@@ -285,10 +386,26 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         }
         if (hin) {
             FS_CK(cudaStreamWaitEvent(p->h2d, p->ev_start, 0));
-            for (int k = 0; k < p->n; ++k) {
-                upload_view(p, k, io->views[k], p->h2d);
-                mark("h2d_" + std::to_string(k), p->h2d);
-                FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
+            if (chunked) {
+                int next = 0;  // next view whose completion to mark
+                FS_CK(cudaStreamWaitEvent(p->xst, p->ev_start, 0));
+                for (int i = 0; i < (int)p->chunks.size(); ++i) {
+                    const auto& c = p->chunks[i];
+                    upload_chunk(p, c.view, c.r, io->views[c.view], p->h2d);
+                    FS_CK(cudaEventRecord(p->ev_copied[i], p->h2d));
+                    FS_CK(cudaStreamWaitEvent(p->xst, p->ev_copied[i], 0));
+                    expand_chunk(p, c.view, c.r, p->xst);
+                    FS_CK(cudaEventRecord(p->ev_chunk[i], p->xst));
+                    while (next < p->n && p->done_chunk[next] == i)
+                        mark("h2d_" + std::to_string(next++), p->xst);
+                }
+                FS_CK(cudaEventRecord(p->ev_h2d[p->n - 1], p->xst));  // joined at the end
+            } else {
+                for (int k = 0; k < p->n; ++k) {
+                    upload_view(p, k, io->views[k], p->h2d);
+                    mark("h2d_" + std::to_string(k), p->h2d);
+                    FS_CK(cudaEventRecord(p->ev_h2d[k], p->h2d));
+                }
             }
         }
     }
@@ -297,7 +414,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
     }
     init_count(p->cc, s);
-    if (hin) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[0], 0));
+    if (hin) FS_CK(cudaStreamWaitEvent(s, ev_view[0], 0));
     if (dag) {
         FS_CK(cudaMemsetAsync(p->out, 0, (size_t)p->cw * p->chh * 4, s));
         FS_CK(cudaEventRecord(p->ev_clear, s));
@@ -337,7 +454,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     // the counts of views < k (no chain through the earlier folds' partitions)
     FS_CK(cudaMemsetAsync(p->hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->own));
     for (int k = 0; k < p->n; ++k) {
-        if (hin) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
+        if (hin && !chunked) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
         launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own, p->hist);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_own[k], p->own));
@@ -371,7 +488,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FoldWS<ViewU8>& f = p->folds[k - 1];
         ViewU8 v = view_of(p, k);
         cudaStream_t b = p->branch[k - 1];
-        FS_CK(cudaStreamWaitEvent(b, hin ? p->ev_h2d[k] : p->ev_start, 0));
+        FS_CK(cudaStreamWaitEvent(b, hin && !chunked ? p->ev_h2d[k] : p->ev_start, 0));
         FS_CK(cudaStreamWaitEvent(b, p->ev_own[k - 1], 0));  // views < k claimed
         const PanoViews pv = views_before(p, k);
         const std::string fk = std::to_string(k);
@@ -386,15 +503,17 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         cudaStream_t a2s = es;  // (on the branch: C2 0.5% slower)
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_own[k], 0));
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_clear, 0));
+        if (chunked) FS_CK(cudaStreamWaitEvent(a2s, ev_view[k], 0));  // view k's pixels
         launch::compose_area2(p->cv, v, p->owner, k, a2s, p->out);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_a2[k], a2s));
         if (p->tl_stamp && p->crop_wait[k] == 0) mark("fold" + fk + "_flow_start", b);
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
+        cudaEvent_t crop_in = chunked ? ev_crop[k] : nullptr;
         if (p->crop_wait[k] == 0) {
             launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1, es,
                                               p->ev_efork[k], p->ev_ejoin[k], true,
-                                              p->tensor_stream[k - 1]);
+                                              p->tensor_stream[k - 1], crop_in);
         } else {  // blended pixels inside the box: after that fold's compose
             // (the distance transforms need only the masks: fork them first)
             FS_CK(cudaEventRecord(p->ev_efork[k], b));
@@ -402,6 +521,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             launches += fold_enqueue_edt(f, pv, v, es);
             FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
             FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
+            if (crop_in) FS_CK(cudaStreamWaitEvent(b, crop_in, 0));
             if (p->tl_stamp) mark("fold" + fk + "_flow_start", b);
             launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1,
                                               nullptr, nullptr, nullptr, false,
@@ -411,6 +531,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         mark("fold" + fk + "_edt_end", b);
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
+        if (chunked) FS_CK(cudaStreamWaitEvent(s, ev_view[k], 0));  // L taps anywhere in views <= k
         mark("fold" + fk + "_blend_start", s);
         launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
@@ -429,6 +550,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     FS_CK(cudaEventRecord(p->ev_out_early, p->d2h_early));
     FS_CK(cudaStreamWaitEvent(s, p->ev_out_early, 0));
     if (hfill) FS_CK(cudaStreamWaitEvent(s, p->ev_hfill1, 0));
+    if (chunked) FS_CK(cudaStreamWaitEvent(s, p->ev_h2d[p->n - 1], 0));
     mark("end", s);
     FS_CK(cudaGetLastError());
     return launches;
@@ -1152,6 +1274,13 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
         }
         if (out_channels == 3 && !p->stage_out)
             FS_CK(cudaMalloc(&p->stage_out, (size_t)p->cw * p->chh * 3 + 16));
+        if (view_channels == 3 && p->hv_ch != 3) {
+            // RGB8 views: every pixel valid, alpha 255 before any data lands
+            for (int k = 0; k < p->n; ++k)
+                launch::set_alpha(p->views[k], (size_t)p->rects[k].w * p->rects[k].h, nullptr);
+            FS_CK(cudaDeviceSynchronize());
+            if (p->dag) plan_chunks(p);
+        }
         p->hv_ch = view_channels;
         p->ho_ch = out_channels;
         // the graphs holding host copies were captured for the old formats
@@ -1547,6 +1676,9 @@ void fs_plan_destroy(fs_plan p) {
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_compose)
         if (e) cudaEventDestroy(e);
+    for (auto e : p->ev_chunk) cudaEventDestroy(e);
+    for (auto e : p->ev_copied) cudaEventDestroy(e);
+    if (p->xst) cudaStreamDestroy(p->xst);
     for (auto e : p->ev_h2d)
         if (e) cudaEventDestroy(e);
     for (auto e : p->ev_own)
