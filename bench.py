@@ -49,6 +49,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-len", type=int, default=0,
+                    help="row/column flow tiles of about this length along each fold's long "
+                         "axis (fs_plan_set_tiling; 0: untiled)")
     ap.add_argument("--shard", choices=["auto", "none", "seams"], default="auto",
                     help="seams: ONE panorama whose overlap pairs are sharded over the GPUs "
                          "(strong scaling, strips gathered to rank 0 over NCCL P2P); "
@@ -360,6 +363,8 @@ def main():
     lay = make_layout(args.config, 0 if sharded else rank)
     params = fs.FlowParams(levels=lay.levels)
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, params, device=local)
+    if args.tile_len:
+        plan.set_tiling(args.tile_len)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     sp = None

@@ -185,3 +185,22 @@ def small_panorama(seed: int = 0, parallax: int = 4) -> Layout:
     views.append(rgba(scene[300:400, 0:W]))
     offs.append((0, 300))
     return Layout("C2/10 900x400 panorama", W, H, views, offs, 3)
+
+
+def tile_panorama(seed: int = 0, parallax: int = 6) -> Layout:
+    """C2's geometry at 2048x800 (levels 4): 4 views 620x560 at y = 120 and
+    two 2048x200 bands whose 2048x80 Area3 boxes cross every seam — the layout
+    the row/column flow tiles (fs_plan_set_tiling) are tested on."""
+    W, H = 2048, 800
+    xs = [0, 476, 952, 1428]
+    scene = rgb_scene(H, W + parallax * len(xs), seed)
+    views, offs = [], []
+    for k, x in enumerate(xs):
+        c0 = x + parallax * k
+        views.append(rgba(scene[120:680, c0:c0 + 620]))
+        offs.append((x, 120))
+    views.append(rgba(scene[0:200, 0:W]))
+    offs.append((0, 0))
+    views.append(rgba(scene[600:800, 0:W]))
+    offs.append((0, 600))
+    return Layout("C2 geometry 2048x800 (tile tests)", W, H, views, offs, 4)

@@ -252,6 +252,22 @@ fs_status fs_plan_set_host_format(fs_plan plan, int view_channels, int out_chann
 /* bytes fs_plan_execute_host moves with page-locked buffers: views in, and
  * the canvas read back (rectangles no view covers are zeroed on the host) */
 fs_status fs_plan_transfer_bytes(fs_plan plan, size_t* h2d, size_t* d2h);
+/* Row/column tiles of the folds' flows (the reference has
+ * no tiling — its dense_pyr_lk, src/flow.cpp:194-314, runs over a whole crop):
+ * every fold whose Area3 box is longer than tile_len along its long axis is
+ * cut there into interiors of about tile_len, each computed as its own crop
+ * + pyramid + LK over the interior grown by the whole dependency cone (so the
+ * interior's flow equals the untiled one), the crop waiting only for the
+ * earlier composes its region meets; gathers are certified on the device to
+ * stay `margin` px inside the tile pyramid's exact part, else the fold runs
+ * untiled (fs_plan_check, then execute again).  Boxes whose long side is not
+ * divisible by 2^(levels-1) stay untiled.  tile_len = 0: no tiles (default).
+ * Needs the DAG schedule (<= 16 views). */
+fs_status fs_plan_set_tiling(fs_plan plan, int tile_len, int margin);
+/* tiles of fold k in use (0: untiled, -1: bad argument); region / interior
+ * {x0, y0, w, h} box-relative (either may be NULL) */
+int fs_plan_tile_count(fs_plan plan, int k);
+fs_status fs_plan_tile_info(fs_plan plan, int k, int t, int* region, int* interior);
 /* fold geometry: for fold k (1..n-1) the Area3 box {x0,y0,w,h} and depth */
 fs_status fs_plan_fold_info(fs_plan plan, int k, int* box, int* depth);
 /* fold k's crop flows of the last execution (the FlowFields bidirectional_flow

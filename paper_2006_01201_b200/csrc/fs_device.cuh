@@ -147,6 +147,7 @@ struct FoldStats {
     unsigned int edt_fail;    // bounded-domain EDT certificate failed (bit per mask)
     unsigned int box_mismatch;
     unsigned int reach_fail;  // a blend tap read a canvas pixel this rank does not hold final
+    unsigned int tile_fail;   // a flow tile's gather left its exact pyramid part
 };
 
 // Seam-sharded execution (fs_plan_shard): a fold runs on a GPU whose canvas
@@ -194,6 +195,12 @@ struct LkArgs {
     int tw, th;  // output tile (th <= 0: chosen per level)
     double eig_thresh;
     float flow_cap;
+    // row/column tiles (FlowTile): the taps of the pixels whose coordinate
+    // along cert_axis lies in [zlo, zhi) must stay inside [exlo, exhi), the
+    // part of the tile's pyramid equal to the whole crop's; else *cert_fail
+    // is set (nullptr: no check)
+    unsigned int* cert_fail;
+    int cert_axis, zlo, zhi, exlo, exhi;
 };
 
 struct SmoothArgs {

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "fs_engine.cuh"
@@ -134,6 +135,122 @@ void FlowWS::layout(Arena& a, int w_, int h_, int levels, int ndir_) {
     }
 }
 
+// ---- row/column tiles ------------------------------------------------------
+// The dependency cone, walked back from the interior: at level l the
+// smoothing passes (1 px each), then every iteration (its outputs need the
+// flow and the gathered taps of the pixels within r), then the 2x upsample
+// (align-centres bilinear + nearest ever_ok, src/flow.cpp:138-170) into level
+// l + 1.  A cut edge of the region clamps the tile's pyramid: level l + 1's
+// 5-tap downsample (src/flow.cpp:29-56) reads level l within 2 px, so the
+// clamped border grows to c_{l+1} = ceil((c_l + 2) / 2) px; everything the
+// interior depends on must stay `m` px inside it (m: room for the taps,
+// certified on the device).
+static bool tile_certs(int r0, int r1, int i0, int i1, int len, int depth,
+                       const fs_flow_params& p, int margin, std::vector<TileCert>& cert) {
+    const int R = r1 - r0, N = p.iterations_per_level, r = p.window_radius;
+    const bool cut_lo = r0 > 0, cut_hi = r1 < len;
+    cert.assign((size_t)depth * N, TileCert{});
+    int lo = i0 - r0, hi = i1 - r0, c = 0;
+    for (int l = 0; l < depth; ++l) {
+        const int n = R >> l;
+        // the exact part; a true crop edge clamps like the untiled crop: no bound
+        const int exlo = cut_lo ? c : -(1 << 29), exhi = cut_hi ? n - c : (1 << 29);
+        const int m = std::max(1, (margin + (1 << l) - 1) >> l);
+        lo -= p.smoothing_passes;
+        hi += p.smoothing_passes;
+        for (int it = N - 1; it >= 0; --it) {
+            int zl = lo - r, zh = hi + r;
+            if (cut_lo ? zl < exlo + m : false) return false;
+            if (cut_hi ? zh > exhi - m : false) return false;
+            zl = std::max(zl, 0);
+            zh = std::min(zh, n);
+            cert[(size_t)l * N + it] = TileCert{zl, zh, exlo, exhi};
+            lo = zl;
+            hi = zh;
+        }
+        if (l + 1 < depth) {  // fine u -> coarse (u + 0.5) * 0.5 - 0.5, bilinear + nearest
+            lo = std::max(0, (int)std::floor(lo * 0.5 - 0.25));
+            hi = std::min(n >> 1, (int)std::floor((hi - 1) * 0.5 - 0.25) + 2);
+            c = (c + 3) / 2;
+        }
+    }
+    return true;
+}
+
+bool plan_flow_tiles(int w, int h, int axis, int tile_len, int margin, const fs_flow_params& p,
+                     std::vector<FlowTile>& tiles) {
+    tiles.clear();
+    const int len = axis ? h : w;
+    const int depth = pyramid_depth(w, h, p.levels);
+    const int align = 1 << (depth - 1);
+    if (tile_len <= 0 || len % align || len <= tile_len) return false;
+    const int nt = (len + tile_len - 1) / tile_len;
+    std::vector<int> cuts{0};
+    for (int t = 1; t < nt; ++t) {
+        const int c = (int)((long long)len * t / nt) / align * align;
+        if (c > cuts.back()) cuts.push_back(c);
+    }
+    cuts.push_back(len);
+    if (cuts.size() < 3) return false;
+    for (size_t t = 0; t + 1 < cuts.size(); ++t) {
+        FlowTile ft;
+        ft.axis = axis;
+        const int i0 = cuts[t], i1 = cuts[t + 1];
+        std::vector<TileCert> cert;
+        bool ok = false;
+        int r0 = 0, r1 = len;
+        for (int H = align; !ok; H += align) {
+            r0 = std::max(0, i0 - H);
+            r1 = std::min(len, i1 + H);
+            ok = tile_certs(r0, r1, i0, i1, len, depth, p, margin, cert);
+            if (!ok && r0 == 0 && r1 == len) break;
+        }
+        const int rw = axis ? w : r1 - r0, rh = axis ? r1 - r0 : h;
+        if (!ok || pyramid_depth(rw, rh, p.levels) != depth) {
+            tiles.clear();
+            return false;
+        }
+        // test hook (tests/test_gpu_tiles.py): FS_TILE_CERT_SHRINK=k narrows
+        // every certified exact part by k px after planning, so the device
+        // certificate must refuse the tiles
+        if (const char* sh = getenv("FS_TILE_CERT_SHRINK")) {
+            const int k = atoi(sh);
+            for (TileCert& c : cert) {
+                c.exlo += k;
+                c.exhi -= k;
+            }
+        }
+        ft.region = axis ? Rect{0, r0, w, r1 - r0} : Rect{r0, 0, r1 - r0, h};
+        ft.interior = axis ? Rect{0, i0, w, i1 - i0} : Rect{i0, 0, i1 - i0, h};
+        ft.flow.cert = cert;
+        ft.flow.cert_axis = axis;
+        tiles.push_back(std::move(ft));
+    }
+    return true;
+}
+
+void layout_flow_tile(FlowTile& t, Arena& a, const fs_flow_params& p, int box_w, int box_h) {
+    const size_t n = (size_t)t.region.w * t.region.h;
+    t.gray[0] = a.take<float>(n);
+    t.gray[1] = a.take<float>(n);
+    std::vector<TileCert> cert = t.flow.cert;
+    const int axis = t.flow.cert_axis;
+    t.flow.layout(a, t.region.w, t.region.h, p.levels, 2);
+    t.flow.cert = cert;
+    t.flow.cert_axis = axis;
+    t.flow.cap_lv.clear();
+    int pw = box_w, ph = box_h;
+    for (int l = 0; l < t.flow.depth; ++l) {
+        t.flow.cap_lv.push_back({pw, ph});
+        pw = std::max(1, pw / 2);
+        ph = std::max(1, ph / 2);
+    }
+    for (int d = 0; d < 2; ++d) {
+        t.vec[d] = a.take<float2>(n);
+        t.valid[d] = a.take<uint8_t>(n);
+    }
+}
+
 void flow_split_events(FlowWS& ws) {
     if (!ws.ev_fork) FS_CK(cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming));
     while ((int)ws.ev_tensor.size() < ws.depth) {
@@ -183,7 +300,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
         a.r = r;
         a.th = 0;  // per-level choice (launch::lk_tile_rows)
         a.eig_thresh = eig_thresh;
-        a.flow_cap = static_cast<float>(std::max(L.w, L.h));  // src/flow.cpp:241
+        // src/flow.cpp:241 (a tile: the whole crop's level)
+        const Level C = ws.cap_lv.empty() ? L : ws.cap_lv[l];
+        a.flow_cap = static_cast<float>(std::max(C.w, C.h));
+        a.cert_fail = nullptr;
         for (int d = 0; d < ws.ndir; ++d) {
             int src = ws.ndir == 1 ? 0 : d;
             a.d[d].F = ws.pyr[src][l];
@@ -195,6 +315,9 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     // split schedule: the structure tensors need only the pyramid (the level's
     // `from` gradients), so they run on ts while the chain works coarse to fine
     const bool split = ts && ws.ev_fork && (int)ws.ev_tensor.size() >= ws.depth;
+    const bool certify = ws.cert_fail && !ws.cert.empty();
+    if (certify && !split)  // the tap certificate lives in the fp32 FIRST/ITER sweeps
+        raise(FS_ERR_UNSUPPORTED, "flow tiles need the split LK schedule");
     if (split) {
         FS_CK(cudaEventRecord(ws.ev_fork, s));
         FS_CK(cudaStreamWaitEvent(ts, ws.ev_fork, 0));
@@ -248,6 +371,15 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 a.d[d].okout = ws.ok[d][okcur ^ 1];
             }
             if (full && split) FS_CK(cudaStreamWaitEvent(s, ws.ev_tensor[l], 0));
+            if (certify) {
+                const TileCert& c = ws.cert[(size_t)l * p.iterations_per_level + it];
+                a.cert_fail = ws.cert_fail;
+                a.cert_axis = ws.cert_axis;
+                a.zlo = c.zlo;
+                a.zhi = c.zhi;
+                a.exlo = c.exlo;
+                a.exhi = c.exhi;
+            }
             {
                 // 26 B per px, direction and iteration
                 // (F 4 + T 4 + flow r/w 16 + ok r/w 2); the level-constant
@@ -269,7 +401,10 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             a.w = L.w;
             a.h = L.h;
             a.passes = passes;
-            a.final_cap = fin ? static_cast<float>(std::max(ws.w, ws.h)) : 0.f;
+            a.final_cap = fin ? static_cast<float>(ws.cap_lv.empty() ? std::max(ws.w, ws.h)
+                                                                     : std::max(ws.cap_lv[0].w,
+                                                                                ws.cap_lv[0].h))
+                              : 0.f;
             for (int d = 0; d < ws.ndir; ++d) {
                 a.fin[d] = ws.fb[d][fcur];
                 a.fout[d] = fin ? out_vec[d] : ws.fb[d][fcur ^ 1];
@@ -290,7 +425,9 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             a.ndir = ws.ndir;
             a.w = L.w;
             a.h = L.h;
-            a.final_cap = static_cast<float>(std::max(ws.w, ws.h));
+            a.final_cap = static_cast<float>(
+                ws.cap_lv.empty() ? std::max(ws.w, ws.h)
+                                  : std::max(ws.cap_lv[0].w, ws.cap_lv[0].h));
             for (int d = 0; d < ws.ndir; ++d) {
                 a.fin[d] = ws.fb[d][fcur];
                 a.fout[d] = out_vec[d];
@@ -393,6 +530,7 @@ __global__ void k_init_stats(FoldStats* st) {
     st->edt_fail = 0;
     st->box_mismatch = 0;
     st->reach_fail = 0;
+    st->tile_fail = 0;
 }
 __global__ void k_init_count(CanvasCount* cc) { cc->valid_count = 0; }
 

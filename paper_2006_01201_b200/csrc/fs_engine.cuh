@@ -70,6 +70,10 @@ struct Level {
     int w, h;
 };
 
+// A tile's tap certificate for one sweep launch (see FlowTile).
+struct TileCert {
+    int zlo = 0, zhi = 0, exlo = 0, exhi = 0;  // level-local, along the axis
+};
 // Workspace of one (bi)directional pyramidal LK problem on a w x h crop.
 struct FlowWS {
     int w = 0, h = 0, depth = 0, ndir = 0;
@@ -82,8 +86,39 @@ struct FlowWS {
     // side stream right after the pyramid, off the coarse-to-fine chain
     cudaEvent_t ev_fork = nullptr;
     std::vector<cudaEvent_t> ev_tensor;
+    // a tile of a larger crop (FlowTile): the whole crop's level dims (the
+    // flow caps of src/flow.cpp:241, 300-313) and the per-launch tap
+    // certificates ([level * iterations + iteration])
+    std::vector<Level> cap_lv;
+    std::vector<TileCert> cert;
+    int cert_axis = 0;
+    unsigned int* cert_fail = nullptr;
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
+
+// Row/column tile of a fold's flow: the crop's Area3 box
+// is cut along its long axis into interiors; tile t computes the whole
+// pyramidal LK on its region = interior + halo (its own crop, pyramid and
+// flow), and its interior's flow equals the untiled one: the halo covers the
+// dependency cone of every level (iterations x r + smoothing + the 2x
+// upsample, plus the pyramid's clamped border at a cut), and the gathers of
+// `to` are certified on the device to stay in the tile pyramid's exact part.
+struct FlowTile {
+    int axis = 0;            // 0: cut along x (column tiles), 1: along y (row tiles)
+    Rect region, interior;   // box-relative
+    float* gray[2] = {};
+    FlowWS flow;
+    float2* vec[2] = {};     // region-sized level-0 flow
+    uint8_t* valid[2] = {};
+};
+// Plan the tiles of a w x h crop (box-relative) along `axis` with interiors
+// of about tile_len; margin: extra exact pyramid border for the taps (px of
+// level 0).  Returns false (no tiles) when tiling cannot be exact by
+// construction: the axis length not divisible by 2^(depth-1), or a region
+// that would not hold its cone.
+bool plan_flow_tiles(int w, int h, int axis, int tile_len, int margin, const fs_flow_params& p,
+                     std::vector<FlowTile>& tiles);
+void layout_flow_tile(FlowTile& t, Arena& a, const fs_flow_params& p, int box_w, int box_h);
 void flow_split_events(FlowWS& ws);   // create the split schedule's events
 void flow_destroy_events(FlowWS& ws);
 // Enqueue the whole coarse-to-fine flow on stream s.  ndir = 1: from=g0,
@@ -122,6 +157,10 @@ struct FoldWS {
     EdtWS edt[2];
     float4* blended = nullptr;
     float2* wgray = nullptr;  // (optional) gray of the warped constituents on Area3, box-indexed
+    // row/column tiles of the flow (fs_plan_set_tiling); tiles_on cleared when
+    // a tile's certificate fails (the fold then runs untiled)
+    std::vector<FlowTile> tiles;
+    bool tiles_on = false;
     FoldStats* st = nullptr;
     void layout(Arena& a, const Rect& box, const Rect& pano_bbox, const Rect& view_rect,
                 const fs_flow_params& fp);

@@ -154,6 +154,7 @@ __device__ __forceinline__ void bar_arrive(int id) {
 struct TapF {
     int off, dx, dy;  // T offset of (x0, y0); +x / +y tap steps
     float fx, fy;
+    int x0, y0;
 };
 __device__ __forceinline__ TapF level_tap_f(int w, int h, float px, float py) {
     const float wm = (float)(w - 1), hm = (float)(h - 1);
@@ -166,6 +167,8 @@ __device__ __forceinline__ TapF level_tap_f(int w, int h, float px, float py) {
     t.dy = (min(y0 + 1, h - 1) - y0) * w;
     t.fx = px - (float)x0;
     t.fy = py - (float)y0;
+    t.x0 = x0;
+    t.y0 = y0;
     return t;
 }
 
@@ -463,6 +466,15 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
             const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
             fx[b] = t.fx;
             fy[b] = t.fy;
+            if (a.cert_fail) {  // a tile: this pixel's taps inside the exact pyramid part?
+                // (the position before the clamp: at a cut the clamp itself
+                // would differ from the untiled sample)
+                const int q = a.cert_axis ? yb + b : x;
+                const float raw = a.cert_axis ? (float)yy + fl[b].y : (float)xc + fl[b].x;
+                if (xin && yb + b >= 0 && yb + b < h && q >= a.zlo && q < a.zhi &&
+                    !(raw >= (float)a.exlo && raw <= (float)(a.exhi - 1)))
+                    atomicOr(a.cert_fail, 1u);
+            }
             const float* p = T + t.off;
             const uint32_t d = tap0 + (uint32_t)(((bi & 1) * NB + b) * 4 * IW) * 4u;
             cp_async4(d, p);

@@ -113,6 +113,16 @@ struct fs_plan_s {
     std::vector<int> crop_chunk;  // per fold: last chunk its crop reads (-1: none)
     std::vector<int> done_chunk;  // per view k: last chunk of views 0..k
     std::vector<cudaEvent_t> ev_chunk, ev_copied;  // expanded / landed
+    // row/column flow tiles (fs_plan_set_tiling): per fold and tile a stream
+    // (+ one for its structure tensors), the tile-done event and the last
+    // earlier fold whose Area3 box meets the tile's region (its crop waits
+    // for that compose; 0: the views alone)
+    char* tile_arena = nullptr;
+    int tile_len = 0, tile_margin = 0;
+    std::vector<std::vector<cudaStream_t>> tile_s, tile_ts;
+    std::vector<std::vector<cudaEvent_t>> ev_tile;
+    std::vector<cudaEvent_t> ev_tfork;
+    std::vector<std::vector<int>> tile_wait;
     cudaStream_t xst = nullptr;  // expands chunks as they land (the copy engine never waits)
     uint8_t* stage_in = nullptr;   // RGB8 views, 4-byte aligned each
     std::vector<size_t> stage_off;
@@ -262,6 +272,23 @@ void plan_chunks(fs_plan_s* p) {
         FS_CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
     }
     if (!p->xst) FS_CK(cudaStreamCreateWithFlags(&p->xst, cudaStreamNonBlocking));
+}
+
+// A tile's interior flow (both directions) into its fold's box-sized planes.
+void copy_tile_interior(const FoldWS<ViewU8>& f, const FlowTile& t, cudaStream_t s) {
+    const Rect &I = t.interior, &R = t.region;
+    const size_t so = (size_t)(I.y0 - R.y0) * R.w + (I.x0 - R.x0);
+    const size_t dof = (size_t)I.y0 * f.box.w + I.x0;
+    for (int d = 0; d < 2; ++d) {
+        FS_CK(cudaMemcpy2DAsync(f.fvec[d] + dof, (size_t)f.box.w * sizeof(float2), t.vec[d] + so,
+                                (size_t)R.w * sizeof(float2), (size_t)I.w * sizeof(float2), I.h,
+                                cudaMemcpyDeviceToDevice, s));
+        FS_CK(cudaMemcpy2DAsync(f.fvalid[d] + dof, f.box.w, t.valid[d] + so, R.w, I.w, I.h,
+                                cudaMemcpyDeviceToDevice, s));
+    }
+}
+Rect tile_canvas_rect(const FoldWS<ViewU8>& f, const FlowTile& t) {
+    return Rect{f.box.x0 + t.region.x0, f.box.y0 + t.region.y0, t.region.w, t.region.h};
 }
 
 // A canvas rectangle device -> host in the plan's host format.
@@ -430,11 +457,26 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             ViewU8 v = view_of(p, k);
             launches += fold_enqueue_pre(f, plane, v, s);
             launch::snapshot_count(f.st, p->cc, s);
-            launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr, nullptr,
-                                                  nullptr, nullptr, nullptr, true,
-                                                  // (the legacy stream's non-null handle
-                                                  // when s is the default stream)
-                                                  kLkSplit ? (s ? s : cudaStreamLegacy) : nullptr);
+            // (the legacy stream's non-null handle when s is the default stream)
+            cudaStream_t ts = kLkSplit ? (s ? s : cudaStreamLegacy) : nullptr;
+            if (f.tiles_on) {  // the flow tile by tile, then the distance transforms
+                launch::check_box(f.st, f.box, s);
+                launches += 2;
+                for (FlowTile& t : f.tiles) {
+                    {
+                        ProfScope ps("crop_gray", 29.0 * t.region.area(), s);
+                        launch::crop_gray(plane, v, tile_canvas_rect(f, t), 3, t.gray[0],
+                                          t.gray[1], s);
+                    }
+                    launches += 1 + flow_enqueue(t.flow, t.gray[0], t.gray[1], p->fp, t.vec,
+                                                 t.valid, s, ts);
+                    copy_tile_interior(f, t, s);
+                }
+                launches += fold_enqueue_edt(f, plane, v, s);
+            } else {
+                launches += 1 + fold_enqueue_flow_edt(f, plane, plane, v, 3, p->fp, s, nullptr,
+                                                      nullptr, nullptr, nullptr, nullptr, true, ts);
+            }
             launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s);
         }
         {
@@ -510,7 +552,44 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         if (p->tl_stamp && p->crop_wait[k] == 0) mark("fold" + fk + "_flow_start", b);
         cudaEvent_t f0 = tl_event("fold" + fk + "_flow_start"), f1 = tl_event("fold" + fk + "_flow_end");
         cudaEvent_t crop_in = chunked ? ev_crop[k] : nullptr;
-        if (p->crop_wait[k] == 0) {
+        if (f.tiles_on) {
+            // row/column tiles: the distance transforms on es from the start;
+            // every tile crops (waiting only for the composes its region
+            // meets), builds its pyramid and flows on its own streams
+            FS_CK(cudaEventRecord(p->ev_efork[k], b));
+            FS_CK(cudaStreamWaitEvent(es, p->ev_efork[k], 0));
+            launches += fold_enqueue_edt(f, pv, v, es);
+            FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
+            launch::check_box(f.st, f.box, b);
+            ++launches;
+            FS_CK(cudaEventRecord(p->ev_tfork[k], b));
+            for (size_t t = 0; t < f.tiles.size(); ++t) {
+                FlowTile& ft = f.tiles[t];
+                cudaStream_t tsm = p->tile_s[k][t];
+                FS_CK(cudaStreamWaitEvent(tsm, p->ev_tfork[k], 0));
+                if (crop_in) FS_CK(cudaStreamWaitEvent(tsm, crop_in, 0));
+                const Rect rc = tile_canvas_rect(f, ft);
+                const int m = p->tile_wait[k][t];
+                {
+                    ProfScope ps("crop_gray", 29.0 * rc.area(), tsm);
+                    if (m) {
+                        FS_CK(cudaStreamWaitEvent(tsm, p->ev_compose[m], 0));
+                        launch::crop_gray(PanoHybrid{pv, plane}, v, rc, 3, ft.gray[0], ft.gray[1],
+                                          tsm);
+                    } else {
+                        launch::crop_gray(pv, v, rc, 3, ft.gray[0], ft.gray[1], tsm);
+                    }
+                }
+                if (p->tl_stamp) mark("fold" + fk + "_tile" + std::to_string(t) + "_start", tsm);
+                launches += 1 + flow_enqueue(ft.flow, ft.gray[0], ft.gray[1], p->fp, ft.vec,
+                                             ft.valid, tsm, p->tile_ts[k][t]);
+                copy_tile_interior(f, ft, tsm);
+                if (p->tl_stamp) mark("fold" + fk + "_tile" + std::to_string(t) + "_end", tsm);
+                FS_CK(cudaEventRecord(p->ev_tile[k][t], tsm));
+                FS_CK(cudaStreamWaitEvent(b, p->ev_tile[k][t], 0));
+            }
+            FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
+        } else if (p->crop_wait[k] == 0) {
             launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1, es,
                                               p->ev_efork[k], p->ev_ejoin[k], true,
                                               p->tensor_stream[k - 1], crop_in);
@@ -1293,6 +1372,112 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
     });
 }
 
+static void free_tiles(fs_plan_s* p) {
+    for (auto& v : p->tile_s)
+        for (auto st : v) cudaStreamDestroy(st);
+    for (auto& v : p->tile_ts)
+        for (auto st : v) cudaStreamDestroy(st);
+    for (auto& v : p->ev_tile)
+        for (auto e : v) cudaEventDestroy(e);
+    for (auto e : p->ev_tfork)
+        if (e) cudaEventDestroy(e);
+    for (auto& f : p->folds) {
+        for (auto& t : f.tiles) flow_destroy_events(t.flow);
+        f.tiles.clear();
+        f.tiles_on = false;
+    }
+    p->tile_s.clear();
+    p->tile_ts.clear();
+    p->ev_tile.clear();
+    p->ev_tfork.clear();
+    p->tile_wait.clear();
+    if (p->tile_arena) cudaFree(p->tile_arena);
+    p->tile_arena = nullptr;
+}
+
+fs_status fs_plan_set_tiling(fs_plan p, int tile_len, int margin) {
+    return plan_guard([&] {
+        if (!p || tile_len < 0 || margin < 0)
+            raise(FS_ERR_CONTRACT, "plan: tile_len and margin must be >= 0");
+        FS_CK(cudaSetDevice(p->device));
+        FS_CK(cudaDeviceSynchronize());
+        drop_graph(p);
+        free_tiles(p);
+        p->tile_len = tile_len;
+        p->tile_margin = margin;
+        if (tile_len == 0) return;
+        if (!p->dag || !kLkSplit)
+            raise(FS_ERR_UNSUPPORTED, "plan: flow tiles need the DAG schedule and the split LK");
+        const int n = p->n;
+        int any = 0;
+        for (int k = 1; k < n; ++k) {
+            FoldWS<ViewU8>& f = p->folds[k - 1];
+            const int axis = f.box.w >= f.box.h ? 0 : 1;  // cut the long axis
+            f.tiles_on = plan_flow_tiles(f.box.w, f.box.h, axis, tile_len, margin, p->fp, f.tiles);
+            any += f.tiles_on;
+        }
+        if (!any) return;
+        auto lay = [&](Arena& a) {
+            for (auto& f : p->folds)
+                for (auto& t : f.tiles) layout_flow_tile(t, a, p->fp, f.box.w, f.box.h);
+        };
+        Arena a0;
+        lay(a0);
+        FS_CK(cudaMalloc(&p->tile_arena, a0.off));
+        Arena a1;
+        a1.base = p->tile_arena;
+        lay(a1);
+        int least = 0, greatest = 0;
+        FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        p->tile_s.assign(n, {});
+        p->tile_ts.assign(n, {});
+        p->ev_tile.assign(n, {});
+        p->ev_tfork.assign(n, nullptr);
+        p->tile_wait.assign(n, {});
+        for (int k = 1; k < n; ++k) {
+            FoldWS<ViewU8>& f = p->folds[k - 1];
+            if (f.tiles.empty()) continue;
+            FS_CK(cudaEventCreateWithFlags(&p->ev_tfork[k], cudaEventDisableTiming));
+            for (auto& t : f.tiles) {
+                t.flow.cert_fail = &f.st->tile_fail;
+                flow_split_events(t.flow);
+                cudaStream_t a, b;
+                cudaEvent_t e;
+                FS_CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, greatest));
+                FS_CK(cudaStreamCreateWithPriority(&b, cudaStreamNonBlocking, greatest));
+                FS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                p->tile_s[k].push_back(a);
+                p->tile_ts[k].push_back(b);
+                p->ev_tile[k].push_back(e);
+                int wait = 0;
+                const Rect rc = tile_canvas_rect(f, t);
+                for (int m = 1; m < k; ++m)
+                    if (rects_meet(p->boxes[m], rc)) wait = m;
+                p->tile_wait[k].push_back(wait);
+            }
+        }
+    });
+}
+
+int fs_plan_tile_count(fs_plan p, int k) {
+    if (!p || k < 1 || k >= p->n) return -1;
+    const auto& f = p->folds[k - 1];
+    return f.tiles_on ? (int)f.tiles.size() : 0;
+}
+
+fs_status fs_plan_tile_info(fs_plan p, int k, int t, int* region, int* interior) {
+    if (!p || k < 1 || k >= p->n) return FS_ERR_CONTRACT;
+    const auto& f = p->folds[k - 1];
+    if (t < 0 || t >= (int)f.tiles.size()) return FS_ERR_CONTRACT;
+    const Rect &R = f.tiles[t].region, &I = f.tiles[t].interior;
+    const int rv[4] = {R.x0, R.y0, R.w, R.h}, iv[4] = {I.x0, I.y0, I.w, I.h};
+    for (int i = 0; i < 4; ++i) {
+        if (region) region[i] = rv[i];
+        if (interior) interior[i] = iv[i];
+    }
+    return FS_OK;
+}
+
 fs_status fs_plan_transfer_bytes(fs_plan p, size_t* h2d, size_t* d2h) {
     if (!p) return FS_ERR_CONTRACT;
     size_t in = 0, out = (size_t)p->cw * p->chh * p->ho_ch;
@@ -1362,6 +1547,17 @@ fs_status fs_plan_check(fs_plan p) {
                 raise(FS_ERR_SHARD_REACH, "plan: sharded fold #" + std::to_string(k + 1) +
                                               " sampled the panorama outside the strips its GPU "
                                               "holds; execute unsharded");
+        bool untiled = false;
+        for (size_t k = 0; k < p->folds.size(); ++k)
+            if (hs[k].tile_fail && p->folds[k].tiles_on) {
+                p->folds[k].tiles_on = false;
+                untiled = true;
+            }
+        if (untiled) {
+            drop_graph(p);
+            raise(FS_ERR_CONTRACT, "plan: a flow tile gathered outside its exact pyramid part; "
+                                   "the fold runs untiled from now on, execute again");
+        }
         bool widened = false;
         for (size_t k = 0; k < p->folds.size(); ++k)
             if (hs[k].edt_fail && !p->folds[k].full_domain) {
@@ -1670,6 +1866,7 @@ fs_status fs_plan_shard_execute(fs_plan p, int segment, const uint8_t* const* vi
 void fs_plan_destroy(fs_plan p) {
     if (!p) return;
     drop_graph(p);
+    free_tiles(p);
     for (auto b : p->branch)
         if (b) cudaStreamDestroy(b);
     for (auto e : p->ev_branch)

@@ -71,6 +71,23 @@ class Plan:
         """Host views RGB8 (3, all valid) or RGBA8 (4); host canvas RGB8 or RGBA8."""
         _raise(N.lib.fs_plan_set_host_format(self._h, view_channels, out_channels))
 
+    def set_tiling(self, tile_len: int, margin: int = 32) -> None:
+        """Row/column tiles of the folds' flows (fs_plan_set_tiling); 0: off."""
+        _raise(N.lib.fs_plan_set_tiling(self._h, int(tile_len), int(margin)))
+
+    def tiles(self, k: int):
+        """Fold k's tiles in use: [(region, interior)] box-relative {x0, y0, w, h}."""
+        n = N.lib.fs_plan_tile_count(self._h, k)
+        if n < 0:
+            raise ValueError("fold index out of range")
+        out = []
+        for t in range(n):
+            reg, inter = np.zeros(4, np.int32), np.zeros(4, np.int32)
+            _raise(N.lib.fs_plan_tile_info(self._h, k, t, reg.ctypes.data_as(C.c_void_p),
+                                           inter.ctypes.data_as(C.c_void_p)))
+            out.append((tuple(int(v) for v in reg), tuple(int(v) for v in inter)))
+        return out
+
     def transfer_bytes(self):
         """(h2d, d2h) bytes of execute_host with page-locked buffers."""
         a, b = C.c_size_t(), C.c_size_t()
