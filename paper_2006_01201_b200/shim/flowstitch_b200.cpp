@@ -26,6 +26,7 @@
 #include "flowstitch/image.hpp"
 #include "flowstitch/parallel.hpp"
 #include "fs_b200.h"
+#include "png_io.hpp"
 
 namespace flowstitch {
 
@@ -94,12 +95,50 @@ Mask ImageBuf::valid_mask() const {
     return m;
 }
 
-// PNG I/O is host file plumbing outside the flow+blend path.
+// Host image I/O on the PNG codec of png_codec.cpp.
+// u8 -> float as load_image does it (src/image.cpp:27-43): value * (1.0f /
+// 255.0f) in float, 1 channel for gray files, 3 otherwise, valid = alpha >= 128
+// when the file has alpha.
 ImageBuf load_image(const std::string& path) {
-    throw IoError("flowstitch-b200: PNG decoding is not part of the GPU path (" + path + ")");
+    detail::RawPng raw = detail::read_png(path);
+    const int oc = raw.channels == 1 ? 1 : 3;
+    ImageBuf img(raw.width, raw.height, oc);
+    const float scale = 1.0f / 255.0f;
+    const size_t n = static_cast<size_t>(raw.width) * raw.height;
+    std::vector<float>& d = img.data();
+    for (size_t k = 0; k < n; ++k) {
+        const uint8_t* px = raw.bytes.data() + k * raw.channels;
+        for (int c = 0; c < oc; ++c) d[k * oc + c] = px[c] * scale;
+    }
+    if (raw.channels == 4) {
+        std::vector<uint8_t> v(n);
+        for (size_t k = 0; k < n; ++k) v[k] = raw.bytes[k * 4 + 3] >= 128;
+        set_valid_bytes(img, v);
+    }
+    return img;
 }
-void save_image(const ImageBuf&, const std::string& path) {
-    throw IoError("flowstitch-b200: PNG encoding is not part of the GPU path (" + path + ")");
+// float -> u8 as save_image does it (src/image.cpp:45-68): alpha only when a
+// pixel is invalid, lround(clamp(v, 0, 1) * 255.0f) (the product in float),
+// gray replicated into RGB when alpha is added.
+void save_image(const ImageBuf& img, const std::string& path) {
+    if (img.empty()) throw ContractError("save_image: empty image");
+    const std::vector<uint8_t> valid = valid_bytes(img);
+    bool any_invalid = false;
+    for (uint8_t v : valid) any_invalid |= v == 0;
+    const int oc = img.channels() == 1 ? (any_invalid ? 4 : 1) : (any_invalid ? 4 : 3);
+    const size_t n = static_cast<size_t>(img.width()) * img.height();
+    std::vector<uint8_t> bytes(n * oc);
+    const std::vector<float>& d = img.data();
+    const int ic = img.channels();
+    for (size_t k = 0; k < n; ++k) {
+        uint8_t* px = bytes.data() + k * oc;
+        for (int c = 0; c < std::min(oc, 3); ++c) {
+            const float v = std::clamp(d[k * ic + std::min(c, ic - 1)], 0.0f, 1.0f);
+            px[c] = static_cast<uint8_t>(std::lround(v * 255.0f));
+        }
+        if (oc == 4) px[3] = valid[k] ? 255 : 0;
+    }
+    detail::write_png(path, img.width(), img.height(), oc, bytes);
 }
 
 ImageBuf to_gray(const ImageBuf& img) {  // image.hpp:94
@@ -314,8 +353,12 @@ BlendField compute_blend(const RegionPartition& partition) {  // blend_field.hpp
     return out;
 }
 
-void save_blend_png(const BlendField&, const std::string& path) {
-    throw IoError("flowstitch-b200: PNG encoding is not part of the GPU path (" + path + ")");
+// src/blend_field.cpp:132-137: lround(clamp(b, 0, 1) * 255.0) in double, gray
+void save_blend_png(const BlendField& field, const std::string& path) {
+    std::vector<uint8_t> bytes(static_cast<size_t>(field.width) * field.height);
+    for (size_t k = 0; k < bytes.size(); ++k)
+        bytes[k] = static_cast<uint8_t>(std::lround(std::clamp(field.b[k], 0.0, 1.0) * 255.0));
+    detail::write_png(path, field.width, field.height, 1, bytes);
 }
 
 // ---------------------------------------------------------------- blender

@@ -1,7 +1,6 @@
-// flowstitch::b200::stitch_placed (include/flowstitch_b200.hpp) and the PNG
-// codec entry points the reference's pipeline.cpp / image layer link against
-// (proj/src/png_io.hpp) — PNG is host file plumbing outside the GPU path, so
-// they report IoError.
+// flowstitch::b200::stitch_placed (include/flowstitch_b200.hpp).  (The PNG
+// codec the reference's pipeline.cpp / image layer link against is
+// png_codec.cpp.)
 #include <chrono>
 #include <cstring>
 #include <vector>
@@ -13,18 +12,6 @@
 #include "png_io.hpp"
 
 namespace flowstitch {
-namespace detail {
-RawPng read_png(const std::string& path) {
-    throw IoError("flowstitch-b200: PNG decoding is not part of the GPU path (" + path + ")");
-}
-void write_png(const std::string& path, int, int, int, const std::vector<uint8_t>&) {
-    throw IoError("flowstitch-b200: PNG encoding is not part of the GPU path (" + path + ")");
-}
-void read_png_size(const std::string& path, int&, int&) {
-    throw IoError("flowstitch-b200: PNG decoding is not part of the GPU path (" + path + ")");
-}
-}  // namespace detail
-
 namespace b200 {
 
 namespace {
