@@ -83,6 +83,14 @@ const char* fs_last_error(void);
 int fs_abi_version(void);
 /* 1 if a usable sm_100 device is present (does not initialise the others). */
 int fs_device_available(void);
+/* Checks builds (make -C paper_2006_01201_b200/csrc EXTRA=-DFS_CHECKS,
+ * tools/checks.sh): device-side bounds / hand-off checks counted on the
+ * device; the number of violations since the last reset (0 in normal builds). */
+unsigned int fs_debug_check_failures(int reset);
+int fs_debug_checks_built(void);
+/* checks builds only: inject a fault the checks must report (1: mis-stamped
+ * producer/consumer hand-off, 2: tap copies read before they landed; 0: off) */
+void fs_debug_inject(int mode);
 void fs_default_flow_params(fs_flow_params* p);
 void fs_default_blend_params(fs_blend_params* p);
 

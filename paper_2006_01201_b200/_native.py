@@ -124,6 +124,9 @@ SIGNATURES = {
     "fs_plan_set_host_format": (I, [P, I, I]),
     "fs_plan_transfer_bytes": (I, [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "fs_plan_set_tiling": (I, [P, I, I]),
+    "fs_debug_check_failures": (C.c_uint, [I]),
+    "fs_debug_checks_built": (I, []),
+    "fs_debug_inject": (None, [I]),
     "fs_plan_tile_count": (I, [P, I]),
     "fs_plan_tile_info": (I, [P, I, I, P, P]),
     "fs_plan_fold_info": (I, [P, I, P, P]),

@@ -149,6 +149,30 @@ extern "C" {
 const char* fs_last_error(void) { return last_error_slot().c_str(); }
 int fs_abi_version(void) { return 2; }
 
+unsigned int fs_debug_check_failures(int reset) {
+    try {
+        ensure_device();
+    } catch (const Error&) {
+        return 0;
+    }
+    return check_failures_lk(reset != 0) + check_failures_kernels(reset != 0) +
+           check_failures_plan(reset != 0);
+}
+void fs_debug_inject(int mode) {
+    try {
+        ensure_device();
+        check_inject_lk(mode);
+    } catch (const Error&) {
+    }
+}
+int fs_debug_checks_built(void) {
+#ifdef FS_CHECKS
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 int fs_device_available(void) {
     try {
         ensure_device();

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 
 #include "fs_math.cuh"
@@ -28,6 +29,44 @@ inline void once_per_device(std::atomic<unsigned long long>& flags, F&& fn) {
 }
 
 constexpr int kInfSq = 0x3fffffff;  // "no seed" squared distance (exceeds any canvas d^2)
+
+// ---- FS_CHECKS builds (tools/checks.sh) ------------------------------------
+// compute-sanitizer is closed on this GPU pool, so the risky hand-offs carry
+// their own checks in a checks build: FS_DCHECK(cond) counts violations in a
+// per-translation-unit device counter (no relocatable device code needed) and
+// prints the first few with their source line; fs_debug_check_failures()
+// (fs_capi.cu) sums the counters.  Without FS_CHECKS every check compiles away.
+#ifdef FS_CHECKS
+static __device__ unsigned int g_fs_check_fail;
+#define FS_DCHECK(cond)                                                                 \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            if (atomicAdd(&::fs::g_fs_check_fail, 1u) < 8)                               \
+                printf("FS_DCHECK failed: %s:%d %s\n", __FILE__, __LINE__, #cond);       \
+        }                                                                               \
+    } while (0)
+// the TU's counter (defined once per .cu with FS_CHECK_TU(name))
+#define FS_CHECK_TU(name)                                                               \
+    unsigned int check_failures_##name(bool reset) {                                    \
+        unsigned int v = 0;                                                             \
+        cudaMemcpyFromSymbol(&v, g_fs_check_fail, sizeof v);                            \
+        if (reset) {                                                                    \
+            unsigned int z = 0;                                                         \
+            cudaMemcpyToSymbol(g_fs_check_fail, &z, sizeof z);                          \
+        }                                                                               \
+        return v;                                                                       \
+    }
+#else
+#define FS_DCHECK(cond) \
+    do {                \
+    } while (0)
+#define FS_CHECK_TU(name) \
+    unsigned int check_failures_##name(bool) { return 0; }
+#endif
+unsigned int check_failures_lk(bool reset);
+unsigned int check_failures_kernels(bool reset);
+unsigned int check_failures_plan(bool reset);
+void check_inject_lk(int mode);
 
 struct Rect {
     int x0 = 0, y0 = 0, w = 0, h = 0;

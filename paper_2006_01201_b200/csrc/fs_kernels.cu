@@ -11,6 +11,9 @@
 
 namespace fs {
 
+FS_CHECK_TU(kernels)
+
+
 // ============================================================================
 // K0 — placement, partition statistics, crop + gray
 // ============================================================================

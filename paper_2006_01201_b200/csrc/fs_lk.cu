@@ -131,9 +131,20 @@ template <int M>
 __host__ __device__ inline size_t lk_tap_bytes() {
     return LkCfg<M>::F32 ? (size_t)2 * LkCfg<M>::NB * 4 * LkCfg<M>::IW * sizeof(float) : 0;
 }
+// FS_CHECKS: the producer / consumer hand-off stamps (batch index last
+// staged / released per buffer) and, for the fp32 sweeps, each tap slot's
+// source offset, behind everything else
+constexpr size_t kLkCheckBytes =
+#ifdef FS_CHECKS
+    256 + 2 * 4 * LK_IW_F32 * 3 * sizeof(int);
+#else
+    0;
+#endif
+template <int M>
+__host__ __device__ inline size_t lk_check_off(int r);
 template <int M>
 __host__ inline size_t lk_smem_bytes(int r) {
-    return lk_ring_bytes<M>(r) +
+    return kLkCheckBytes + lk_ring_bytes<M>(r) +
            LkCfg<M>::NS * lk_stage_elems<M>() * sizeof(typename LkCfg<M>::Acc) +
            lk_tap_bytes<M>();
 }
@@ -279,6 +290,12 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
     Acc V[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) V[q] = 0.0;
+#ifdef FS_CHECKS
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* chk = reinterpret_cast<int*>(smem + lk_check_off<M>(a.r));
+    if (c == 0)
+        for (int k = 0; k < 16; ++k) chk[k] = -1;
+#endif
     auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
     float2 fl[NB];
     if (GATHER) {
@@ -377,6 +394,9 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
             }
         }
         if (i >= 2) bar_sync<NT>(3 + buf);  // consumers released this buffer
+#ifdef FS_CHECKS
+        if (i >= 2) FS_DCHECK(chk[8 + buf] == i - 2);
+#endif
         Acc* st = stage + (size_t)buf * lk_stage_elems<M>();
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
@@ -416,9 +436,18 @@ __device__ __forceinline__ void lk_produce(const LkArgs& a, const LkDir& D, void
 #pragma unroll
             for (int q = 0; q < NQ; ++q) vb[q * NB * IWP] = V[q];
         }
+#ifdef FS_CHECKS
+        if (c == 0) chk[buf] = i;
+#endif
         bar_arrive<NT>(1 + buf);  // batch staged
     }
 }
+
+#ifdef FS_CHECKS
+// fault injection for the checks build's own test (fs_debug_inject): 1 = the
+// producers mis-stamp every staged batch, 2 = they skip the cp.async wait
+static __device__ int g_fs_inject;
+#endif
 
 // ---- producer (fp32 later iterations): a software pipeline ---------------
 // Batch i's taps were issued (cp.async into shared memory) during batch i-1,
@@ -456,6 +485,13 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
     for (int k = 0; k < K; ++k) ring[k * IW + c] = make_float2(0.f, 0.f);
     float V0 = 0.f, V1 = 0.f;
     auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
+#ifdef FS_CHECKS
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* chk = reinterpret_cast<int*>(smem + lk_check_off<M>(a.r));  // staged[8], freed[8]
+    int* chk_tap = chk + 64;  // [buffer][row][column][off, dx, dy]
+    if (c == 0)
+        for (int k = 0; k < 16; ++k) chk[k] = -1;
+#endif
     const uint32_t tap0 = (uint32_t)__cvta_generic_to_shared(tapb + c);
     // issue batch bi's taps (src/flow.cpp:100-111 at (i + dx, j + dy), :248)
     auto stage_taps = [&](int bi, const float2* fl, float* fx, float* fy) {
@@ -477,6 +513,13 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
             }
             const float* p = T + t.off;
             const uint32_t d = tap0 + (uint32_t)(((bi & 1) * NB + b) * 4 * IW) * 4u;
+#ifdef FS_CHECKS
+            FS_DCHECK(t.off >= 0 && t.off + t.dy + t.dx < w * h);
+            int* ct = chk_tap + ((((bi & 1) * NB + b) * IW) + c) * 3;
+            ct[0] = t.off;
+            ct[1] = t.dx;
+            ct[2] = t.dy;
+#endif
             cp_async4(d, p);
             cp_async4(d + IW * 4, p + t.dx);
             cp_async4(d + 2 * IW * 4, p + t.dy);
@@ -531,20 +574,39 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
             for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
 #pragma unroll
             for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ybase + NB + b) + eoff);
-            cp_async_wait<1>();
+#ifdef FS_CHECKS
+            if (g_fs_inject != 2)
+#endif
+                cp_async_wait<1>();
         } else {
-            cp_async_wait<0>();
+#ifdef FS_CHECKS
+            if (g_fs_inject != 2)
+#endif
+                cp_async_wait<0>();
         }
         float dts[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {  // float bilinear (lerp form) of the staged taps
             const float* tp = tapb + ((tb * NB + b) * 4) * IW + c;
             const float t00 = tp[0], t10 = tp[IW], t01 = tp[2 * IW], t11 = tp[3 * IW];
+#ifdef FS_CHECKS
+            {  // the cp.async copies of this batch landed (wait_group) and are this batch's
+                const int* ct = chk_tap + (((tb * NB + b) * IW) + c) * 3;
+                const float* g = T + ct[0];
+                FS_DCHECK(__float_as_int(t00) == __float_as_int(__ldg(g)) &&
+                          __float_as_int(t10) == __float_as_int(__ldg(g + ct[1])) &&
+                          __float_as_int(t01) == __float_as_int(__ldg(g + ct[2])) &&
+                          __float_as_int(t11) == __float_as_int(__ldg(g + ct[2] + ct[1])));
+            }
+#endif
             const float u = __fmaf_rn(tfx[b], t10 - t00, t00);
             const float v = __fmaf_rn(tfx[b], t11 - t01, t01);
             dts[b] = __fmaf_rn(tfy[b], v - u, u) - ctr[b];
         }
         if (i >= NS) bar_sync<NT>(1 + NS + buf);  // consumers released this buffer
+#ifdef FS_CHECKS
+        if (i >= NS) FS_DCHECK(chk[8 + buf] == i - NS);
+#endif
         float* st = stage + (size_t)buf * lk_stage_elems<M>();
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
@@ -559,7 +621,13 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
             slot = slot + 1 == K ? 0 : slot + 1;
             st[b * IWP + c] = V0;
             st[NB * IWP + b * IWP + c] = V1;
+#ifdef FS_CHECKS
+            FS_DCHECK(slot >= 0 && slot < K);
+#endif
         }
+#ifdef FS_CHECKS
+        if (c == 0) chk[buf] = i + (g_fs_inject == 1);
+#endif
         bar_arrive<NT>(1 + buf);  // batch staged
         if (more) {
 #pragma unroll
@@ -614,6 +682,11 @@ __device__ __forceinline__ void lk_consume_scan(const LkArgs& a, const LkDir& D,
             }
         }
         bar_sync<NT>(1 + buf);
+#ifdef FS_CHECKS
+        extern __shared__ __align__(16) unsigned char smem[];
+        int* chk = reinterpret_cast<int*>(smem + lk_check_off<M>(a.r));
+        FS_DCHECK(chk[buf] == i);
+#endif
         if (rowact) {
             float* vb = stage + (size_t)buf * lk_stage_elems<M>() + b * IWP;
             float H[2][CPL];
@@ -692,10 +765,16 @@ __device__ __forceinline__ void lk_consume_scan(const LkArgs& a, const LkDir& D,
                         final_cap(a.flow_cap, ndx, ndy);  // src/flow.cpp:283-287
                         f = make_float2(ndx, ndy);
                     }
+#ifdef FS_CHECKS
+                    FS_DCHECK(oi < (size_t)a.w * a.h && yo >= 0 && yo < a.h);
+#endif
                     D.fout[oi] = f;
                 }
             }
         }
+#ifdef FS_CHECKS
+        if (t == 0) chk[8 + buf] = i;
+#endif
         if (i + NS < nbat) bar_arrive<NT>(1 + NS + buf);  // buffer free for batch i + NS
     }
 }
@@ -735,6 +814,11 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D,
             }
         }
         bar_sync<NT>(1 + buf);
+#ifdef FS_CHECKS
+        extern __shared__ __align__(16) unsigned char smem[];
+        int* chk = reinterpret_cast<int*>(smem + lk_check_off<M>(a.r));
+        FS_DCHECK(chk[buf] == i);
+#endif
         if (active) {
             const Acc* vb = stage + (size_t)buf * lk_stage_elems<M>() + b * IWP + cs;
             const int QS = NB * IWP;  // plane stride
@@ -809,8 +893,18 @@ __device__ __forceinline__ void lk_consume(const LkArgs& a, const LkDir& D,
                 D.fout[oi] = f;
             }
         }
+#ifdef FS_CHECKS
+        if (t == 0) chk[8 + buf] = i;
+#endif
         if (i + 2 < nbat) bar_arrive<NT>(3 + buf);  // buffer free for batch i + 2
     }
+}
+
+template <int M>
+__host__ __device__ inline size_t lk_check_off(int r) {
+    return lk_ring_bytes<M>(r) +
+           LkCfg<M>::NS * lk_stage_elems<M>() * sizeof(typename LkCfg<M>::Acc) +
+           lk_tap_bytes<M>();
 }
 
 template <int M>
@@ -836,6 +930,15 @@ __global__ void __launch_bounds__(LkCfg<M>::THREADS, LkCfg<M>::MINB) k_lk_sweep(
         lk_produce<M>(a, D, ring, stage, x0, ystart, yend, nbat);
     else
         lk_consume<M>(a, D, stage, x0, y0, ystart, yo_end, nbat);
+}
+
+FS_CHECK_TU(lk)
+void check_inject_lk(int mode) {
+#ifdef FS_CHECKS
+    cudaMemcpyToSymbol(g_fs_inject, &mode, sizeof mode);
+#else
+    (void)mode;
+#endif
 }
 
 namespace launch {

@@ -15,6 +15,9 @@
 #include "fs_engine.cuh"
 
 using namespace fs;
+namespace fs {
+FS_CHECK_TU(plan)
+}  // namespace fs
 
 constexpr size_t kMaxStamps = 512;
 

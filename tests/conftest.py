@@ -13,6 +13,18 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    """FS_CHECKS_RUN=1 (tools/checks.sh, a -DFS_CHECKS build): every GPU test
+    must leave the device-side bounds / hand-off check counters at zero."""
+    yield
+    if os.environ.get("FS_CHECKS_RUN") and request.node.get_closest_marker("gpu"):
+        from paper_2006_01201_b200 import _native as N
+        assert N.lib.fs_debug_checks_built() == 1, "FS_CHECKS_RUN needs a -DFS_CHECKS build"
+        n = N.lib.fs_debug_check_failures(1)
+        assert n == 0, "%d device-side check failure(s) (see the FS_DCHECK lines above)" % n
+
+
 @pytest.fixture(scope="session")
 def fs():
     import paper_2006_01201_b200 as m
