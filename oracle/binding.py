@@ -34,6 +34,8 @@ _SIGS = {
     "compute_blend": (I, [P, P, I, I, P]),
     "softmax_weights": (None, [D, D, D, D, D, D, P]),
     "blend_pair": (I, [P, P, P, P, I, I, I, P, P, P, P, D, D, P, P]),
+    "feather_blend": (I, [P, P, I, I, I, P, P, P, P]),
+    "warp_constituents": (I, [P, P, P, P, I, I, I, P, P, P, P, P, P, P, P]),
     "stitch_placed": (I, [I, P, P, P, P, I, I, I, I, I, I, D, I, D, D, P, P]),
     "misalignment_score": (I, [P, P, P, P, I, I, I, P, P, I, I, P]),
     "estimate_translation": (I, [P, P, I, I, I, I, P, P, P]),
@@ -253,6 +255,31 @@ class Oracle:
             _p(np.ascontiguousarray(flow_rl, np.float32)), _p(np.ascontiguousarray(b, np.float64)),
             _p(np.ascontiguousarray(label, np.uint8)), k, coef, _p(out), _p(ov)), "blend_pair")
         return out, ov
+
+    def feather_blend(self, L, R, b, label):
+        L = np.ascontiguousarray(L, np.float32)
+        h, w, ch = L.shape
+        out = np.empty_like(L)
+        ov = np.empty((h, w), np.uint8)
+        self._ok(self._fn("feather_blend")(
+            _p(L), _p(np.ascontiguousarray(R, np.float32)), w, h, ch,
+            _p(np.ascontiguousarray(b, np.float64)), _p(np.ascontiguousarray(label, np.uint8)),
+            _p(out), _p(ov)), "feather_blend")
+        return out, ov
+
+    def warp_constituents(self, L, vL, R, vR, flow_lr, flow_rl, b, label):
+        L = np.ascontiguousarray(L, np.float32)
+        h, w, ch = L.shape
+        ol, orr = np.empty_like(L), np.empty_like(L)
+        vl, vr = np.empty((h, w), np.uint8), np.empty((h, w), np.uint8)
+        self._ok(self._fn("warp_constituents")(
+            _p(L), _p(np.ascontiguousarray(vL, np.uint8)), _p(np.ascontiguousarray(R, np.float32)),
+            _p(np.ascontiguousarray(vR, np.uint8)), w, h, ch,
+            _p(np.ascontiguousarray(flow_lr, np.float32)),
+            _p(np.ascontiguousarray(flow_rl, np.float32)), _p(np.ascontiguousarray(b, np.float64)),
+            _p(np.ascontiguousarray(label, np.uint8)), _p(ol), _p(vl), _p(orr), _p(vr)),
+            "warp_constituents")
+        return (ol, vl), (orr, vr)
 
     # ---- fold ----
     def _stitch_args(self, images, valids, offsets, cw, chh, params, k, coef):

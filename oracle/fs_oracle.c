@@ -635,6 +635,67 @@ int fso_blend_pair(const float* l, const uint8_t* vl, const float* r, const uint
     return FSO_OK;
 }
 
+/* proj/src/blender.cpp:102-135: Area1 -> L, Area2 -> R, Area3 ->
+ * clamp((1 - b) L + b R) in double, Outside -> 0 and invalid. */
+int fso_feather_blend(const float* l, const float* r, int w, int h, int ch, const double* b,
+                      const uint8_t* label, float* out, uint8_t* out_valid) {
+    for (int j = 0; j < h; ++j)
+        for (int i = 0; i < w; ++i) {
+            size_t idx = (size_t)j * w + i;
+            out_valid[idx] = 1;
+            for (int c = 0; c < ch; ++c) out[idx * ch + c] = 0.0f;
+            switch (label[idx]) {
+                case 1:
+                    for (int c = 0; c < ch; ++c) out[idx * ch + c] = l[idx * ch + c];
+                    break;
+                case 2:
+                    for (int c = 0; c < ch; ++c) out[idx * ch + c] = r[idx * ch + c];
+                    break;
+                case 3:
+                    for (int c = 0; c < ch; ++c) {
+                        double v = (1.0 - b[idx]) * l[idx * ch + c] + b[idx] * r[idx * ch + c];
+                        out[idx * ch + c] = (float)clampd(v, 0.0, 1.0);
+                    }
+                    break;
+                default:
+                    out_valid[idx] = 0;
+                    break;
+            }
+        }
+    return FSO_OK;
+}
+
+/* proj/src/blender.cpp:137-163: copies of L and R whose Area3 pixels are
+ * replaced by the samples Code 1 blends — L at p + FlowRtoL (1 - BlendL),
+ * R at p + FlowLtoR (1 - BlendR) — marked valid. */
+int fso_warp_constituents(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr,
+                          int w, int h, int ch, const float* flow_lr, const float* flow_rl,
+                          const double* b, const uint8_t* label, float* out_l, uint8_t* out_vl,
+                          float* out_r, uint8_t* out_vr) {
+    size_t n = (size_t)w * h;
+    memcpy(out_l, l, n * ch * sizeof(float));
+    memcpy(out_r, r, n * ch * sizeof(float));
+    memcpy(out_vl, vl, n);
+    memcpy(out_vr, vr, n);
+    float color[3];
+    for (int j = 0; j < h; ++j)
+        for (int i = 0; i < w; ++i) {
+            size_t idx = (size_t)j * w + i;
+            if (label[idx] != 3) continue;
+            double blend_r = b[idx];
+            double blend_l = 1.0 - blend_r;
+            fso_bilinear_sample(l, vl, w, h, ch, i + flow_rl[2 * idx] * (1.0 - blend_l),
+                                j + flow_rl[2 * idx + 1] * (1.0 - blend_l), color);
+            for (int c = 0; c < ch; ++c) out_l[idx * ch + c] = color[c];
+            out_vl[idx] = 1;
+            fso_bilinear_sample(r, vr, w, h, ch, i + flow_lr[2 * idx] * (1.0 - blend_r),
+                                j + flow_lr[2 * idx + 1] * (1.0 - blend_r), color);
+            for (int c = 0; c < ch; ++c) out_r[idx * ch + c] = color[c];
+            out_vr[idx] = 1;
+        }
+    return FSO_OK;
+}
+
 /* proj/src/pipeline.cpp:140-212 without the misalignment metrics
  * (:184-187, :194-199), which read the panorama but never write it. */
 int fso_stitch_placed(int n, const float* const* imgs, const uint8_t* const* valids,

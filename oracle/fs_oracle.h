@@ -57,6 +57,12 @@ int fso_distance_transform(const uint8_t* mask, int w, int h, double* out);
 int fso_compute_blend(const uint8_t* label, const int64_t* counts, int w, int h, double* b);
 void fso_softmax_weights(double blend_l, double blend_r, double mag_rtol, double mag_ltor,
                          double k, double coef, double* out2);
+int fso_feather_blend(const float* l, const float* r, int w, int h, int ch, const double* b,
+                      const uint8_t* label, float* out, uint8_t* out_valid);
+int fso_warp_constituents(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr,
+                          int w, int h, int ch, const float* flow_lr, const float* flow_rl,
+                          const double* b, const uint8_t* label, float* out_l, uint8_t* out_vl,
+                          float* out_r, uint8_t* out_vr);
 int fso_blend_pair(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr, int w,
                    int h, int ch, const float* flow_lr, const float* flow_rl, const double* b,
                    const uint8_t* label, double k, double coef, float* out, uint8_t* out_valid);

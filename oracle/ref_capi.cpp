@@ -255,6 +255,42 @@ int fsref_blend_pair(const float* l, const uint8_t* vl, const float* r, const ui
     });
 }
 
+// proj/src/blender.cpp:102-135
+int fsref_feather_blend(const float* l, const float* r, int w, int h, int ch, const double* b,
+                        const uint8_t* label, float* out, uint8_t* out_valid) {
+    return guarded([&] {
+        int64_t counts[4] = {0, 0, 0, 0};
+        for (size_t q = 0; q < static_cast<size_t>(w) * h; ++q) ++counts[label[q]];
+        BlendField bf;
+        bf.width = w;
+        bf.height = h;
+        bf.b.assign(b, b + static_cast<size_t>(w) * h);
+        ImageBuf f = feather_blend(make_image(l, nullptr, w, h, ch), make_image(r, nullptr, w, h, ch),
+                                   bf, make_partition(label, counts, w, h));
+        export_image(f, out, out_valid);
+    });
+}
+
+// proj/src/blender.cpp:137-163
+int fsref_warp_constituents(const float* l, const uint8_t* vl, const float* r, const uint8_t* vr,
+                            int w, int h, int ch, const float* flow_lr, const float* flow_rl,
+                            const double* b, const uint8_t* label, float* out_l, uint8_t* out_vl,
+                            float* out_r, uint8_t* out_vr) {
+    return guarded([&] {
+        int64_t counts[4] = {0, 0, 0, 0};
+        for (size_t q = 0; q < static_cast<size_t>(w) * h; ++q) ++counts[label[q]];
+        BlendField bf;
+        bf.width = w;
+        bf.height = h;
+        bf.b.assign(b, b + static_cast<size_t>(w) * h);
+        auto pr = warp_constituents(make_image(l, vl, w, h, ch), make_image(r, vr, w, h, ch),
+                                    make_flow(flow_lr, w, h), make_flow(flow_rl, w, h), bf,
+                                    make_partition(label, counts, w, h));
+        export_image(pr.first, out_l, out_vl);
+        export_image(pr.second, out_r, out_vr);
+    });
+}
+
 namespace {
 
 using Clock = std::chrono::steady_clock;

@@ -319,8 +319,16 @@ def test_feather_and_warp_constituents(fs, oracle):
     a3 = part.label == 3
     exp = (1 - b.b[..., None]) * L + b.b[..., None] * R
     assert np.abs(Fe.data[a3] - exp[a3]).max() <= 1e-6
+    # the oracle restatement of proj/src/blender.cpp:102-135 (itself pinned to
+    # the compiled reference, tests/test_oracle.py): bit-exact, valid too
+    of, ofv = oracle.feather_blend(L, R, b.b, part.label)
+    assert np.array_equal(Fe.data, of) and np.array_equal(Fe.valid, ofv)
     wl, wr = fs.warp_constituents(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
                                   fs.FlowField(frl, ones), b, part)
+    # proj/src/blender.cpp:137-163: the samples Code 1 blends, bit-exact
+    (owl, owlv), (owr, owrv) = oracle.warp_constituents(L, vl, R, vr, flr, frl, b.b, part.label)
+    assert np.array_equal(wl.data, owl) and np.array_equal(wl.valid, owlv)
+    assert np.array_equal(wr.data, owr) and np.array_equal(wr.valid, owrv)
     F = fs.blend_pair(_img(fs, L, vl), _img(fs, R, vr), fs.FlowField(flr, ones),
                       fs.FlowField(frl, ones), b, part)
     lo = np.minimum(wl.data, wr.data) - 1e-6

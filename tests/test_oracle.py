@@ -101,6 +101,31 @@ def test_restatement_matches_reference_flow(fso, params):
 
 
 @needs_ref
+@pytest.mark.parametrize("seed", [0, 1])
+def test_restatement_matches_reference_feather_and_warp(fso, seed):
+    # proj/src/blender.cpp:102-163 (feather_blend, warp_constituents)
+    ref = reference()
+    rng = np.random.RandomState(40 + seed)
+    h, w = 33, 47
+    L = np.stack([S.value_noise(h, w, seed + c) for c in range(3)], -1)
+    R = np.stack([S.value_noise(h, w, seed + 9 + c) for c in range(3)], -1)
+    vl = (rng.rand(h, w) > 0.2).astype(np.uint8)
+    vr = (rng.rand(h, w) > 0.2).astype(np.uint8)
+    vl[:, 30:] = 0
+    vr[:, :12] = 0
+    lab, cnt = ref.compute_partition(vl, vr)
+    b = ref.compute_blend(lab, cnt)
+    flr = rng.uniform(-5, 5, size=(h, w, 2)).astype(np.float32)
+    frl = rng.uniform(-5, 5, size=(h, w, 2)).astype(np.float32)
+    fa, fb = fso.feather_blend(L, R, b, lab), ref.feather_blend(L, R, b, lab)
+    assert np.array_equal(fa[0], fb[0]) and np.array_equal(fa[1], fb[1])
+    wa, wb = (fso.warp_constituents(L, vl, R, vr, flr, frl, b, lab),
+              ref.warp_constituents(L, vl, R, vr, flr, frl, b, lab))
+    for x, y in zip(wa, wb):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
+@needs_ref
 def test_restatement_matches_reference_fold(fso):
     ref = reference()
     lay = S.small_panorama(seed=2)
