@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the configs[4] throughput leg (20 C2 sets, two in flight)")
     ap.add_argument("--tile-len", type=int, default=0,
                     help="row/column flow tiles of about this length along each fold's long "
                          "axis (fs_plan_set_tiling; 0: untiled)")
@@ -339,6 +341,61 @@ def run_dry(args, ws, rank):
         sys.exit(1)
 
 
+def c5_leg(fs, torch, plan, lay, params, host_views, host_out, rgb_in, rgb_out, sets=20):
+    """BASELINE configs[4] on one GPU: 20 C2 panorama sets back to back, two
+    in flight (two plans on two streams, so one set's band folds overlap the
+    next set's seam folds).  Device-resident and end to end (pinned host views
+    in, pinned canvas out: fs_plan_execute_host_async).  The second plan holds
+    a second synthetic scene (seed 1) of the same geometry; the sets alternate
+    between the two (the fold's work depends on the geometry only)."""
+    import numpy as np
+    lay2 = make_layout("c2", 1)
+    plan2 = fs.Plan(lay2.dims, lay2.offsets, lay2.canvas_w, lay2.canvas_h, params)
+    plan2.set_host_format(3 if rgb_in else 4, 3 if rgb_out else 4)
+    hv2 = [torch.from_numpy(np.ascontiguousarray(v[..., :3]) if rgb_in else v).pin_memory()
+           for v in lay2.views]
+    ho2 = torch.empty_like(host_out).pin_memory()
+    plans = [(plan, [t.data_ptr() for t in host_views], host_out.data_ptr()),
+             (plan2, [t.data_ptr() for t in hv2], ho2.data_ptr())]
+    plan2.execute_ptrs(plans[1][1], plans[1][2])  # uploads, validates plan 2
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+    def run(host):
+        for i in range(2):  # warm-up: one set per plan
+            p, vp, op = plans[i]
+            (p.execute_ptrs_async(vp, op, streams[i].cuda_stream) if host
+             else p.execute(streams[i].cuda_stream))
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(streams[0])
+        streams[1].wait_event(a)
+        for k in range(sets):
+            p, vp, op = plans[k % 2]
+            st = streams[k % 2].cuda_stream
+            p.execute_ptrs_async(vp, op, st) if host else p.execute(st)
+        e1 = torch.cuda.Event()
+        e1.record(streams[1])
+        streams[0].wait_event(e1)
+        b.record(streams[0])
+        torch.cuda.synchronize()
+        for p, _, _ in plans:
+            p.check()
+        return a.elapsed_time(b)
+
+    dev_ms = run(False)
+    e2e_ms = run(True)
+    plan2.close()
+    mpx = sets * lay.canvas_mpx
+    return {"what": "BASELINE configs[4]: %d C2 9000x4000 sets back to back on one GPU, two in "
+                    "flight (two plans, two streams); sets alternate between two synthetic scenes "
+                    "(seeds 0, 1) of the same geometry" % sets,
+            "value": round(mpx / (dev_ms / 1e3), 2), "unit": UNIT,
+            "ms_per_set": round(dev_ms / sets, 4),
+            "e2e": {"value": round(mpx / (e2e_ms / 1e3), 2), "unit": UNIT,
+                    "ms_per_set": round(e2e_ms / sets, 4),
+                    "what": "pinned host views in / canvas out per set, inside the timing"}}
+
+
 def main():
     args = parse_args()
     if maybe_spawn(args):
@@ -499,6 +556,11 @@ def main():
                "h2d_bytes_per_step": h2d_bytes * ws, "d2h_bytes_per_step": d2h_bytes * units,
                "s_per_panorama": round(e_ms / 1e3, 5), "ms_per_step": round(e_ms, 4)}
 
+    # ---- configs[4] throughput (20 sets, two in flight), rank 0 at N = 1
+    c5 = None
+    if ws == 1 and args.config == "c2" and not args.no_c5 and not args.no_e2e:
+        c5 = c5_leg(fs, torch, plan, lay, params, host_views, host_out, rgb_in, rgb_out)
+
     # ---- per-kernel roofline: event-timed launches on the launching stream
     fam = {}
     tot_ms = []
@@ -590,7 +652,7 @@ def main():
                                    "strip_transfers": len(sp.schedule.xfers), "mode": smode}
                                   if sp is not None else None)},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
-            "dp": dp, "clocks": clocks.summary(), "gpu_launches": launches * args.steps,
+            "dp": dp, "c5": c5, "clocks": clocks.summary(), "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)
     plan.close()

@@ -248,6 +248,12 @@ fs_status fs_plan_execute(fs_plan plan, void* stream);
 /* end-to-end: copy host (or device) views in, fold, copy the canvas out */
 fs_status fs_plan_execute_host(fs_plan plan, const uint8_t* const* views_rgba, uint8_t* out_rgba,
                                void* stream);
+/* the same, asynchronous on `stream` (page-locked host buffers, DAG plans):
+ * no synchronisation and no check — after synchronising, the caller calls
+ * fs_plan_check (and on a status other than FS_OK repeats the execution with
+ * fs_plan_execute_host).  Lets several plans (panoramas) overlap on one GPU. */
+fs_status fs_plan_execute_host_async(fs_plan plan, const uint8_t* const* views_rgba,
+                                     uint8_t* out_rgba, void* stream);
 /* after the stream is synchronised: FS_OK or the first device-side error */
 fs_status fs_plan_check(fs_plan plan);
 /* number of kernel launches of one execution (for accounting) */

@@ -119,6 +119,7 @@ SIGNATURES = {
     "fs_plan_output_buffer": (P, [P]),
     "fs_plan_execute": (I, [P, P]),
     "fs_plan_execute_host": (I, [P, PP, P, P]),
+    "fs_plan_execute_host_async": (I, [P, PP, P, P]),
     "fs_plan_check": (I, [P]),
     "fs_plan_launch_count": (I, [P]),
     "fs_plan_set_host_format": (I, [P, I, I]),

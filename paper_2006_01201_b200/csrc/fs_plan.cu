@@ -1524,6 +1524,34 @@ fs_status fs_plan_fold_flow(fs_plan p, int k, float* ltor_vec, uint8_t* ltor_val
     });
 }
 
+fs_status fs_plan_execute_host_async(fs_plan p, const uint8_t* const* views_rgba,
+                                     uint8_t* out_rgba, void* stream) {
+    return plan_guard([&] {
+        FS_CK(cudaSetDevice(p->device));
+        bool ok = p->dag && views_rgba && out_rgba && async_copyable(out_rgba);
+        for (int k = 0; ok && k < p->n; ++k) ok = async_copyable(views_rgba[k]);
+        if (!ok)
+            raise(FS_ERR_UNSUPPORTED, "plan: execute_host_async needs the DAG schedule and "
+                                      "page-locked views and canvas");
+        std::vector<const void*> key;
+        for (int k = 0; k < p->n; ++k) key.push_back(views_rgba[k]);
+        key.push_back((const void*)1);
+        key.push_back(out_rgba);
+        if (p->hexec && p->hkey != key) {
+            cudaGraphExecDestroy(p->hexec);
+            cudaGraphDestroy(p->hgraph);
+            p->hexec = nullptr;
+            p->hgraph = nullptr;
+        }
+        if (!p->hexec) {
+            HostIO io{views_rgba, out_rgba};
+            capture(p, &io, &p->hgraph, &p->hexec);
+            p->hkey = key;
+        }
+        FS_CK(cudaGraphLaunch(p->hexec, static_cast<cudaStream_t>(stream)));
+    });
+}
+
 fs_status fs_plan_execute(fs_plan p, void* stream) {
     return plan_guard([&] {
         FS_CK(cudaSetDevice(p->device));

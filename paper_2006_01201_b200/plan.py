@@ -127,6 +127,13 @@ class Plan:
         _raise(N.lib.fs_plan_execute_host(self._h, arg, C.c_void_p(out_ptr) if out_ptr else None,
                                           C.c_void_p(stream)))
 
+    def execute_ptrs_async(self, view_ptrs: Sequence[int], out_ptr: int, stream: int = 0) -> None:
+        """End to end, asynchronous (page-locked buffers): no sync, no check —
+        call check() after synchronising the stream."""
+        arg = C.cast((C.c_void_p * self.n)(*view_ptrs), N.PP)
+        _raise(N.lib.fs_plan_execute_host_async(self._h, arg, C.c_void_p(out_ptr),
+                                                C.c_void_p(stream)))
+
     def timeline(self, view_ptrs: Optional[Sequence[int]] = None, out_ptr: Optional[int] = None,
                  stream: int = 0) -> dict:
         """One DAG execution with timing events at its schedule points
