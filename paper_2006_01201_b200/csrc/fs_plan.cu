@@ -215,6 +215,12 @@ void upload_view(fs_plan_s* p, int k, const uint8_t* src, cudaStream_t st) {
 // into RGBA8 (on another stream, so the copies run back to back).
 void expand_chunk(fs_plan_s* p, int k, const Rect& r, cudaStream_t st) {
     const Rect& v = p->rects[k];
+    const size_t off = (size_t)(r.y0 - v.y0) * v.w;
+    if (r.x0 == v.x0 && r.w == v.w && off % 4 == 0) {  // whole rows, aligned: vectorised
+        launch::expand_rgb(p->stage_in + p->stage_off[k] + off * 3, p->views[k] + off,
+                           (size_t)r.w * r.h, st);
+        return;
+    }
     launch::expand_rgb_rect(p->stage_in + p->stage_off[k], p->views[k], v.w,
                             Rect{r.x0 - v.x0, r.y0 - v.y0, r.w, r.h}, st);
 }

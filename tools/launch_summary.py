@@ -17,7 +17,7 @@ def main():
         if len(r) < len(H) or r[ix["Metric Name"]] != "gpu__time_duration.sum":
             continue
         name = r[ix["Kernel Name"]].replace("void ", "").split("(")[0]
-        if not name.startswith("fs::"):
+        if not name.startswith(("fs::", "launch::")):
             continue
         v = float(r[ix["Metric Value"]].replace(",", ""))
         unit = r[ix["Metric Unit"]]
