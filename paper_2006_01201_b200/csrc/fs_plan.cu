@@ -67,6 +67,7 @@ struct fs_plan_s {
     std::vector<cudaEvent_t> ev_branch, ev_compose, ev_h2d, ev_own, ev_efork, ev_ejoin;
     std::vector<cudaStream_t> edt_stream;  // per fold: the distance transforms
     std::vector<cudaStream_t> tensor_stream;  // per fold: the LK structure tensors
+    std::vector<cudaStream_t> a2_stream;      // per fold: the Area2 copy (host uploads)
     cudaEvent_t ev_start = nullptr, ev_place = nullptr, ev_out = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr, own = nullptr;
     uint8_t* owner = nullptr;  // first covering view per canvas pixel (PanoViews)
@@ -551,7 +552,10 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         // view: written on the fold's side stream, off the ordered chain and
         // ahead of its distance transforms, while the branch crops and flows
         cudaStream_t es = p->edt_stream[k - 1];
-        cudaStream_t a2s = es;  // (on the branch: C2 0.5% slower)
+        // device-resident: on the EDT stream (on the branch: C2 0.5% slower);
+        // host uploads: on its own stream, so the distance transforms (which
+        // need no pixels) do not wait behind the copy for the view to land
+        cudaStream_t a2s = chunked ? p->a2_stream[k - 1] : es;
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_own[k], 0));
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_clear, 0));
         if (chunked) FS_CK(cudaStreamWaitEvent(a2s, ev_view[k], 0));  // view k's pixels
@@ -617,6 +621,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
         mark("fold" + fk + "_edt_end", b);
+        if (chunked) FS_CK(cudaStreamWaitEvent(b, p->ev_a2[k], 0));  // joins the copy's stream
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         if (chunked) FS_CK(cudaStreamWaitEvent(s, ev_view[k], 0));  // L taps anywhere in views <= k
@@ -1276,11 +1281,14 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
             p->edt_stream.assign(n - 1, nullptr);
             p->tensor_stream.assign(n - 1, nullptr);
+            p->a2_stream.assign(n - 1, nullptr);
             for (int k = 0; k < n - 1; ++k) {
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
                                                    greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->tensor_stream[k], cudaStreamNonBlocking,
+                                                   greatest));
+                FS_CK(cudaStreamCreateWithPriority(&p->a2_stream[k], cudaStreamNonBlocking,
                                                    greatest));
             }
             p->ev_h2d.assign(n, nullptr);
@@ -1922,6 +1930,8 @@ void fs_plan_destroy(fs_plan p) {
     for (auto e : p->ev_ejoin)
         if (e) cudaEventDestroy(e);
     for (auto st : p->edt_stream)
+        if (st) cudaStreamDestroy(st);
+    for (auto st : p->a2_stream)
         if (st) cudaStreamDestroy(st);
     for (auto st : p->tensor_stream)
         if (st) cudaStreamDestroy(st);
