@@ -456,6 +456,9 @@ static __device__ int g_fs_inject;
 // starts with its data on chip: gradients, It (float bilinear of the staged
 // taps), the two products, the column's running window sums (the row leaving
 // the window comes from the ring of the last 2r + 1 products), staging.
+// Batches whose preloaded rows all lie inside the level address them from one
+// row offset (no per-row clamps); only the first and last batches of a
+// column clamp.  CERT (row/column tiles only) adds the tap certificate.
 __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -465,7 +468,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int M>
+template <int M, bool CERT>
 __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, float2* ring,
                                                float* stage, float* tapb, int x0, int ystart,
                                                int yend, int nbat) {
@@ -476,6 +479,7 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
     const int x = x0 - r + c;
     const bool xin = x >= 0 && x < w;
     const int xc = clampi(x, 0, w - 1);
+    const float xcf = (float)xc, wm = (float)(w - 1), hm = (float)(h - 1);
     // warp edge lanes: the horizontal neighbour outside the warp (others: own column)
     const int eoff = lane == 0 ? clampi(x - 1, 0, w - 1) - xc
                    : lane == 31 ? clampi(x + 1, 0, w - 1) - xc : 0;
@@ -483,6 +487,9 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
     const float2* __restrict__ Uc = D.fin + xc;
     const float* __restrict__ T = D.T;
     for (int k = 0; k < K; ++k) ring[k * IW + c] = make_float2(0.f, 0.f);
+    float2* rp = ring + c;  // this column's ring slot the next input row replaces
+    float2* const rend = ring + c + K * IW;
+    const unsigned yhi = (unsigned)min(h, yend);  // rows with products: [0, yhi)
     float V0 = 0.f, V1 = 0.f;
     auto ro = [&](int y) { return clampi(y, 0, h - 1) * w; };
 #ifdef FS_CHECKS
@@ -493,37 +500,42 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
         for (int k = 0; k < 16; ++k) chk[k] = -1;
 #endif
     const uint32_t tap0 = (uint32_t)__cvta_generic_to_shared(tapb + c);
-    // issue batch bi's taps (src/flow.cpp:100-111 at (i + dx, j + dy), :248)
-    auto stage_taps = [&](int bi, const float2* fl, float* fx, float* fy) {
-        const int yb = ystart + bi * NB;
+    // issue the taps of the batch starting at row yb into tap buffer tbuf
+    // (src/flow.cpp:100-111 at (i + dx, j + dy), :248): the clamp bounds are
+    // integers, so clamp / truncate / fraction are exact in float
+    auto stage_taps = [&](int yb, int tbuf, const float2* fl, float* fx, float* fy) {
+        const uint32_t d0 = tap0 + (uint32_t)(tbuf * NB * 4 * IW * 4);
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
             const int yy = clampi(yb + b, 0, h - 1);
-            const TapF t = level_tap_f(w, h, (float)xc + fl[b].x, (float)yy + fl[b].y);
-            fx[b] = t.fx;
-            fy[b] = t.fy;
-            if (a.cert_fail) {  // a tile: this pixel's taps inside the exact pyramid part?
+            const float rx = xcf + fl[b].x, ry = (float)yy + fl[b].y;
+            const float px = fminf(fmaxf(rx, 0.f), wm), py = fminf(fmaxf(ry, 0.f), hm);
+            const int ix = (int)px, iy = (int)py;
+            fx[b] = px - (float)ix;
+            fy[b] = py - (float)iy;
+            if (CERT) {  // a tile: this pixel's taps inside the exact pyramid part?
                 // (the position before the clamp: at a cut the clamp itself
                 // would differ from the untiled sample)
                 const int q = a.cert_axis ? yb + b : x;
-                const float raw = a.cert_axis ? (float)yy + fl[b].y : (float)xc + fl[b].x;
+                const float raw = a.cert_axis ? ry : rx;
                 if (xin && yb + b >= 0 && yb + b < h && q >= a.zlo && q < a.zhi &&
                     !(raw >= (float)a.exlo && raw <= (float)(a.exhi - 1)))
                     atomicOr(a.cert_fail, 1u);
             }
-            const float* p = T + t.off;
-            const uint32_t d = tap0 + (uint32_t)(((bi & 1) * NB + b) * 4 * IW) * 4u;
+            const int dx = ix < w - 1 ? 1 : 0, dyw = iy < h - 1 ? w : 0;
+            const float* p = T + (iy * w + ix);
+            const uint32_t d = d0 + (uint32_t)(b * 4 * IW * 4);
 #ifdef FS_CHECKS
-            FS_DCHECK(t.off >= 0 && t.off + t.dy + t.dx < w * h);
-            int* ct = chk_tap + ((((bi & 1) * NB + b) * IW) + c) * 3;
-            ct[0] = t.off;
-            ct[1] = t.dx;
-            ct[2] = t.dy;
+            FS_DCHECK(iy * w + ix >= 0 && iy * w + ix + dyw + dx < w * h);
+            int* ct = chk_tap + (((tbuf * NB + b) * IW) + c) * 3;
+            ct[0] = iy * w + ix;
+            ct[1] = dx;
+            ct[2] = dyw;
 #endif
             cp_async4(d, p);
-            cp_async4(d + IW * 4, p + t.dx);
-            cp_async4(d + 2 * IW * 4, p + t.dy);
-            cp_async4(d + 3 * IW * 4, p + (t.dy + t.dx));
+            cp_async4(d + IW * 4, p + dx);
+            cp_async4(d + 2 * IW * 4, p + dyw);
+            cp_async4(d + 3 * IW * 4, p + (dyw + dx));
         }
         cp_async_commit();
     };
@@ -531,7 +543,7 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
     float tfx[NB], tfy[NB], cen[NB + 2], edg[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + b)];
-    stage_taps(0, fl, tfx, tfy);
+    stage_taps(ystart, 0, fl, tfx, tfy);
     if (nbat > 1) {
 #pragma unroll
         for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ystart + NB + b)];
@@ -540,7 +552,6 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
     for (int j = 0; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ystart - 1 + j));
 #pragma unroll
     for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ystart + b) + eoff);
-    int slot = 0;
     for (int i = 0; i < nbat; ++i) {
         const int buf = i % NS, tb = i & 1;
         const int ybase = ystart + i * NB;
@@ -560,20 +571,33 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
             gxs[b] = 0.5f * (rt - lf);
         }
         float nfx[NB], nfy[NB];
-        if (more) {  // next batch's taps, then the flow two batches ahead
-            stage_taps(i + 1, fl, nfx, nfy);
-            if (i + 2 < nbat) {
-#pragma unroll
-                for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + 2 * NB + b)];
-            }
-        }
-        if (more) {  // next batch's `from` rows and edge neighbours
+        if (more) {
+            // next batch's taps, then the flow two batches ahead, the next
+            // batch's `from` rows (ybase + NB + 1 ..) and edge neighbours
+            stage_taps(ybase + NB, tb ^ 1, fl, nfx, nfy);
+            const bool fl2 = i + 2 < nbat;
             cen[0] = cen[NB];
             cen[1] = cen[NB + 1];
+            if (ybase + NB >= 0 && ybase + 3 * NB <= h) {  // every row below inside
+                const int rb = (ybase + NB) * w;
+                if (fl2) {
 #pragma unroll
-            for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
+                    for (int b = 0; b < NB; ++b) fl[b] = Uc[rb + (NB + b) * w];
+                }
 #pragma unroll
-            for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ybase + NB + b) + eoff);
+                for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + (rb + (j - 1) * w));
+#pragma unroll
+                for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + (rb + b * w + eoff));
+            } else {
+                if (fl2) {
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) fl[b] = Uc[ro(ybase + 2 * NB + b)];
+                }
+#pragma unroll
+                for (int j = 2; j < NB + 2; ++j) cen[j] = __ldg(Fc + ro(ybase + NB - 1 + j));
+#pragma unroll
+                for (int b = 0; b < NB; ++b) edg[b] = __ldg(Fc + ro(ybase + NB + b) + eoff);
+            }
 #ifdef FS_CHECKS
             if (g_fs_inject != 2)
 #endif
@@ -607,22 +631,21 @@ __device__ __forceinline__ void lk_produce_f32(const LkArgs& a, const LkDir& D, 
 #ifdef FS_CHECKS
         if (i >= NS) FS_DCHECK(chk[8 + buf] == i - NS);
 #endif
-        float* st = stage + (size_t)buf * lk_stage_elems<M>();
+        float* st = stage + (size_t)buf * lk_stage_elems<M>() + c;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-            const int y = ybase + b;
-            const bool in = xin && y >= 0 && y < h && y < yend;
+            const bool in = xin && (unsigned)(ybase + b) < yhi;
             const float px = in ? gxs[b] * dts[b] : 0.f, py = in ? gys[b] * dts[b] : 0.f;
-            float2* rp = ring + (slot * IW + c);
             const float2 o = *rp;
             *rp = make_float2(px, py);
             V0 = (V0 + px) - o.x;
             V1 = (V1 + py) - o.y;
-            slot = slot + 1 == K ? 0 : slot + 1;
-            st[b * IWP + c] = V0;
-            st[NB * IWP + b * IWP + c] = V1;
+            rp += IW;
+            if (rp == rend) rp = ring + c;
+            st[b * IWP] = V0;
+            st[NB * IWP + b * IWP] = V1;
 #ifdef FS_CHECKS
-            FS_DCHECK(slot >= 0 && slot < K);
+            FS_DCHECK(rp >= ring + c && rp < rend);
 #endif
         }
 #ifdef FS_CHECKS
@@ -907,7 +930,8 @@ __host__ __device__ inline size_t lk_check_off(int r) {
            lk_tap_bytes<M>();
 }
 
-template <int M>
+// CERT: the row/column tiles' tap certificate (fp32 sweeps only)
+template <int M, bool CERT = false>
 __global__ void __launch_bounds__(LkCfg<M>::THREADS, LkCfg<M>::MINB) k_lk_sweep(LkArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     void* ring = smem;
@@ -922,8 +946,8 @@ __global__ void __launch_bounds__(LkCfg<M>::THREADS, LkCfg<M>::MINB) k_lk_sweep(
         float* tapb = reinterpret_cast<float*>(smem + lk_ring_bytes<M>(a.r) +
                                                LkCfg<M>::NS * lk_stage_elems<M>() * sizeof(float));
         if (threadIdx.x < LkCfg<M>::IW)
-            lk_produce_f32<M>(a, D, static_cast<float2*>(ring), stage, tapb, x0, ystart, yend,
-                              nbat);
+            lk_produce_f32<M, CERT>(a, D, static_cast<float2*>(ring), stage, tapb, x0, ystart,
+                                    yend, nbat);
         else
             lk_consume_scan<M>(a, D, stage, x0, y0, ystart, yo_end, nbat);
     } else if (threadIdx.x < LkCfg<M>::IW)
@@ -969,6 +993,10 @@ void lk_init() {
                              mx);
         cudaFuncSetAttribute(k_lk_sweep<LK_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              mx);
+        cudaFuncSetAttribute(k_lk_sweep<LK_ITER, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_lk_sweep<LK_FIRST, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     });
 }
 
@@ -1008,6 +1036,12 @@ static void sweep_launch(LkArgs a, cudaStream_t s) {
     a.tw = LkCfg<M>::IW - 2 * a.r;
     if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB, a.tw);
     dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
+    if constexpr (LkCfg<M>::F32) {
+        if (a.cert_fail) {
+            k_lk_sweep<M, true><<<g, LkCfg<M>::THREADS, lk_smem_bytes<M>(a.r), s>>>(a);
+            return;
+        }
+    }
     k_lk_sweep<M><<<g, LkCfg<M>::THREADS, lk_smem_bytes<M>(a.r), s>>>(a);
 }
 
