@@ -4,12 +4,12 @@
 # Leaves lib_B.so installed.
 L=paper_2006_01201_b200/libfs_b200.so
 mkdir -p gpurun_out/ab
-for v in A B; do
+for v in ${VARS:-A B}; do
   cp build/ab/lib_$v.so $L
   python tools/flow_bits.py /tmp/flows_$v.npz > /dev/null 2>&1 || echo "flow dump $v failed"
 done
 python tools/flow_bits.py /tmp/flows_A.npz /tmp/flows_B.npz 2>&1 | tail -15
-for rep in 1 2; do for v in A B; do
+for rep in 1 2; do for v in ${VARS:-A B}; do
   cp build/ab/lib_$v.so $L
   for c in ${CFGS:-c2}; do
     python bench.py --config $c --no-cpu-baseline --no-c5 --steps 30 2>/dev/null | tail -1 > gpurun_out/ab/bench_${v}_${c}_$rep.json
