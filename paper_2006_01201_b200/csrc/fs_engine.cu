@@ -335,6 +335,7 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     }
     int fcur = 0, okcur = 0;
     for (int l = ws.depth - 1; l >= 0; --l) {
+        if (ws.mark) ws.mark("L" + std::to_string(l), s);
         const Level L = ws.lv[l];
         const double npx = (double)L.w * L.h * ws.ndir;
         LkArgs a = level_args(l);
@@ -441,6 +442,7 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             ++launches;
         }
     }
+    if (ws.mark) ws.mark("flow_end", s);
     FS_CK(cudaGetLastError());
     return launches;
 }

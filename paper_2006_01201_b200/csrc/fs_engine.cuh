@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -93,6 +94,9 @@ struct FlowWS {
     std::vector<TileCert> cert;
     int cert_axis = 0;
     unsigned int* cert_fail = nullptr;
+    // schedule marks (fs_plan_timeline_graph): called at every level start
+    // ("L<l>") and after the last level ("flow_end") on the chain's stream
+    std::function<void(const std::string&, cudaStream_t)> mark;
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
 

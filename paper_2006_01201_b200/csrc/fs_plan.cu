@@ -603,6 +603,9 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             }
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         } else if (p->crop_wait[k] == 0) {
+            if (p->tl_stamp) f.flow.mark = [&, fk](const std::string& l, cudaStream_t st) {
+                mark("fold" + fk + "_" + l, st);
+            };
             launches += fold_enqueue_flow_edt(f, pv, pv, v, 3, p->fp, b, f0, f1, es,
                                               p->ev_efork[k], p->ev_ejoin[k], true,
                                               p->tensor_stream[k - 1], crop_in);
@@ -614,12 +617,18 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             FS_CK(cudaEventRecord(p->ev_ejoin[k], es));
             FS_CK(cudaStreamWaitEvent(b, p->ev_compose[p->crop_wait[k]], 0));
             if (crop_in) FS_CK(cudaStreamWaitEvent(b, crop_in, 0));
-            if (p->tl_stamp) mark("fold" + fk + "_flow_start", b);
+            if (p->tl_stamp) {
+                mark("fold" + fk + "_flow_start", b);
+                f.flow.mark = [&, fk](const std::string& l, cudaStream_t st) {
+                    mark("fold" + fk + "_" + l, st);
+                };
+            }
             launches += fold_enqueue_flow_edt(f, pv, PanoHybrid{pv, plane}, v, 3, p->fp, b, f0, f1,
                                               nullptr, nullptr, nullptr, false,
                                               p->tensor_stream[k - 1]);
             FS_CK(cudaStreamWaitEvent(b, p->ev_ejoin[k], 0));
         }
+        f.flow.mark = nullptr;
         mark("fold" + fk + "_edt_end", b);
         if (chunked) FS_CK(cudaStreamWaitEvent(b, p->ev_a2[k], 0));  // joins the copy's stream
         FS_CK(cudaEventRecord(p->ev_branch[k], b));
@@ -1255,7 +1264,14 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             if (r.w <= 0 || r.h <= 0) raise(FS_ERR_CONTRACT, "plan: empty view");
             p->rects.push_back(r);
         }
-        FS_CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+        {
+            // the graph's own stream carries the ordered blend + compose chain
+            // (and place, clear): critical path, highest priority (the graph's
+            // kernel nodes keep the priority of the stream they were captured on)
+            int least = 0, greatest = 0;
+            FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            FS_CK(cudaStreamCreateWithPriority(&p->cap, cudaStreamNonBlocking, greatest));
+        }
         std::vector<Rect> boxes = views_rgba ? boxes_from_masks(p, views_rgba) : boxes_from_rects(p);
         // DAG: fold k's L crop may come straight from the views when no earlier
         // fold's Area3 box overlaps its own (those pixels hold the first
@@ -1282,14 +1298,23 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             p->edt_stream.assign(n - 1, nullptr);
             p->tensor_stream.assign(n - 1, nullptr);
             p->a2_stream.assign(n - 1, nullptr);
+            // Priorities by slack: the flow chains first (their coarse levels
+            // are few CTAs, latency-bound, and starved behind big side
+            // kernels otherwise); the level tensors (needed level by level)
+            // and the distance transforms / Area2 copies of the folds that
+            // start at once next; the distance transforms of the folds whose
+            // flow waits for an earlier compose (C2's bands: needed a whole
+            // phase later) last.
+            const int p_next = std::min(least, greatest + 1);
             for (int k = 0; k < n - 1; ++k) {
+                const int p_side = p->crop_wait[k + 1] ? least : p_next;
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
-                                                   greatest));
+                                                   p_side));
                 FS_CK(cudaStreamCreateWithPriority(&p->tensor_stream[k], cudaStreamNonBlocking,
-                                                   greatest));
+                                                   p_next));
                 FS_CK(cudaStreamCreateWithPriority(&p->a2_stream[k], cudaStreamNonBlocking,
-                                                   greatest));
+                                                   p_side));
             }
             p->ev_h2d.assign(n, nullptr);
             p->ev_own.assign(n, nullptr);
