@@ -232,6 +232,7 @@ struct LkArgs {
     int mode;    // 0 zero, 1 flow-in, 2 upsample-from-coarse
     int r;
     int tw, th;  // output tile (th <= 0: chosen per level)
+    int slot_div;  // th choice: the CTA slots a launch can expect (148 x CTAs/SM / slot_div)
     double eig_thresh;
     float flow_cap;
     // row/column tiles (FlowTile): the taps of the pixels whose coordinate

@@ -1003,11 +1003,11 @@ void lk_init() {
 #ifndef LK_TH_MIN
 #define LK_TH_MIN 16  // smallest tile height (smaller: faster alone, slower in the DAG)
 #endif
-static int lk_tile_rows(int w, int h, int r, int ndir, int per_sm, int tw) {
+static int lk_tile_rows(int w, int h, int r, int ndir, int per_sm, int tw, int slot_div) {
     // A CTA sweeps th + 2r rows; CTAs run in waves of 148 SMs x per_sm.  Pick th
     // minimising waves x rows per CTA (wave quantisation vs. halo rows).
     const long cols = (w + tw - 1) / tw;
-    const long slots = 148L * per_sm;
+    const long slots = 148L * per_sm / std::max(1, slot_div);
     int best = LK_TH_MIN;
     long best_cost = -1;
     for (int th = LK_TH_MIN; th <= 256; th += (th < 32 ? 4 : 8)) {
@@ -1034,7 +1034,7 @@ cudaError_t lk_prep(const LkArgs& a, cudaStream_t s) {
 template <int M>
 static void sweep_launch(LkArgs a, cudaStream_t s) {
     a.tw = LkCfg<M>::IW - 2 * a.r;
-    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB, a.tw);
+    if (a.th <= 0) a.th = lk_tile_rows(a.w, a.h, a.r, a.ndir, LkCfg<M>::MINB, a.tw, a.slot_div);
     dim3 g((a.w + a.tw - 1) / a.tw, (a.h + a.th - 1) / a.th, a.ndir);
     if constexpr (LkCfg<M>::F32) {
         if (a.cert_fail) {
