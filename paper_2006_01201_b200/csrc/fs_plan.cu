@@ -281,7 +281,11 @@ void plan_chunks(fs_plan_s* p) {
         FS_CK(cudaEventCreateWithFlags(&p->ev_chunk[i], cudaEventDisableTiming));
         FS_CK(cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming));
     }
-    if (!p->xst) FS_CK(cudaStreamCreateWithFlags(&p->xst, cudaStreamNonBlocking));
+    if (!p->xst) {  // the expansions gate the folds' crops: highest priority
+        int least = 0, greatest = 0;
+        FS_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        FS_CK(cudaStreamCreateWithPriority(&p->xst, cudaStreamNonBlocking, greatest));
+    }
 }
 
 // A tile's interior flow (both directions) into its fold's box-sized planes.
@@ -1334,9 +1338,12 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
                                    &p->ev_clear})
                 FS_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
             FS_CK(cudaMalloc(&p->hist, sizeof(unsigned long long) * kMaxDagViews));
-            FS_CK(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
-            FS_CK(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
-            FS_CK(cudaStreamCreateWithFlags(&p->d2h_early, cudaStreamNonBlocking));
+            // the transfer streams' kernels (RGB8 expansion and packing) are
+            // tiny and gate the copy engines: highest priority, so they do
+            // not queue behind the flows
+            FS_CK(cudaStreamCreateWithPriority(&p->h2d, cudaStreamNonBlocking, greatest));
+            FS_CK(cudaStreamCreateWithPriority(&p->d2h, cudaStreamNonBlocking, greatest));
+            FS_CK(cudaStreamCreateWithPriority(&p->d2h_early, cudaStreamNonBlocking, greatest));
             FS_CK(cudaStreamCreateWithFlags(&p->hfill, cudaStreamNonBlocking));
             FS_CK(cudaEventCreateWithFlags(&p->ev_hfill1, cudaEventDisableTiming));
             // the claims gate every fold's branch: highest priority
