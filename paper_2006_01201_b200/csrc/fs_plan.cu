@@ -1311,7 +1311,12 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
             // phase later) last.
             const int p_next = std::min(least, greatest + 1);
             for (int k = 0; k < n - 1; ++k) {
-                const int p_side = p->crop_wait[k + 1] ? least : p_next;
+                int p_side = p->crop_wait[k + 1] ? least : p_next;
+                // the first fold of the first phase blends first: its distance
+                // transforms at the flows' priority (C2 3.394 -> 3.382 ms)
+                bool first = !p->crop_wait[k + 1];
+                for (int m = 1; m < k + 1; ++m) first &= p->crop_wait[m] != 0;
+                if (first) p_side = greatest;
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
                                                    p_side));
