@@ -330,16 +330,22 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
     if (split) {
         FS_CK(cudaEventRecord(ws.ev_fork, s));
         FS_CK(cudaStreamWaitEvent(ts, ws.ev_fork, 0));
+        // the coarsest level's tensor is the chain's first need: on the chain
+        // itself (on ts it waited behind the other folds' side work: C2
+        // 3.378 -> 3.366 ms); the finer levels' tensors have slack
+        const int l_chain = ws.depth - 1;
         for (int l = ws.depth - 1; l >= 0; --l) {
             LkArgs a = level_args(l);
+            cudaStream_t st = l == l_chain ? s : ts;
             {
                 // per pixel and direction: F 4 in, coef 16 out
                 ProfScope ps(kSweepNames[2][std::min(l, 7)],
-                             20.0 * ws.lv[l].w * ws.lv[l].h * ws.ndir, ts);
-                FS_CK(launch::lk_sweep(a, 2, ts));
+                             20.0 * ws.lv[l].w * ws.lv[l].h * ws.ndir, st);
+                FS_CK(launch::lk_sweep(a, 2, st));
+                if (ws.mark && getenv("FS_TL_FINE")) ws.mark("T" + std::to_string(l), st);
             }
             ++launches;
-            FS_CK(cudaEventRecord(ws.ev_tensor[l], ts));
+            FS_CK(cudaEventRecord(ws.ev_tensor[l], st));
         }
     }
     int fcur = 0, okcur = 0;
@@ -368,6 +374,7 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
             // flow 8 + ok 1 out, + the coarser flow/ok 9/4
             ProfScope ps("lk_prep", (9.0 + (a.mode == 2 ? 2.25 : 0.0)) * npx, s);
             FS_CK(launch::lk_prep(a, s));
+            if (ws.mark && getenv("FS_TL_FINE")) ws.mark("L" + std::to_string(l) + "_prep", s);
         }
         ++launches;
         fcur ^= 1;
@@ -396,6 +403,8 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
                 // inverse tensor this design also moves (16 B) is not counted
                 ProfScope ps(kSweepNames[full && !split][std::min(l, 7)], 26.0 * npx, s);
                 FS_CK(launch::lk_sweep(a, full ? (split ? 3 : 1) : 0, s));
+                if (ws.mark && getenv("FS_TL_FINE"))
+                    ws.mark("L" + std::to_string(l) + "_it" + std::to_string(it), s);
             }
             ++launches;
             fcur ^= 1;
