@@ -40,10 +40,12 @@ def main():
         op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
         c = per_op[op]
         c["warp_inst"] += num(x[ix["Instructions Executed"]])
-        c["l1_tag_global"] += num(x[ix["L1 Tag Requests Global"]])
-        c["l1_wf_shared"] += num(x[ix["L1 Wavefronts Shared"]])
-        c["l1_wf_shared_ideal"] += num(x[ix["L1 Wavefronts Shared Ideal"]])
-        c["l2_sectors"] += num(x[ix["L2 Theoretical Sectors Global"]])
+        for key, col in (("l1_tag_global", "L1 Tag Requests Global"),
+                         ("l1_wf_shared", "L1 Wavefronts Shared"),
+                         ("l1_wf_shared_ideal", "L1 Wavefronts Shared Ideal"),
+                         ("l2_sectors", "L2 Theoretical Sectors Global")):
+            if col in ix:  # absent when the kernel has no such access
+                c[key] += num(x[ix[col]])
         c["samples"] += num(x[ix["Warp Stall Sampling (All Samples)"]])
         tot_samples += num(x[ix["Warp Stall Sampling (All Samples)"]])
         for s in stall_cols:
