@@ -331,9 +331,9 @@ int flow_enqueue(FlowWS& ws, const float* g0, const float* g1, const fs_flow_par
         FS_CK(cudaEventRecord(ws.ev_fork, s));
         FS_CK(cudaStreamWaitEvent(ts, ws.ev_fork, 0));
         // the coarsest level's tensor is the chain's first need: on the chain
-        // itself (on ts it waited behind the other folds' side work: C2
-        // 3.378 -> 3.366 ms); the finer levels' tensors have slack
-        const int l_chain = ws.depth - 1;
+        // itself when other folds' side work competes for the GPU (see
+        // FlowWS::tensor0_on_chain)
+        const int l_chain = ws.tensor0_on_chain ? ws.depth - 1 : -1;
         for (int l = ws.depth - 1; l >= 0; --l) {
             LkArgs a = level_args(l);
             cudaStream_t st = l == l_chain ? s : ts;

@@ -97,6 +97,11 @@ struct FlowWS {
     // schedule marks (fs_plan_timeline_graph): called at every level start
     // ("L<l>") and after the last level ("flow_end") on the chain's stream
     std::function<void(const std::string&, cudaStream_t)> mark;
+    // split schedule: the coarsest level's tensor on the chain's own stream
+    // (set by the plan for folds that start with others: on the tensor
+    // stream it waited behind their side work, C2 3.381 -> 3.367 ms; a fold
+    // alone, C1, is faster with it beside the chain, 0.354 -> 0.337 ms)
+    bool tensor0_on_chain = false;
     void layout(Arena& a, int w, int h, int levels, int ndir);
 };
 

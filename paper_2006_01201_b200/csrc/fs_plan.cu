@@ -1316,7 +1316,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
                 // transforms at the flows' priority (C2 3.394 -> 3.382 ms)
                 bool first = !p->crop_wait[k + 1];
                 for (int m = 1; m < k + 1; ++m) first &= p->crop_wait[m] != 0;
-                if (first) p_side = greatest;
+                                if (first) p_side = greatest;
                 FS_CK(cudaStreamCreateWithPriority(&p->branch[k], cudaStreamNonBlocking, greatest));
                 FS_CK(cudaStreamCreateWithPriority(&p->edt_stream[k], cudaStreamNonBlocking,
                                                    p_side));
@@ -1370,6 +1370,11 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         layout_plan(p, a1, boxes);
         if (kLkSplit)
             for (auto& f : p->folds) flow_split_events(f.flow);
+        for (int k = 1; k < n; ++k) {  // folds released together with others
+            int together = 0;
+            for (int m = 1; m < n; ++m) together += p->crop_wait[m] == p->crop_wait[k];
+            p->folds[k - 1].flow.tensor0_on_chain = together > 1;
+        }
         if (views_rgba)
             for (int k = 0; k < n; ++k)
                 FS_CK(cudaMemcpy(p->views[k], views_rgba[k],
