@@ -26,14 +26,15 @@ constexpr size_t kMaxStamps = 512;
 #define FS_LK_SPLIT 1  // the level tensors off the chain (TENSOR), then fp32 FIRST + ITER
 #endif
 constexpr bool kLkSplit = FS_LK_SPLIT != 0;
-// RGB8 upload order: whole views in fold order (default), or every fold's
-// Area3 box parts first (pitched copies), then the rest.  Measured C2 e2e:
-// boxes first 5.81 ms vs whole views 4.97 ms (the pitched copies run at
-// ~36 GB/s, and the first-cover read-backs wait for the late "rest" chunks).
+// RGB8 upload order (plan_chunks): 0 = chosen per plan (crop parts first
+// when the folds bound the execution, else whole views), 1 = every fold's
+// Area3 box parts first, then the rest (measured C2 e2e 5.81 vs 4.97 ms:
+// the pitched copies run at ~36 GB/s and the first-cover read-backs wait
+// for the late "rest" chunks), 2 = crop parts first always.
 #ifndef FS_UPLOAD_BOXES
 #define FS_UPLOAD_BOXES 0
 #endif
-constexpr bool kUploadBoxesFirst = FS_UPLOAD_BOXES != 0;
+constexpr bool kUploadBoxesFirst = FS_UPLOAD_BOXES == 1;
 
 // first-cover copies a sharded rank keeps around each own fold's Area3 box:
 // a blend tap farther out is refused (ReachCheck) and the panorama runs unsharded
@@ -114,6 +115,11 @@ struct fs_plan_s {
         Rect r;  // canvas coordinates
     };
     std::vector<Chunk> chunks;
+    bool crop_first = false;  // plan_chunks' order (see there)
+    // %globaltimer when each view's last chunk was expanded: device-side
+    // telemetry, and the graph node it takes keeps the copy chain flowing
+    // (without one the crop-first order measured 5.1 instead of 4.0 ms, C2)
+    unsigned long long* landed = nullptr;
     std::vector<int> crop_chunk;  // per fold: last chunk its crop reads (-1: none)
     std::vector<int> done_chunk;  // per view k: last chunk of views 0..k
     std::vector<cudaEvent_t> ev_chunk, ev_copied;  // expanded / landed
@@ -258,12 +264,47 @@ void plan_chunks(fs_plan_s* p) {
         }
         rem[m] = keep;
     };
-    if (kUploadBoxesFirst)
+    // Crop parts first when the folds, not the link, bound the execution:
+    // then the folds that start at once (their flows need only their boxes'
+    // pixels) start a view's upload earlier, and the rest of every view
+    // follows in view order (the blends need whole views); a view whose
+    // fold's box spans whole rows of it sends those rows in its turn and the
+    // rest last (C2 e2e 4.55 -> 4.03 ms).  When the link bounds it (C4: 13.3
+    // vs 15.8 ms) the pitched crop-part copies only slow it down: whole views
+    // in fold order.  Estimate: ~0.3 ms per Mpx of Area3 boxes on the device
+    // vs the larger direction's bytes at ~50 GB/s.
+    double box_mpx = 0, in_b = 0, out_b = (double)p->cw * p->chh * p->ho_ch;
+    for (int k = 1; k < n; ++k) box_mpx += p->boxes[k].area() * 1e-6;
+    for (int m = 0; m < n; ++m) in_b += (double)p->rects[m].area() * 3;
+    p->crop_first = FS_UPLOAD_BOXES == 2 ||
+                    (FS_UPLOAD_BOXES == 0 && 0.3 * box_mpx > std::max(in_b, out_b) / 50e6);
+    if (p->crop_first) {
         for (int k = 1; k < n; ++k)
-            for (int m = k; m >= 0; --m) carve(m, p->boxes[k]);
-    for (int m = 0; m < n; ++m)
-        for (const Rect& r : rem[m])
-            if (r.w > 0 && r.h > 0) p->chunks.push_back({m, r});
+            if (!p->crop_wait[k])
+                for (int m = k; m >= 0; --m) carve(m, p->boxes[k]);
+        std::vector<std::pair<int, Rect>> late;
+        for (int m = 0; m < n; ++m) {
+            const Rect& v = p->rects[m];
+            const Rect b = m >= 1 && p->crop_wait[m] ? rect_inter(v, p->boxes[m]) : Rect{};
+            const bool rows = b.w == v.w && b.h > 0 && b.h < v.h;
+            if (rows) carve(m, b);
+            for (const Rect& r : rem[m])
+                if (r.w > 0 && r.h > 0) {
+                    if (rows)
+                        late.push_back({m, r});
+                    else
+                        p->chunks.push_back({m, r});
+                }
+        }
+        for (const auto& c : late) p->chunks.push_back({c.first, c.second});
+    } else {
+        if (kUploadBoxesFirst)
+            for (int k = 1; k < n; ++k)
+                for (int m = k; m >= 0; --m) carve(m, p->boxes[k]);
+        for (int m = 0; m < n; ++m)
+            for (const Rect& r : rem[m])
+                if (r.w > 0 && r.h > 0) p->chunks.push_back({m, r});
+    }
     const int nc = (int)p->chunks.size();
     p->crop_chunk.assign(n, -1);
     p->done_chunk.assign(n, -1);
@@ -437,8 +478,10 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
                     FS_CK(cudaStreamWaitEvent(p->xst, p->ev_copied[i], 0));
                     expand_chunk(p, c.view, c.r, p->xst);
                     FS_CK(cudaEventRecord(p->ev_chunk[i], p->xst));
-                    while (next < p->n && p->done_chunk[next] == i)
+                    while (next < p->n && p->done_chunk[next] == i) {
+                        launch::stamp(p->landed + next, p->xst);
                         mark("h2d_" + std::to_string(next++), p->xst);
+                    }
                 }
                 FS_CK(cudaEventRecord(p->ev_h2d[p->n - 1], p->xst));  // joined at the end
             } else {
@@ -1365,6 +1408,7 @@ fs_status fs_plan_create(fs_plan* out, int device, int n, const int* dims, const
         Arena a0;
         layout_plan(p, a0, boxes);
         FS_CK(cudaMalloc(&p->arena, a0.off));
+        FS_CK(cudaMalloc(&p->landed, sizeof(unsigned long long) * n));
         Arena a1;
         a1.base = p->arena;
         layout_plan(p, a1, boxes);
@@ -1417,6 +1461,7 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
             for (int k = 0; k < p->n; ++k)
                 launch::set_alpha(p->views[k], (size_t)p->rects[k].w * p->rects[k].h, nullptr);
             FS_CK(cudaDeviceSynchronize());
+            p->ho_ch = out_channels;  // the chunk order weighs the read-back bytes
             if (p->dag) plan_chunks(p);
         }
         p->hv_ch = view_channels;
@@ -1992,6 +2037,7 @@ void fs_plan_destroy(fs_plan p) {
     if (p->arena) cudaFree(p->arena);
     if (p->hstats) cudaFreeHost(p->hstats);
     if (p->stamps) cudaFree(p->stamps);
+    if (p->landed) cudaFree(p->landed);
     if (p->stage_in) cudaFree(p->stage_in);
     if (p->stage_out) cudaFree(p->stage_out);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
