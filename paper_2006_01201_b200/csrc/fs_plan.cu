@@ -278,6 +278,12 @@ void plan_chunks(fs_plan_s* p) {
     for (int m = 0; m < n; ++m) in_b += (double)p->rects[m].area() * 3;
     p->crop_first = FS_UPLOAD_BOXES == 2 ||
                     (FS_UPLOAD_BOXES == 0 && 0.3 * box_mpx > std::max(in_b, out_b) / 50e6);
+    // test hook (tests/test_gpu_parity.py): FS_UPLOAD_ORDER=crop|views forces
+    // the order, so both are checked on the same layout
+    if (const char* o = getenv("FS_UPLOAD_ORDER")) {
+        if (!strcmp(o, "crop")) p->crop_first = true;
+        if (!strcmp(o, "views")) p->crop_first = false;
+    }
     if (p->crop_first) {
         for (int k = 1; k < n; ++k)
             if (!p->crop_wait[k])

@@ -769,13 +769,18 @@ def test_gpu_matches_golden_vectors(fs):
         assert np.array_equal(lv.data[..., 0], g["pyr_l%d" % k])
 
 
-@pytest.mark.parametrize("which", ["panorama", "gaps"])
-def test_plan_rgb8_host_formats(fs, which):
+@pytest.mark.parametrize("order", ["crop", "views"])
+@pytest.mark.parametrize("which", ["panorama", "gaps", "c2"])
+def test_plan_rgb8_host_formats(fs, which, order, monkeypatch):
     """RGB8 host views (alpha implicit) and an RGB8 host canvas give the RGBA8
     path's panorama (its RGB channels), through the overlapped graph
-    (page-locked) and the copy / graph / copy path (pageable)."""
+    (page-locked) and the copy / graph / copy path (pageable), with either
+    upload order of plan_chunks (the first folds' crop parts first, or whole
+    views; FS_UPLOAD_ORDER forces it)."""
     import torch
-    lay = S.small_panorama(seed=2) if which == "panorama" else _gaps_layout()
+    monkeypatch.setenv("FS_UPLOAD_ORDER", order)
+    lay = {"panorama": lambda: S.small_panorama(seed=2), "gaps": _gaps_layout,
+           "c2": lambda: S.c2_panorama(3)}[which]()
     assert all((v[..., 3] == 255).all() for v in lay.views)
     plan = fs.Plan(lay.dims, lay.offsets, lay.canvas_w, lay.canvas_h, fs.FlowParams(levels=3))
     ref = np.empty((lay.canvas_h, lay.canvas_w, 4), np.uint8)
