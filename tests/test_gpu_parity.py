@@ -674,6 +674,16 @@ def test_plan_crop_waits_for_last_meeting_box(fs, oracle):
         assert diff.max() <= 1 and np.mean(diff == 0) >= 0.999
     tl = plan.timeline()  # the schedule diagnostics run on this layout too
     assert tl["end"] >= tl["fold3_compose_end"] >= tl["fold3_flow_start"] > 0
+    # inside the production graph: a stamp at every LK level of every fold,
+    # coarse to fine, between the fold's flow start and its blend
+    tg = plan.timeline_graph()
+    for k in range(1, plan.n):
+        levels = sorted((int(key.rsplit("_L", 1)[1]), t) for key, t in tg.items()
+                        if key.startswith("fold%d_L" % k))
+        assert levels and levels[0][0] == 0, (k, levels)
+        lv = [t for _, t in reversed(levels)]  # coarse to fine
+        assert tg["fold%d_flow_start" % k] <= lv[0] and lv == sorted(lv), (k, lv)
+        assert lv[-1] <= tg["fold%d_blend_start" % k] <= tg["fold%d_compose_end" % k]
     plan.close()
 
 
