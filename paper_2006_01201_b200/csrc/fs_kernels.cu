@@ -622,22 +622,38 @@ __global__ void k_edt_envelope(EdtJob<M> J0, EdtJob<M> J1, const FoldStats* st) 
     __syncwarp();
     int ne = 0;
     if (lane == 0) {
+        // the top two stack entries (site t over u) and their g = f + s^2 in
+        // registers, the next candidate's site and g loaded one step ahead:
+        // a pop reads one entry back, a push writes one (the same exact int64
+        // comparisons as the textbook loop)
+        int t = 0, u = 0;
+        long long gt = 0, gu = 0;
+        int qn = n > 0 ? stk[0] : 0;
+        long long fn = n > 0 ? f[qn] : 0;
         for (int i = 0; i < n; ++i) {
-            const int q = stk[i];
-            const long long fq = f[q];
+            const int q = qn;
+            const long long gq = fn + (long long)q * q;
+            if (i + 1 < n) {
+                qn = stk[i + 1];
+                fn = f[qn];
+            }
             while (ne >= 2) {
-                const int t = stk[ne - 1], u = stk[ne - 2];
-                const long long ft = f[t], fu = f[u];
-                const long long n1 = (fq + (long long)q * q) - (ft + (long long)t * t);
-                const long long d1 = 2LL * (q - t);
-                const long long n2 = (ft + (long long)t * t) - (fu + (long long)u * u);
-                const long long d2 = 2LL * (t - u);
-                if (n1 * d2 <= n2 * d1)
-                    --ne;
-                else
-                    break;
+                const long long n1 = gq - gt, d1 = 2LL * (q - t);
+                const long long n2 = gt - gu, d2 = 2LL * (t - u);
+                if (n1 * d2 > n2 * d1) break;
+                --ne;  // t is hidden: u becomes the top
+                t = u;
+                gt = gu;
+                if (ne >= 2) {
+                    u = stk[ne - 2];
+                    gu = (long long)f[u] + (long long)u * u;
+                }
             }
             stk[ne++] = q;
+            u = t;
+            gu = gt;
+            t = q;
+            gt = gq;
         }
     }
     ne = __shfl_sync(0xffffffffu, ne, 0);
