@@ -41,12 +41,18 @@ def raw(path):
                 i = hdr.index(m)
                 d[k] = (vals[i], units[i])
         stalls = []
-        for i, h in enumerate(hdr):
-            if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio"):
-                try:
-                    stalls.append((float(vals[i]), h[len("smsp__average_warp_latency_issue_stalled_"):-6]))
-                except ValueError:
-                    pass
+        # warps stalled per issue-active cycle, by reason (this ncu's names;
+        # older versions: smsp__average_warp_latency_issue_stalled_*)
+        for pre, post in (("smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"),
+                          ("smsp__average_warp_latency_issue_stalled_", ".ratio")):
+            for i, h in enumerate(hdr):
+                if h.startswith(pre) and h.endswith(post):
+                    try:
+                        stalls.append((float(vals[i].replace(",", "")), h[len(pre):-len(post)]))
+                    except ValueError:
+                        pass
+            if stalls:
+                break
         stalls.sort(reverse=True)
         d["top_stalls_cycles_per_issue"] = [(n, round(v, 2)) for v, n in stalls[:6]]
         res.append(d)
