@@ -97,8 +97,12 @@ __device__ __forceinline__ float u8f(unsigned int word, int byte) {
 struct ViewU8 {
     const uchar4* px;
     Rect rect;  // canvas placement
+    // every pixel valid (a plan's RGB8 host views: alpha preset to 255), so
+    // validity is the placement alone and needs no load
+    int all_valid = 0;
     __device__ __forceinline__ bool valid_at(int x, int y) const {
         if (!rect.contains(x, y)) return false;
+        if (all_valid) return true;
         return px[(size_t)(y - rect.y0) * rect.w + (x - rect.x0)].w >= 128;
     }
     __device__ __forceinline__ float4 value_at(int x, int y) const {

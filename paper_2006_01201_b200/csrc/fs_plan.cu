@@ -195,7 +195,14 @@ Rect rect_inter(const Rect& a, const Rect& b) {
     return Rect{x0, y0, std::max(0, x1 - x0), std::max(0, y1 - y0)};
 }
 
-ViewU8 view_of(const fs_plan_s* p, int k) { return ViewU8{p->views[k], p->rects[k]}; }
+ViewU8 view_of(const fs_plan_s* p, int k) {
+#ifdef FS_NO_ALL_VALID
+    return ViewU8{p->views[k], p->rects[k]};
+#else
+    // RGB8 host views are valid everywhere (fs_plan_set_host_format)
+    return ViewU8{p->views[k], p->rects[k], p->hv_ch == 3 ? 1 : 0};
+#endif
+}
 
 PanoViews views_before(const fs_plan_s* p, int k) {
     PanoViews pv{};
@@ -1472,13 +1479,9 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
         }
         p->hv_ch = view_channels;
         p->ho_ch = out_channels;
-        // the graphs holding host copies were captured for the old formats
-        if (p->hexec) cudaGraphExecDestroy(p->hexec);
-        if (p->hgraph) cudaGraphDestroy(p->hgraph);
-        p->hexec = nullptr;
-        p->hgraph = nullptr;
-        p->hkey.clear();
-        drop_shard_graphs(p);
+        // the graphs were captured for the old formats (the host copies; the
+        // views' validity: RGB8 views are valid everywhere)
+        drop_graph(p);
     });
 }
 
