@@ -327,9 +327,12 @@ template <class V> void union_valid(const Canvas&, const V&, cudaStream_t);
 // (hist: += the pixels claimed, at hist[k])
 void claim_owner(uint8_t* owner, int w, const ViewU8& view, int k, cudaStream_t,
                  unsigned long long* hist = nullptr);
-// out != nullptr: also the RGBA8 value of every valid pixel written
+// out != nullptr: also the RGBA8 value of every valid pixel written;
+// write_cv false: the float canvas is not written (the DAG's first-cover
+// pixels are read from the views, blend_area3's first_cover)
 template <class V>
-void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t, uchar4* out = nullptr);
+void place_view(const Canvas&, const V&, CanvasCount*, cudaStream_t, uchar4* out = nullptr,
+                bool write_cv = true);
 template <class V, class P> void partition(const P&, const V&, FoldStats*, cudaStream_t);
 void snapshot_count(FoldStats* st, const CanvasCount* cc, cudaStream_t);  // pv_count = cc
 void check_box(FoldStats*, const Rect&, cudaStream_t);
@@ -350,7 +353,8 @@ void edt(const EdtJob<M>&, const EdtJob<M>&, const FoldStats*, cudaStream_t);
 template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
                  const int*, FoldStats*, double, double, float4*, float2*,
-                 const uint8_t* owner, int fold, cudaStream_t, const ReachCheck* rc = nullptr);
+                 const uint8_t* owner, int fold, cudaStream_t, const ReachCheck* rc = nullptr,
+                 const PanoViews* first_cover = nullptr);
 template <class V>
 void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
                    uchar4* out = nullptr, const Rect* clip = nullptr,

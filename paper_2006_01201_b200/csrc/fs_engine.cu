@@ -639,14 +639,14 @@ int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s)
 template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
                        const fs_blend_params& bp, cudaStream_t s, const uint8_t* owner, int fold,
-                       uchar4* out, const ReachCheck* rc) {
+                       uchar4* out, const ReachCheck* rc, const PanoViews* first_cover) {
     int launches = 0;
     {
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
         ProfScope ps("blend", 61.0 * f.box.area(), s);
         launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
                             f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, f.wgray,
-                            owner, fold, s, rc);
+                            owner, fold, s, rc, first_cover);
     }
     if (owner) {  // Area3 only: the fold's Area2 was copied on its branch
         ProfScope ps("compose", 21.0 * f.box.area(), s);  // owner 1 + view 4 + blended 16
@@ -692,9 +692,11 @@ template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoView
                                                  cudaStream_t);
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t,
-                                        const uint8_t*, int, uchar4*, const ReachCheck*);
+                                        const uint8_t*, int, uchar4*, const ReachCheck*,
+                                        const PanoViews*);
 template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t,
-                                        const uint8_t*, int, uchar4*, const ReachCheck*);
+                                        const uint8_t*, int, uchar4*, const ReachCheck*,
+                                        const PanoViews*);
 
 }  // namespace fs

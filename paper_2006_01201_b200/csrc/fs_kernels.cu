@@ -38,7 +38,7 @@ __device__ __forceinline__ uchar4 quantize_px(float4 v, int ch) {
 // writer of a pixel leaves its final 8-bit value.
 template <class V>
 __global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCount* count,
-                                                    uchar4* __restrict__ out) {
+                                                    uchar4* __restrict__ out, int write_cv) {
     __shared__ int red[8];
     const int x = view.rect.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int ya = view.rect.y0 + blockIdx.y * PART_ROWS;
@@ -49,8 +49,10 @@ __global__ void __launch_bounds__(256) k_place_view(Canvas cv, V view, CanvasCou
             size_t p = (size_t)y * cv.w + x;
             bool v = view.valid_at(x, y);
             const float4 val = view.value_at(x, y);
-            cv.rgb[p] = val;
-            cv.valid[p] = v ? 1 : 0;
+            if (write_cv) {
+                cv.rgb[p] = val;
+                cv.valid[p] = v ? 1 : 0;
+            }
             if (out && v) out[p] = quantize_px(val, cv.ch);
             n += v;
         }
@@ -778,13 +780,16 @@ struct CanvasSampler {
 #ifndef BLEND_MINB
 #define BLEND_MINB 12  // 40 registers: 12 CTAs of 128 per SM (latency-bound gathers)
 #endif
-template <class V, class PV, int CH>
+// LS: the sampler of L (the panorama before the fold) — the canvas, or
+// (PanoHybrid) the first covering view's pixel where no earlier fold blended
+// and the canvas only where one did, so first-cover pixels need no float copy
+template <class V, class PV, int CH, class LS>
 __global__ void __launch_bounds__(128, BLEND_MINB) k_blend_area3(Canvas cv, PV pv, V view, Rect box,
                                                      const float2* __restrict__ flr,
                               const float2* __restrict__ frl, const int* __restrict__ d1,
                               const int* __restrict__ d2, FoldStats* st, double k,
                               double coef, float4* __restrict__ out, float2* __restrict__ wgray,
-                              const ReachCheck rc) {
+                              const ReachCheck rc, const LS L) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
@@ -796,7 +801,6 @@ __global__ void __launch_bounds__(128, BLEND_MINB) k_blend_area3(Canvas cv, PV p
     double blend_l = 1.0 - blend_r;
     float2 rl = frl[o], lr = flr[o];
     float cl[3], cr[3];
-    CanvasSampler<PV> L{cv.rgb, pv, cv.w};
     const double lx = x + rl.x * (1.0 - blend_l), ly = y + rl.y * (1.0 - blend_l);
     if (rc.on) {
         const BiTap t = bi_tap(cv.w, cv.h, lx, ly);
@@ -1006,9 +1010,10 @@ namespace launch {
 static inline dim3 row_grid(int w, int h, int bx = 256) { return dim3((w + bx - 1) / bx, h); }
 
 template <class V>
-void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s, uchar4* out) {
+void place_view(const Canvas& cv, const V& view, CanvasCount* count, cudaStream_t s, uchar4* out,
+                bool write_cv) {
     k_place_view<<<row_grid(view.rect.w, (view.rect.h + PART_ROWS - 1) / PART_ROWS), 256, 0, s>>>(
-        cv, view, count, out);
+        cv, view, count, out, write_cv ? 1 : 0);
 }
 template <class V, class P>
 void partition(const P& pano, const V& view, FoldStats* st, cudaStream_t s) {
@@ -1087,26 +1092,29 @@ template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
                  const float2* frl, const int* d1, const int* d2, FoldStats* st, double k,
                  double coef, float4* out, float2* wgray, const uint8_t* owner, int fold,
-                 cudaStream_t s, const ReachCheck* rc) {
+                 cudaStream_t s, const ReachCheck* rc, const PanoViews* first_cover) {
     const ReachCheck r = rc ? *rc : ReachCheck{};
     const dim3 g = row_grid(box.w, box.h, 128);
-    if (owner) {
+#define FS_BLEND(PVT, LSV)                                                                    \
+    do {                                                                                      \
+        if (cv.ch == 3)                                                                       \
+            k_blend_area3<V, PVT, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1, d2,   \
+                                                      st, k, coef, out, wgray, r, LSV);      \
+        else                                                                                  \
+            k_blend_area3<V, PVT, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1, d2,   \
+                                                      st, k, coef, out, wgray, r, LSV);      \
+    } while (0)
+    if (owner && first_cover) {
         const PanoOwnerBefore pv{owner, cv.w, fold};
-        if (cv.ch == 3)
-            k_blend_area3<V, PanoOwnerBefore, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
-                                                                 d2, st, k, coef, out, wgray, r);
-        else
-            k_blend_area3<V, PanoOwnerBefore, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
-                                                                 d2, st, k, coef, out, wgray, r);
+        FS_BLEND(PanoOwnerBefore, (PanoHybrid{*first_cover, PanoPlane{cv.valid, cv.rgb, cv.w}}));
+    } else if (owner) {
+        const PanoOwnerBefore pv{owner, cv.w, fold};
+        FS_BLEND(PanoOwnerBefore, (CanvasSampler<PanoOwnerBefore>{cv.rgb, pv, cv.w}));
     } else {
         const PanoValidPlane pv{cv.valid, cv.w};
-        if (cv.ch == 3)
-            k_blend_area3<V, PanoValidPlane, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
-                                                                d2, st, k, coef, out, wgray, r);
-        else
-            k_blend_area3<V, PanoValidPlane, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1,
-                                                                d2, st, k, coef, out, wgray, r);
+        FS_BLEND(PanoValidPlane, (CanvasSampler<PanoValidPlane>{cv.rgb, pv, cv.w}));
     }
+#undef FS_BLEND
 }
 template <class V>
 void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fold,
@@ -1245,9 +1253,9 @@ void export_float(const Canvas& cv, float* out, uint8_t* vout, cudaStream_t s) {
 // explicit instantiations
 template void union_valid<ViewU8>(const Canvas&, const ViewU8&, cudaStream_t);
 template void place_view<ViewU8>(const Canvas&, const ViewU8&, CanvasCount*, cudaStream_t,
-                                 uchar4*);
+                                 uchar4*, bool);
 template void place_view<ViewF4>(const Canvas&, const ViewF4&, CanvasCount*, cudaStream_t,
-                                 uchar4*);
+                                 uchar4*, bool);
 template void partition<ViewU8, PanoPlane>(const PanoPlane&, const ViewU8&, FoldStats*,
                                            cudaStream_t);
 template void partition<ViewU8, PanoViews>(const PanoViews&, const ViewU8&, FoldStats*,
@@ -1284,11 +1292,11 @@ template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, c
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t,
-                                  const ReachCheck*);
+                                  const ReachCheck*, const PanoViews*);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t,
-                                  const ReachCheck*);
+                                  const ReachCheck*, const PanoViews*);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,

@@ -463,6 +463,15 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     // RGB8 views in chunks (validity needs no data): ev_view[k] = views 0..k
     // complete, ev_crop[k] = fold k's crop inputs in
     const bool chunked = dag && hin && p->hv_ch == 3 && !p->chunks.empty();
+    // RGB8 views (valid everywhere): the blends read a first-cover pixel of L
+    // from its view, so the float canvas holds only blended pixels (the
+    // placement and Area2 copies write the RGBA8 output alone)
+#ifdef FS_NO_FIRST_COVER
+    const bool fc_mode = false;
+#else
+    const bool fc_mode = dag && p->hv_ch == 3;
+#endif
+    const Rect no_cv{0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_view(p->n, nullptr), ev_crop(p->n, nullptr);
     if (hin) {
         for (int k = 0; k < p->n; ++k) {
@@ -518,7 +527,7 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     }
     {
         ProfScope ps("place", 21.0 * p->rects[0].area(), s);  // view 4 in, rgb 16 + valid 1 out
-        launch::place_view(p->cv, view_of(p, 0), p->cc, s, dag ? p->out : nullptr);
+        launch::place_view(p->cv, view_of(p, 0), p->cc, s, dag ? p->out : nullptr, !fc_mode);
     }
     launches += 2;
     if (!dag) {
@@ -619,7 +628,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_own[k], 0));
         FS_CK(cudaStreamWaitEvent(a2s, p->ev_clear, 0));
         if (chunked) FS_CK(cudaStreamWaitEvent(a2s, ev_view[k], 0));  // view k's pixels
-        launch::compose_area2(p->cv, v, p->owner, k, a2s, p->out);
+        launch::compose_area2(p->cv, v, p->owner, k, a2s, p->out, nullptr,
+                              fc_mode ? &no_cv : nullptr);
         ++launches;
         FS_CK(cudaEventRecord(p->ev_a2[k], a2s));
         if (p->tl_stamp && p->crop_wait[k] == 0) mark("fold" + fk + "_flow_start", b);
@@ -695,7 +705,8 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         if (chunked) FS_CK(cudaStreamWaitEvent(s, ev_view[k], 0));  // L taps anywhere in views <= k
         mark("fold" + fk + "_blend_start", s);
-        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out);
+        launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out, nullptr,
+                                       fc_mode ? &pv : nullptr);
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
         mark("fold" + fk + "_compose_end", s);
     }
