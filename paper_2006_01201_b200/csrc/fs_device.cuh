@@ -363,7 +363,8 @@ void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cuda
 void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaStream_t);
 template <class V>
 void compose_area3(const Canvas&, const V&, const Rect& box, const float4*, const uint8_t* owner,
-                   int fold, cudaStream_t, uchar4* out = nullptr);
+                   int fold, cudaStream_t, uchar4* out = nullptr,
+                   bool write_cv = true);  // false: only `out` (no later fold reads the canvas)
 template <class V>
 void compose(const Canvas&, const V&, const Rect&, const float4*, CanvasCount*, const FoldStats*,
              cudaStream_t);

@@ -639,7 +639,8 @@ int fold_enqueue_edt(FoldWS<V>& f, const P& pano, const V& view, cudaStream_t s)
 template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
                        const fs_blend_params& bp, cudaStream_t s, const uint8_t* owner, int fold,
-                       uchar4* out, const ReachCheck* rc, const PanoViews* first_cover) {
+                       uchar4* out, const ReachCheck* rc, const PanoViews* first_cover,
+                       bool write_cv) {
     int launches = 0;
     {
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
@@ -650,7 +651,7 @@ int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCoun
     }
     if (owner) {  // Area3 only: the fold's Area2 was copied on its branch
         ProfScope ps("compose", 21.0 * f.box.area(), s);  // owner 1 + view 4 + blended 16
-        launch::compose_area3(cv, view, f.box, f.blended, owner, fold, s, out);
+        launch::compose_area3(cv, view, f.box, f.blended, owner, fold, s, out, write_cv);
         FS_CK(cudaGetLastError());
         return launches + 2;
     }
@@ -693,10 +694,10 @@ template int fold_enqueue_edt<ViewU8, PanoViews>(FoldWS<ViewU8>&, const PanoView
 template int fold_enqueue_blend<ViewU8>(FoldWS<ViewU8>&, const Canvas&, const ViewU8&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t,
                                         const uint8_t*, int, uchar4*, const ReachCheck*,
-                                        const PanoViews*);
+                                        const PanoViews*, bool);
 template int fold_enqueue_blend<ViewF4>(FoldWS<ViewF4>&, const Canvas&, const ViewF4&,
                                         CanvasCount*, const fs_blend_params&, cudaStream_t,
                                         const uint8_t*, int, uchar4*, const ReachCheck*,
-                                        const PanoViews*);
+                                        const PanoViews*, bool);
 
 }  // namespace fs

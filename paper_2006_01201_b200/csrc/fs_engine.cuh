@@ -199,7 +199,7 @@ template <class V>
 int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCount* cc,
                        const fs_blend_params& bp, cudaStream_t s, const uint8_t* owner = nullptr,
                        int fold = 0, uchar4* out = nullptr, const ReachCheck* rc = nullptr,
-                       const PanoViews* first_cover = nullptr);
+                       const PanoViews* first_cover = nullptr, bool write_cv = true);
 
 void init_stats(FoldStats* st, cudaStream_t s);
 void init_count(CanvasCount* cc, cudaStream_t s);

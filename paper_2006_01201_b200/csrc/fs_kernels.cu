@@ -900,14 +900,14 @@ __global__ void __launch_bounds__(256) k_compose_area2(Canvas cv, V view,
 template <class V>
 __global__ void k_compose_area3(Canvas cv, V view, Rect box, const float4* __restrict__ blended,
                                 const uint8_t* __restrict__ owner, int k,
-                                uchar4* __restrict__ out) {
+                                uchar4* __restrict__ out, int write_cv) {
     const int x = box.x0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int y = box.y0 + blockIdx.y;
     if (x >= box.x1()) return;
     const size_t p = (size_t)y * cv.w + x;
     if (owner[p] < k && view.valid_at(x, y)) {
         const float4 v = blended[(size_t)(y - box.y0) * box.w + (x - box.x0)];
-        cv.rgb[p] = v;
+        if (write_cv) cv.rgb[p] = v;
         if (out) out[p] = quantize_px(v, cv.ch);
     }
 }
@@ -1136,9 +1136,9 @@ void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaS
 }
 template <class V>
 void compose_area3(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
-                   const uint8_t* owner, int fold, cudaStream_t s, uchar4* out) {
+                   const uint8_t* owner, int fold, cudaStream_t s, uchar4* out, bool write_cv) {
     k_compose_area3<<<row_grid(box.w, box.h), 256, 0, s>>>(cv, view, box, blended, owner, fold,
-                                                          out);
+                                                          out, write_cv ? 1 : 0);
 }
 template <class V>
 void compose(const Canvas& cv, const V& view, const Rect& box, const float4* blended,
@@ -1286,9 +1286,9 @@ template void edt<LabelMask>(const EdtJob<LabelMask>&, const EdtJob<LabelMask>&,
 template void compose_area2<ViewU8>(const Canvas&, const ViewU8&, const uint8_t*, int,
                                     cudaStream_t, uchar4*, const Rect*, const Rect*);
 template void compose_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
-                                    const uint8_t*, int, cudaStream_t, uchar4*);
+                                    const uint8_t*, int, cudaStream_t, uchar4*, bool);
 template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
-                                    const uint8_t*, int, cudaStream_t, uchar4*);
+                                    const uint8_t*, int, cudaStream_t, uchar4*, bool);
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t,

@@ -515,14 +515,17 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
             }
         }
     }
-    {
+    if (!fc_mode) {  // (first-cover mode reads validity from the owner plane only)
         ProfScope ps("clear", (double)p->cw * p->chh, s);
         FS_CK(cudaMemsetAsync(p->cv.valid, 0, (size_t)p->cw * p->chh, s));
     }
     init_count(p->cc, s);
     if (hin) FS_CK(cudaStreamWaitEvent(s, ev_view[0], 0));
     if (dag) {
-        FS_CK(cudaMemsetAsync(p->out, 0, (size_t)p->cw * p->chh * 4, s));
+        // every pixel of a canvas the (valid everywhere) views cover is
+        // written by its writers: no clear of the output
+        if (!(fc_mode && p->empty_rects.empty()))
+            FS_CK(cudaMemsetAsync(p->out, 0, (size_t)p->cw * p->chh * 4, s));
         FS_CK(cudaEventRecord(p->ev_clear, s));
     }
     {
@@ -705,8 +708,10 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         FS_CK(cudaStreamWaitEvent(s, p->ev_branch[k], 0));
         if (chunked) FS_CK(cudaStreamWaitEvent(s, ev_view[k], 0));  // L taps anywhere in views <= k
         mark("fold" + fk + "_blend_start", s);
+        // (the last fold's blended pixels are read by no later fold: only the
+        // RGBA8 output is written for them in first-cover mode)
         launches += fold_enqueue_blend(f, p->cv, v, p->cc, p->bp, s, p->owner, k, p->out, nullptr,
-                                       fc_mode ? &pv : nullptr);
+                                       fc_mode ? &pv : nullptr, !(fc_mode && k == p->n - 1));
         FS_CK(cudaEventRecord(p->ev_compose[k], s));
         mark("fold" + fk + "_compose_end", s);
     }
