@@ -354,7 +354,8 @@ template <class V>
 void blend_area3(const Canvas&, const V&, const Rect&, const float2*, const float2*, const int*,
                  const int*, FoldStats*, double, double, float4*, float2*,
                  const uint8_t* owner, int fold, cudaStream_t, const ReachCheck* rc = nullptr,
-                 const PanoViews* first_cover = nullptr);
+                 const PanoViews* first_cover = nullptr,
+                 uchar4* canvas_out = nullptr);  // set: the RGBA8 canvas, not the box buffer
 template <class V>
 void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
                    uchar4* out = nullptr, const Rect* clip = nullptr,

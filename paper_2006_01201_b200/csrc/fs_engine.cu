@@ -642,12 +642,19 @@ int fold_enqueue_blend(FoldWS<V>& f, const Canvas& cv, const V& view, CanvasCoun
                        uchar4* out, const ReachCheck* rc, const PanoViews* first_cover,
                        bool write_cv) {
     int launches = 0;
+    // no later fold reads this fold's blended pixels (write_cv false): the
+    // blend writes the RGBA8 canvas itself and there is no compose
+    const bool direct = owner && out && !write_cv;
     {
         // pano rgb 16 + valid 1, view 4, two flows 16, two d^2 8 in; 16 out
         ProfScope ps("blend", 61.0 * f.box.area(), s);
         launch::blend_area3(cv, view, f.box, f.fvec[0], f.fvec[1], f.edt[0].out, f.edt[1].out,
                             f.st, bp.k_softmax_sharpness, bp.k_flow_mag_coef, f.blended, f.wgray,
-                            owner, fold, s, rc, first_cover);
+                            owner, fold, s, rc, first_cover, direct ? out : nullptr);
+    }
+    if (direct) {
+        FS_CK(cudaGetLastError());
+        return launches + 1;
     }
     if (owner) {  // Area3 only: the fold's Area2 was copied on its branch
         ProfScope ps("compose", 21.0 * f.box.area(), s);  // owner 1 + view 4 + blended 16

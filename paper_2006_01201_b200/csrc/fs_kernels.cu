@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(128, BLEND_MINB) k_blend_area3(Canvas cv, PV p
                               const float2* __restrict__ frl, const int* __restrict__ d1,
                               const int* __restrict__ d2, FoldStats* st, double k,
                               double coef, float4* __restrict__ out, float2* __restrict__ wgray,
-                              const ReachCheck rc, const LS L) {
+                              const ReachCheck rc, const LS L, uchar4* __restrict__ canvas_out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     int j = blockIdx.y;
     if (i >= box.w) return;
@@ -822,7 +822,11 @@ __global__ void __launch_bounds__(128, BLEND_MINB) k_blend_area3(Canvas cv, PV p
         double v = cl[c] * sl + cr[c] * sr;
         res[c] = (float)clampd(v, 0.0, 1.0);
     }
-    out[o] = make_float4(res[0], res[1], res[2], 0.f);
+    if (canvas_out)  // the fold's compose folded in: only the RGBA8 canvas (k_compose_area3)
+        canvas_out[(size_t)y * cv.w + x] =
+            quantize_px(make_float4(res[0], res[1], res[2], 0.f), cv.ch);
+    else
+        out[o] = make_float4(res[0], res[1], res[2], 0.f);
     if (wgray)  // gray of the warped constituents (warp_constituents, src/blender.cpp:150-158)
         wgray[o] = CH == 3 ? make_float2(gray3(cl[0], cl[1], cl[2]), gray3(cr[0], cr[1], cr[2]))
                            : make_float2(cl[0], cr[0]);
@@ -1092,17 +1096,20 @@ template <class V>
 void blend_area3(const Canvas& cv, const V& view, const Rect& box, const float2* flr,
                  const float2* frl, const int* d1, const int* d2, FoldStats* st, double k,
                  double coef, float4* out, float2* wgray, const uint8_t* owner, int fold,
-                 cudaStream_t s, const ReachCheck* rc, const PanoViews* first_cover) {
+                 cudaStream_t s, const ReachCheck* rc, const PanoViews* first_cover,
+                 uchar4* canvas_out) {
     const ReachCheck r = rc ? *rc : ReachCheck{};
     const dim3 g = row_grid(box.w, box.h, 128);
 #define FS_BLEND(PVT, LSV)                                                                    \
     do {                                                                                      \
         if (cv.ch == 3)                                                                       \
             k_blend_area3<V, PVT, 3><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1, d2,   \
-                                                      st, k, coef, out, wgray, r, LSV);      \
+                                                      st, k, coef, out, wgray, r, LSV,       \
+                                                      canvas_out);                            \
         else                                                                                  \
             k_blend_area3<V, PVT, 1><<<g, 128, 0, s>>>(cv, pv, view, box, flr, frl, d1, d2,   \
-                                                      st, k, coef, out, wgray, r, LSV);      \
+                                                      st, k, coef, out, wgray, r, LSV,       \
+                                                      canvas_out);                            \
     } while (0)
     if (owner && first_cover) {
         const PanoOwnerBefore pv{owner, cv.w, fold};
@@ -1292,11 +1299,11 @@ template void compose_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, c
 template void blend_area3<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t,
-                                  const ReachCheck*, const PanoViews*);
+                                  const ReachCheck*, const PanoViews*, uchar4*);
 template void blend_area3<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float2*,
                                   const float2*, const int*, const int*, FoldStats*, double,
                                   double, float4*, float2*, const uint8_t*, int, cudaStream_t,
-                                  const ReachCheck*, const PanoViews*);
+                                  const ReachCheck*, const PanoViews*, uchar4*);
 template void compose<ViewU8>(const Canvas&, const ViewU8&, const Rect&, const float4*,
                               CanvasCount*, const FoldStats*, cudaStream_t);
 template void compose<ViewF4>(const Canvas&, const ViewF4&, const Rect&, const float4*,
