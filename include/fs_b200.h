@@ -261,7 +261,10 @@ int fs_plan_launch_count(fs_plan plan);
 /* Host buffer formats of fs_plan_execute_host / fs_plan_shard_execute:
  * views RGBA8 (4, default) or RGB8 (3: every pixel valid, expanded to RGBA8
  * on the device), canvas RGBA8 (4, default) or RGB8 (3: alpha dropped, for
- * canvases the views cover completely).  Fewer bytes cross PCIe. */
+ * canvases the views cover completely).  Fewer bytes cross PCIe.  With RGB8
+ * views the plan also treats every view pixel as valid in the device-
+ * resident fs_plan_execute (a view's validity is its placement), so views
+ * written into fs_plan_view_buffer must then be fully valid as well. */
 fs_status fs_plan_set_host_format(fs_plan plan, int view_channels, int out_channels);
 /* bytes fs_plan_execute_host moves with page-locked buffers: views in, and
  * the canvas read back (rectangles no view covers are zeroed on the host) */
