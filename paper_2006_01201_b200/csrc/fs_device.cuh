@@ -360,7 +360,6 @@ template <class V>
 void compose_area2(const Canvas&, const V&, const uint8_t* owner, int fold, cudaStream_t,
                    uchar4* out = nullptr, const Rect* clip = nullptr,
                    const Rect* cv_clip = nullptr);  // float canvas written only inside cv_clip
-void restore_stats(FoldStats* st, const FoldStats* tmpl, cudaStream_t);
 // pv_count of fold k = sum of hist[m] over m < k
 void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaStream_t);
 template <class V>

@@ -149,17 +149,6 @@ __global__ void k_snapshot_count(FoldStats* st, const CanvasCount* cc) {
 
 // |pano valid| before fold k from the claims' counts (hist[m]: pixels first
 // covered by view m)
-// a fold's statistics restored from the ones computed with the format (RGB8
-// views: the partitions depend on the placements alone); the per-execution
-// flags start cleared
-__global__ void k_restore_stats(FoldStats* st, const FoldStats* tmpl) {
-    FoldStats v = *tmpl;
-    v.edt_fail = 0;
-    v.box_mismatch = 0;
-    v.reach_fail = 0;
-    v.tile_fail = 0;
-    *st = v;
-}
 __global__ void k_count_from_hist(FoldStats* st, const unsigned long long* hist, int k) {
     unsigned long long c = 0;
     for (int m = 0; m < k; ++m) c += hist[m];
@@ -1148,9 +1137,6 @@ void compose_area2(const Canvas& cv, const V& view, const uint8_t* owner, int fo
     const int bx = ((r.w + 3) / 4 + 1 + 255) / 256;
     const int by = std::min(r.h, std::max(1, 148 * 8 / bx));
     k_compose_area2<<<dim3(bx, by), 256, 0, s>>>(cv, view, owner, fold, out, r, cvr);
-}
-void restore_stats(FoldStats* st, const FoldStats* tmpl, cudaStream_t s) {
-    k_restore_stats<<<1, 1, 0, s>>>(st, tmpl);
 }
 void count_from_hist(FoldStats* st, const unsigned long long* hist, int k, cudaStream_t s) {
     k_count_from_hist<<<1, 1, 0, s>>>(st, hist, k);

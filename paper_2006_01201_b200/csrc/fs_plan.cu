@@ -119,7 +119,6 @@ struct fs_plan_s {
     // RGB8 views (valid everywhere): the owner plane and the claim counts are
     // a function of the placements, computed once when the format is set
     bool owner_static = false;
-    FoldStats* stats_static = nullptr;  // [n-1] the folds' partitions (owner_static)
     // %globaltimer when each view's last chunk was expanded: device-side
     // telemetry, and the graph node it takes keeps the copy chain flowing
     // (without one the crop-first order measured 5.1 instead of 4.0 ms, C2)
@@ -630,14 +629,9 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
         const PanoViews pv = views_before(p, k);
         const std::string fk = std::to_string(k);
         mark("fold" + fk + "_start", b);
-        if (fc_mode && p->owner_static && !hin) {  // the partition of the format's claims
-            launch::restore_stats(f.st, p->stats_static + (k - 1), b);
-            ++launches;
-        } else {
-            launches += fold_enqueue_pre(f, pv, v, b);
-            launch::count_from_hist(f.st, p->hist, k, b);  // claims < k are in
-            ++launches;
-        }
+        launches += fold_enqueue_pre(f, pv, v, b);
+        launch::count_from_hist(f.st, p->hist, k, b);  // claims < k are in
+        ++launches;
         // the fold's Area2 (the pixels view k covers first) is a copy of the
         // view: written on the fold's side stream, off the ordered chain and
         // ahead of its distance transforms, while the branch crops and flows
@@ -1519,16 +1513,6 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
             FS_CK(cudaMemsetAsync(p->hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->cap));
             for (int k = 0; k < p->n; ++k)
                 launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->cap, p->hist);
-            // and every fold's partition statistics (a function of the same)
-            if (!p->stats_static)
-                FS_CK(cudaMalloc(&p->stats_static, sizeof(FoldStats) * p->folds.size()));
-            for (int k = 1; k < p->n; ++k) {
-                FoldWS<ViewU8>& f = p->folds[k - 1];
-                fold_enqueue_pre(f, views_before(p, k), view_of(p, k), p->cap);
-                launch::count_from_hist(f.st, p->hist, k, p->cap);
-                FS_CK(cudaMemcpyAsync(p->stats_static + (k - 1), f.st, sizeof(FoldStats),
-                                      cudaMemcpyDeviceToDevice, p->cap));
-            }
             FS_CK(cudaStreamSynchronize(p->cap));
             p->owner_static = true;
         }
@@ -2100,7 +2084,6 @@ void fs_plan_destroy(fs_plan p) {
     if (p->hstats) cudaFreeHost(p->hstats);
     if (p->stamps) cudaFree(p->stamps);
     if (p->landed) cudaFree(p->landed);
-    if (p->stats_static) cudaFree(p->stats_static);
     if (p->stage_in) cudaFree(p->stage_in);
     if (p->stage_out) cudaFree(p->stage_out);
     if (p->shard.ev_seg) cudaEventDestroy(p->shard.ev_seg);
