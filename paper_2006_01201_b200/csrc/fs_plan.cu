@@ -116,9 +116,6 @@ struct fs_plan_s {
     };
     std::vector<Chunk> chunks;
     bool crop_first = false;  // plan_chunks' order (see there)
-    // RGB8 views (valid everywhere): the owner plane and the claim counts are
-    // a function of the placements, computed once when the format is set
-    bool owner_static = false;
     // %globaltimer when each view's last chunk was expanded: device-side
     // telemetry, and the graph node it takes keeps the copy chain flowing
     // (without one the crop-first order measured 5.1 instead of 4.0 ms, C2)
@@ -576,24 +573,15 @@ int enqueue_all(fs_plan_s* p, cudaStream_t s, bool dag, const HostIO* io = nullp
     mark("place", s);
     // the owner plane: views claimed in fold order as they land
     FS_CK(cudaStreamWaitEvent(p->own, p->ev_start, 0));
-    if (fc_mode && p->owner_static && !hin) {
-        // RGB8 views: the owner plane and the claims' counts depend on the
-        // placements alone and were computed with the format.  (Device-
-        // resident graph only: with the host copies in the graph, dropping
-        // the claims measured slower end to end, 4.04 -> 4.37 ms — as with
-        // the landing stamps, the copy schedule follows the node structure.)
-        for (int k = 0; k < p->n; ++k) FS_CK(cudaEventRecord(p->ev_own[k], p->own));
-    } else {
-        FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
-        // the claims count their pixels: |pano valid| before fold k is the sum
-        // of the counts of views < k (no chain through the earlier partitions)
-        FS_CK(cudaMemsetAsync(p->hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->own));
-        for (int k = 0; k < p->n; ++k) {
-            if (hin && !chunked) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
-            launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own, p->hist);
-            ++launches;
-            FS_CK(cudaEventRecord(p->ev_own[k], p->own));
-        }
+    FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->own));
+    // the claims count their pixels: |pano valid| before fold k is the sum of
+    // the counts of views < k (no chain through the earlier folds' partitions)
+    FS_CK(cudaMemsetAsync(p->hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->own));
+    for (int k = 0; k < p->n; ++k) {
+        if (hin && !chunked) FS_CK(cudaStreamWaitEvent(p->own, p->ev_h2d[k], 0));
+        launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->own, p->hist);
+        ++launches;
+        FS_CK(cudaEventRecord(p->ev_own[k], p->own));
     }
     // the read-backs: quantise (and copy) every rectangle once final
     // (the RGBA8 canvas is written by each pixel's writers: copies only)
@@ -1507,15 +1495,6 @@ fs_status fs_plan_set_host_format(fs_plan p, int view_channels, int out_channels
         }
         p->hv_ch = view_channels;
         p->ho_ch = out_channels;
-        p->owner_static = false;
-        if (p->dag && view_channels == 3) {  // the claims of views valid everywhere, once
-            FS_CK(cudaMemsetAsync(p->owner, 0xFF, (size_t)p->cw * p->chh, p->cap));
-            FS_CK(cudaMemsetAsync(p->hist, 0, sizeof(unsigned long long) * kMaxDagViews, p->cap));
-            for (int k = 0; k < p->n; ++k)
-                launch::claim_owner(p->owner, p->cw, view_of(p, k), k, p->cap, p->hist);
-            FS_CK(cudaStreamSynchronize(p->cap));
-            p->owner_static = true;
-        }
         // the graphs were captured for the old formats (the host copies; the
         // views' validity: RGB8 views are valid everywhere)
         drop_graph(p);
