@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(256) k_claim_owner(uint8_t* __restrict__ owner
         for (int j = 0; j < 4; ++j) {
             const long long x = (long long)(f + j) - (long long)row;
             if (x >= view.rect.x0 && x < view.rect.x1() && b[j] == 0xFF &&
-                src[x - view.rect.x0].w >= 128) {
+                (view.all_valid || src[x - view.rect.x0].w >= 128)) {
                 b[j] = (uint8_t)k;
                 ++c;
             }
